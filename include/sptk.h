@@ -1,0 +1,142 @@
+/*
+ * sptk.h -- C ABI of the B200-native stochastic sparse-Tucker SGD library
+ * (libsptk.so, built for sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/pkg/src/sptucker).  The reference's Python driver
+ * trainer.train (trainer.py:150-271) calls two numba kernels and numpy's
+ * Generator; each of those is replaced here by a C entry point that a ctypes
+ * binding (paper_2204_07104_b200/_lib.py) calls with
+ * device pointers (torch tensors' data_ptr()) and a cudaStream_t:
+ *
+ *   _loops.factor_pass(idx, vals, visit, fac, foff, cor, coff, jr, rcore,
+ *                      gammas, lambdas) -> 0            (_loops.py:17-18)
+ *       -> sptk_factor_pass / sptk_factor_pass_f64
+ *   _loops.core_pass(idx, vals, visit, fac, foff, cor, coff, jr, rcore,
+ *                    acc, aoff) -> 0                     (_loops.py:66-67)
+ *       -> sptk_core_pass / sptk_core_pass_f64 (aoff == coff, as at
+ *          trainer.py:226-230), then the merge+apply of trainer.py:238-247
+ *       -> sptk_core_apply / sptk_core_apply_f64
+ *   np.random.default_rng([seed,1,t,*block]).permutation(len(ids))
+ *                                                        (trainer.py:300-303)
+ *       -> sptk_pcg64_seed + sptk_permutation
+ *   np.random.default_rng([seed,2,t]).choice(nnz, k, replace=False)
+ *                                                        (trainer.py:317-324)
+ *       -> sptk_pcg64_seed + sptk_choice
+ *   build_partition(tensor, m)                           (partition.py:47-81)
+ *       -> sptk_partition (+ the device re-layout of the COO data)
+ *   predict_entries / rmse / mae          (model.py:134-146, trainer.py:89-102)
+ *       -> sptk_eval / sptk_eval_f64
+ *
+ * Conventions
+ *   - d_* arguments are device pointers, h_* arguments are host pointers.
+ *   - `stream` is a cudaStream_t (0 = legacy default stream).
+ *   - Nonzeros live on the device as packed records: `rw` 32-bit words per
+ *     nonzero, {i_0..i_{N-1} (int32), value}; the value is fp32 at word N
+ *     (rw = 4/8/16 for N <= 3/7/15) or, for the fp64 verification entry points,
+ *     an fp64 at word (N+1)&~1 (rw from sptk_record_words(N, 1)).  This packs
+ *     the reference's (idx int64 [nnz,N], vals f64 [nnz]) pair so a gathered
+ *     nonzero is one 16/32-byte load.
+ *   - Model layout is the reference's (_loops.py:8-10): A(n) row i at
+ *     fac[h_foff[n] + i*h_jr[n]], B(n)[j][r] at cor[h_coff[n] + j*rcore + r].
+ *   - Every function returns 0 on success and nonzero on failure;
+ *     sptk_last_error() describes the last failure.  The library never
+ *     allocates device memory: callers pass workspaces sized by *_ws_bytes.
+ */
+#ifndef SPTK_H
+#define SPTK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- introspection ---------------------------------------------------- */
+const char* sptk_last_error(void);
+int sptk_version(void);
+long long sptk_launch_count(void);
+void sptk_reset_launch_count(void);
+int sptk_record_words(int order, int f64_records);
+
+/* ---- K2: samplers (bit-exact with numpy 2.x Generator/PCG64) ----------- */
+/* default_rng(entropy).bit_generator state: {state_hi, state_lo, inc_hi, inc_lo}
+ * (SeedSequence(entropy) -> PCG64 seeding), computed on the host. */
+int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_out[4]);
+size_t sptk_permutation_ws_bytes(long long n);
+/* d_out[n] (int32) = Generator.permutation(n) for the generator in h_state. */
+int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, void* d_ws, size_t ws_bytes,
+                     void* stream);
+/* test hook: the Fisher-Yates index sequence j_i (i = 1..n-1) of permutation(n). */
+int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,
+                       void* stream);
+size_t sptk_choice_ws_bytes(long long pop, long long k);
+/* d_out[k] = Generator.choice(pop, k, replace=False).  shuffle=0 returns the
+ * same set without the final _shuffle_int (the core phase only needs the
+ * set).  *h_path_out = 1 (tail shuffle) or 2 (Floyd). */
+int sptk_choice(const uint64_t h_state[4], long long pop, long long k, int shuffle, int32_t* d_out, void* d_ws,
+                size_t ws_bytes, int* h_path_out, void* stream);
+/* raw buffered 32-bit draws at stream positions q0..q0+n-1 (test hook). */
+int sptk_u32_stream(const uint64_t h_state[4], unsigned long long q0, long long n, uint32_t* d_out, void* stream);
+
+/* ---- K1: partition + device layout ------------------------------------ */
+size_t sptk_partition_ws_bytes(long long nnz, int order, long long m);
+/* d_idx int64 [nnz, order], d_vals f64 [nnz] -> d_rec (block-grouped records),
+ * d_ids[nnz] (source id of each record: the concatenated block_entries),
+ * d_pos_of_id[nnz] (inverse), d_block_off[m^order + 1] (record offset of each
+ * block key).  Any of d_ids / d_pos_of_id may be NULL. */
+int sptk_partition(const int64_t* d_idx, const double* d_vals, long long nnz, int order, const int64_t* h_dims,
+                   long long m, int f64_records, int32_t* d_rec, int32_t* d_ids, int32_t* d_pos_of_id,
+                   int32_t* d_block_off, void* d_ws, size_t ws_bytes, void* stream);
+int sptk_pack_records(const int64_t* d_idx, const double* d_vals, long long nnz, int order, int f64_records,
+                      int32_t* d_rec, void* stream);
+
+/* ---- K3: factor-row SGD (one pass over a visit list) ------------------- */
+/* record index of the k-th visited sample = base + d_visit[k] (d_visit may be
+ * NULL: k).  mode 0 = throughput (Hogwild, visit order), 1 = deterministic
+ * (strictly sequential, reference operation order). */
+int sptk_factor_pass(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, long long base,
+                     float* d_fac, const int64_t* h_foff, const float* d_cor, const int64_t* h_coff,
+                     const int64_t* h_jr, int n_modes, int rcore, const double* h_gammas, const double* h_lambdas,
+                     int mode, void* stream);
+int sptk_factor_pass_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, long long base,
+                         double* d_fac, const int64_t* h_foff, const double* d_cor, const int64_t* h_coff,
+                         const int64_t* h_jr, int n_modes, int rcore, const double* h_gammas,
+                         const double* h_lambdas, int mode, void* stream);
+
+/* ---- K4/K5: core gradient + apply ------------------------------------- */
+size_t sptk_core_ws_bytes(const int64_t* h_jr, int n_modes, int rcore, int exact_chunks);
+/* d_acc (fp64, layout coff) += sum over visited samples.  sample id of the
+ * k-th entry = d_visit[k] (or k); record index = d_map[id] (or id).
+ * exact_chunks = 0: throughput reduction; > 0: verification mode, the visit
+ * list split like np.array_split(psi, exact_chunks), accumulated in order and
+ * merged in chunk order (trainer.py:221-240). */
+int sptk_core_pass(const int32_t* d_rec, int rw, const int32_t* d_visit, const int32_t* d_map, long long n_visit,
+                   const float* d_fac, const int64_t* h_foff, const float* d_cor, const int64_t* h_coff,
+                   const int64_t* h_jr, int n_modes, int rcore, double* d_acc, int exact_chunks, void* d_ws,
+                   size_t ws_bytes, void* stream);
+int sptk_core_pass_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, const int32_t* d_map,
+                       long long n_visit, const double* d_fac, const int64_t* h_foff, const double* d_cor,
+                       const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore, double* d_acc,
+                       int exact_chunks, void* d_ws, size_t ws_bytes, void* stream);
+/* B <- B - gamma_b * (acc/denom + lambda_b * B) over cor_size entries. */
+int sptk_core_apply(float* d_cor, const double* d_acc, int cor_size, double gamma_b, double lambda_b, double denom,
+                    void* stream);
+int sptk_core_apply_f64(double* d_cor, const double* d_acc, int cor_size, double gamma_b, double lambda_b,
+                        double denom, void* stream);
+
+/* ---- K6: predictions / RMSE / MAE ------------------------------------- */
+/* d_pred[m] (may be NULL) = predictions; d_sums[2] (may be NULL) +=
+ * {sum (x - x_hat)^2, sum |x - x_hat|} in fp64. */
+int sptk_eval(const int32_t* d_rec, int rw, long long m, const float* d_fac, const int64_t* h_foff,
+              const float* d_cor, const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore, float* d_pred,
+              double* d_sums, void* stream);
+int sptk_eval_f64(const int32_t* d_rec, int rw, long long m, const double* d_fac, const int64_t* h_foff,
+                  const double* d_cor, const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore,
+                  double* d_pred, double* d_sums, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPTK_H */

@@ -1,0 +1,251 @@
+// capi.cu -- extern "C" entry points (include/sptk.h) and the host-side
+// SeedSequence -> PCG64 seeding.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "../../include/sptk.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sptk {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+void count_launch(int n) { g_launches += n; }
+
+// numpy.random.bit_generator.SeedSequence (pool size 4) + PCG64 seeding
+// (pcg64_set_seed -> pcg_setseq_128_srandom_r).  Used by the reference at
+// trainer.py:300-302 and trainer.py:318 through np.random.default_rng.
+static uint32_t ss_hashmix(uint32_t v, uint32_t* hc) {
+  v ^= *hc;
+  *hc *= 0x931e8875u;
+  v *= *hc;
+  v ^= v >> 16;
+  return v;
+}
+static uint32_t ss_mix(uint32_t x, uint32_t y) {
+  uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+  r ^= r >> 16;
+  return r;
+}
+
+static int build_model_desc(ModelDesc* md, const int64_t* h_foff, const int64_t* h_coff, const int64_t* h_jr,
+                            int n_modes, int rcore) {
+  SPTK_REQUIRE(n_modes >= 2 && n_modes <= SPTK_MAX_MODES, "order must be in [2, %d]", SPTK_MAX_MODES);
+  SPTK_REQUIRE(rcore >= 1, "rcore must be >= 1");
+  md->n_modes = n_modes;
+  md->rcore = rcore;
+  int cs = 0;
+  for (int n = 0; n < n_modes; ++n) {
+    SPTK_REQUIRE(h_jr[n] >= 1 && h_jr[n] <= 4096, "j_ranks out of range");
+    md->jr[n] = (int)h_jr[n];
+    md->foff[n] = h_foff[n];
+    md->coff[n] = (int)h_coff[n];
+    cs += md->jr[n] * rcore;
+  }
+  md->cor_size = cs;
+  return 0;
+}
+
+}  // namespace sptk
+
+using namespace sptk;
+
+template <typename T>
+static int core_dispatch(const int32_t* d_rec, int rw, const int32_t* d_visit, const int32_t* d_map,
+                         long long n_visit, const T* d_fac, const int64_t* h_foff, const T* d_cor,
+                         const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore, double* d_acc,
+                         int exact_chunks, void* d_ws, size_t ws_bytes, void* stream) {
+  ModelDesc md;
+  if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
+  if (exact_chunks > 0)
+    return core_pass_exact<T>(d_rec, rw, d_visit, d_map, n_visit, exact_chunks, d_fac, d_cor, md, d_acc, d_ws,
+                              ws_bytes, (cudaStream_t)stream);
+  return core_pass<T>(d_rec, rw, d_visit, d_map, n_visit, d_fac, d_cor, md, d_acc, d_ws, ws_bytes,
+                      (cudaStream_t)stream);
+}
+
+extern "C" {
+
+const char* sptk_last_error(void) { return g_err; }
+int sptk_version(void) { return 100; }
+long long sptk_launch_count(void) { return g_launches.load(); }
+void sptk_reset_launch_count(void) { g_launches = 0; }
+int sptk_record_words(int order, int f64_records) { return rec_words_t(order, f64_records != 0); }
+
+int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_out[4]) {
+  uint32_t words[512];
+  int nw = 0;
+  for (int e = 0; e < n_entropy; ++e) {
+    uint64_t x = h_entropy[e];
+    if (x == 0) {
+      SPTK_REQUIRE(nw < 512, "entropy too long");
+      words[nw++] = 0;
+    }
+    while (x) {
+      SPTK_REQUIRE(nw < 512, "entropy too long");
+      words[nw++] = (uint32_t)(x & 0xffffffffu);
+      x >>= 32;
+    }
+  }
+  uint32_t pool[4];
+  uint32_t hc = 0x43b0d7e5u;
+  for (int i = 0; i < 4; ++i) pool[i] = ss_hashmix(i < nw ? words[i] : 0u, &hc);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], &hc));
+  for (int s = 4; s < nw; ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = ss_mix(pool[d], ss_hashmix(words[s], &hc));
+  uint32_t out[8];
+  uint32_t hb = 0x8b51f9ddu;
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i % 4];
+    v ^= hb;
+    hb *= 0x58f38dedu;
+    v *= hb;
+    v ^= v >> 16;
+    out[i] = v;
+  }
+  uint64_t v64[4];
+  for (int k = 0; k < 4; ++k) v64[k] = (uint64_t)out[2 * k] | ((uint64_t)out[2 * k + 1] << 32);
+  typedef unsigned __int128 u128;
+  const u128 mult = (((u128)0x2360ED051FC65DA4ULL) << 64) | (u128)0x4385DF649FCCF645ULL;
+  u128 initstate = ((u128)v64[0] << 64) | v64[1];
+  u128 initseq = ((u128)v64[2] << 64) | v64[3];
+  u128 inc = (initseq << 1) | 1u;
+  u128 state = 0;
+  state = state * mult + inc;
+  state += initstate;
+  state = state * mult + inc;
+  h_state_out[0] = (uint64_t)(state >> 64);
+  h_state_out[1] = (uint64_t)state;
+  h_state_out[2] = (uint64_t)(inc >> 64);
+  h_state_out[3] = (uint64_t)inc;
+  return 0;
+}
+
+size_t sptk_permutation_ws_bytes(long long n) { return perm_ws_bytes(n); }
+
+int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, void* d_ws, size_t ws_bytes,
+                     void* stream) {
+  return permutation(h_state, n, d_out, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,
+                       void* stream) {
+  return permutation_j(h_state, n, d_j, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t sptk_choice_ws_bytes(long long pop, long long k) { return choice_ws_bytes(pop, k); }
+
+int sptk_choice(const uint64_t h_state[4], long long pop, long long k, int shuffle, int32_t* d_out, void* d_ws,
+                size_t ws_bytes, int* h_path_out, void* stream) {
+  return choice(h_state, pop, k, shuffle, d_out, d_ws, ws_bytes, h_path_out, (cudaStream_t)stream);
+}
+
+int sptk_u32_stream(const uint64_t h_state[4], unsigned long long q0, long long n, uint32_t* d_out, void* stream) {
+  return u32_stream(h_state, q0, n, d_out, (cudaStream_t)stream);
+}
+
+size_t sptk_partition_ws_bytes(long long nnz, int order, long long m) { return partition_ws_bytes(nnz, order, m); }
+
+int sptk_partition(const int64_t* d_idx, const double* d_vals, long long nnz, int order, const int64_t* h_dims,
+                   long long m, int f64_records, int32_t* d_rec, int32_t* d_ids, int32_t* d_pos_of_id,
+                   int32_t* d_block_off, void* d_ws, size_t ws_bytes, void* stream) {
+  return partition((const long long*)d_idx, d_vals, nnz, order, (const long long*)h_dims, m, d_rec, d_ids,
+                   d_pos_of_id, d_block_off, d_ws, ws_bytes, (cudaStream_t)stream, f64_records);
+}
+
+int sptk_pack_records(const int64_t* d_idx, const double* d_vals, long long nnz, int order, int f64_records,
+                      int32_t* d_rec, void* stream) {
+  return pack_records((const long long*)d_idx, d_vals, nnz, order, d_rec, (cudaStream_t)stream, f64_records);
+}
+
+int sptk_factor_pass(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, long long base,
+                     float* d_fac, const int64_t* h_foff, const float* d_cor, const int64_t* h_coff,
+                     const int64_t* h_jr, int n_modes, int rcore, const double* h_gammas, const double* h_lambdas,
+                     int mode, void* stream) {
+  ModelDesc md;
+  if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
+  float g[SPTK_MAX_MODES], l[SPTK_MAX_MODES];
+  for (int n = 0; n < n_modes; ++n) {
+    g[n] = (float)h_gammas[n];
+    l[n] = (float)h_lambdas[n];
+  }
+  return factor_pass<float>(d_rec, rw, d_visit, n_visit, base, d_fac, d_cor, md, g, l, mode, (cudaStream_t)stream);
+}
+
+int sptk_factor_pass_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, long long base,
+                         double* d_fac, const int64_t* h_foff, const double* d_cor, const int64_t* h_coff,
+                         const int64_t* h_jr, int n_modes, int rcore, const double* h_gammas,
+                         const double* h_lambdas, int mode, void* stream) {
+  ModelDesc md;
+  if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
+  return factor_pass<double>(d_rec, rw, d_visit, n_visit, base, d_fac, d_cor, md, h_gammas, h_lambdas, mode,
+                             (cudaStream_t)stream);
+}
+
+size_t sptk_core_ws_bytes(const int64_t* h_jr, int n_modes, int rcore, int exact_chunks) {
+  size_t cs = 0;
+  for (int n = 0; n < n_modes; ++n) cs += (size_t)h_jr[n] * rcore;
+  size_t blocks = exact_chunks > 0 ? (size_t)exact_chunks : (size_t)148 * 4;
+  return blocks * cs * sizeof(double) + sizeof(long long) * (blocks + 2) + 1024;
+}
+
+int sptk_core_pass(const int32_t* d_rec, int rw, const int32_t* d_visit, const int32_t* d_map, long long n_visit,
+                   const float* d_fac, const int64_t* h_foff, const float* d_cor, const int64_t* h_coff,
+                   const int64_t* h_jr, int n_modes, int rcore, double* d_acc, int exact_chunks, void* d_ws,
+                   size_t ws_bytes, void* stream) {
+  return core_dispatch<float>(d_rec, rw, d_visit, d_map, n_visit, d_fac, h_foff, d_cor, h_coff, h_jr, n_modes,
+                              rcore, d_acc, exact_chunks, d_ws, ws_bytes, stream);
+}
+
+int sptk_core_pass_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, const int32_t* d_map,
+                       long long n_visit, const double* d_fac, const int64_t* h_foff, const double* d_cor,
+                       const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore, double* d_acc,
+                       int exact_chunks, void* d_ws, size_t ws_bytes, void* stream) {
+  return core_dispatch<double>(d_rec, rw, d_visit, d_map, n_visit, d_fac, h_foff, d_cor, h_coff, h_jr, n_modes,
+                               rcore, d_acc, exact_chunks, d_ws, ws_bytes, stream);
+}
+
+int sptk_core_apply(float* d_cor, const double* d_acc, int cor_size, double gamma_b, double lambda_b, double denom,
+                    void* stream) {
+  return core_apply<float>(d_cor, d_acc, cor_size, gamma_b, lambda_b, denom, (cudaStream_t)stream);
+}
+
+int sptk_core_apply_f64(double* d_cor, const double* d_acc, int cor_size, double gamma_b, double lambda_b,
+                        double denom, void* stream) {
+  return core_apply<double>(d_cor, d_acc, cor_size, gamma_b, lambda_b, denom, (cudaStream_t)stream);
+}
+
+int sptk_eval(const int32_t* d_rec, int rw, long long m, const float* d_fac, const int64_t* h_foff,
+              const float* d_cor, const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore, float* d_pred,
+              double* d_sums, void* stream) {
+  ModelDesc md;
+  if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
+  SPTK_REQUIRE(rw == rec_words_t(n_modes, false), "eval: record width mismatch");
+  return eval<float>(d_rec, rw, m, d_fac, d_cor, md, d_pred, d_sums, (cudaStream_t)stream);
+}
+
+int sptk_eval_f64(const int32_t* d_rec, int rw, long long m, const double* d_fac, const int64_t* h_foff,
+                  const double* d_cor, const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore,
+                  double* d_pred, double* d_sums, void* stream) {
+  ModelDesc md;
+  if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
+  SPTK_REQUIRE(rw == rec_words_t(n_modes, true), "eval_f64: record width mismatch");
+  return eval<double>(d_rec, rw, m, d_fac, d_cor, md, d_pred, d_sums, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+// common.cuh -- shared helpers for the sptk CUDA library (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef SPTK_MAX_MODES
+#define SPTK_MAX_MODES 16
+#endif
+
+namespace sptk {
+
+// Set by every entry point on failure; read through sptk_last_error().
+void set_error(const char* fmt, ...);
+// Counts kernels launched by this library (read through sptk_launch_count()).
+void count_launch(int n = 1);
+
+// Model layout shared by the factor / core / eval kernels.  This is the
+// reference's packing (_loops.py:8-10, trainer.py:135-141): A(n) row i at
+// fac[foff[n] + i*jr[n]], B(n)[j][r] at cor[coff[n] + j*rcore + r].
+struct ModelDesc {
+  int n_modes;
+  int rcore;
+  int jr[SPTK_MAX_MODES];
+  long long foff[SPTK_MAX_MODES];
+  int coff[SPTK_MAX_MODES];
+  int cor_size;  // sum_n jr[n] * rcore
+};
+
+// Nonzeros as packed AoS records of `rw` 32-bit words: idx[0..N) (int32)
+// followed by the value (fp32 bits).  rw = 4 for N <= 3, 8 for N <= 7,
+// 16 for N <= 15, so one record is one 16/32/64-byte aligned load.
+struct MDims {
+  long long d[SPTK_MAX_MODES];
+};
+
+struct RecDesc {
+  const int* rec;
+  int rw;
+};
+
+__host__ __device__ inline int rec_words(int n_modes) {
+  return n_modes <= 3 ? 4 : (n_modes <= 7 ? 8 : 16);
+}
+
+// fp64 records (verification mode): the value is a double at an even word
+// offset so that fp64 inputs reach the kernels unrounded.
+__host__ __device__ inline int rec_val_off(int n_modes, bool f64) {
+  return f64 ? ((n_modes + 1) & ~1) : n_modes;
+}
+__host__ __device__ inline int rec_words_t(int n_modes, bool f64) {
+  if (!f64) return rec_words(n_modes);
+  int need = rec_val_off(n_modes, true) + 2;
+  int w = 4;
+  while (w < need) w *= 2;
+  return w;
+}
+
+template <typename T>
+__device__ __forceinline__ T load_val(const int* rp, int vo);
+template <>
+__device__ __forceinline__ float load_val<float>(const int* rp, int vo) {
+  return __int_as_float(__ldg(rp + vo));
+}
+template <>
+__device__ __forceinline__ double load_val<double>(const int* rp, int vo) {
+  return __ldg(reinterpret_cast<const double*>(rp + vo));
+}
+
+}  // namespace sptk
+
+#define SPTK_CUDA_TRY(expr)                                                        \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      ::sptk::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,                \
+                        cudaGetErrorString(_e));                                   \
+      return 1;                                                                    \
+    }                                                                              \
+  } while (0)
+
+#define SPTK_CHECK_LAUNCH()                                                        \
+  do {                                                                             \
+    cudaError_t _e = cudaGetLastError();                                           \
+    if (_e != cudaSuccess) {                                                       \
+      ::sptk::set_error("%s:%d launch failed: %s", __FILE__, __LINE__,            \
+                        cudaGetErrorString(_e));                                   \
+      return 1;                                                                    \
+    }                                                                              \
+    ::sptk::count_launch();                                                        \
+  } while (0)
+
+#define SPTK_REQUIRE(cond, ...)                                                    \
+  do {                                                                             \
+    if (!(cond)) {                                                                 \
+      ::sptk::set_error(__VA_ARGS__);                                              \
+      return 2;                                                                    \
+    }                                                                              \
+  } while (0)

@@ -1,0 +1,271 @@
+// core.cu -- K4 (core-gradient reduction) and K5 (core apply).
+//
+// K4 restates _loops.core_pass (_loops.py:66-104): against a frozen model,
+//     acc[n][j][r] += (x_hat - x) * (prod_{n0!=n} c[n0,r]) * A(n)[i_n, j]
+// summed over the core batch Psi (trainer.py:212-237).  This is a
+// [J x |Psi|] . [|Psi| x R] reduction per mode.  Each CTA stages S samples at
+// a time in shared memory (phase 1: one thread per sample computes its c table,
+// residual and the coefficient vectors v_n[r] = resid * w_n[r]; phase 2: the
+// CTA's threads own (n,j,r) outputs and reduce sum_s a_n[s][j] * v_n[s][r]
+// over the staged samples), then writes one fp64 partial per CTA.  A second
+// kernel sums the partials in CTA order (deterministic, fp64) -- the
+// equivalent of the reference's chunk-order merge (trainer.py:238-240).
+//
+// EXACT = true is the verification mode: one CTA per reference chunk
+// (np.array_split of Psi), samples accumulated one at a time in order with
+// the reference's operation order and no FMA contraction, so that in fp64 the
+// per-chunk accumulators equal the reference's bit for bit.
+//
+// K5 restates trainer.py:241-247 / core_sgd.py:62-79:
+//     B(n) <- B(n) - gamma_b * (acc / denom + lambda_b * B(n)).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sptk {
+
+template <typename T>
+__device__ __forceinline__ T cmul(T a, T b);
+template <>
+__device__ __forceinline__ float cmul<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double cmul<double>(double a, double b) { return __dmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T cadd(T a, T b);
+template <>
+__device__ __forceinline__ float cadd<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double cadd<double>(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(256) core_pass_kernel(const int* __restrict__ rec, int rw, int vo,
+                                                        const int* __restrict__ visit, const int* __restrict__ map,
+                                                        long long n_visit, const T* __restrict__ fac,
+                                                        const T* __restrict__ cor, ModelDesc md, int S,
+                                                        double* __restrict__ partial, const long long* chunk_lo) {
+  extern __shared__ unsigned char smem_raw[];
+  T* Bs = reinterpret_cast<T*>(smem_raw);
+  const int N = md.n_modes, R = md.rcore, CS = md.cor_size;
+  int aoff[SPTK_MAX_MODES];
+  int tot = 0;
+  for (int n = 0; n < N; ++n) {
+    aoff[n] = tot;
+    tot += md.jr[n];
+  }
+  const int NR = N * R;
+  T* sa = Bs + ((CS + 3) & ~3);  // [S][tot]
+  T* sv = sa + (size_t)S * tot;  // [S][NR]
+  T* sc = sv + (size_t)S * NR;   // [S][NR] c tables
+  for (int i = threadIdx.x; i < CS; i += blockDim.x) Bs[i] = cor[i];
+  double* out = partial + (size_t)blockIdx.x * CS;
+  for (int o = threadIdx.x; o < CS; o += blockDim.x) out[o] = 0.0;
+  __syncthreads();
+  long long k_lo, k_hi, k_step;
+  if (EXACT) {
+    k_lo = chunk_lo[blockIdx.x];
+    k_hi = chunk_lo[blockIdx.x + 1];
+    k_step = S;
+  } else {
+    k_lo = (long long)blockIdx.x * S;
+    k_hi = n_visit;
+    k_step = (long long)gridDim.x * S;
+  }
+  for (long long kb = k_lo; kb < k_hi; kb += k_step) {
+    const int t = threadIdx.x;
+    const long long k = kb + t;
+    // phase 1
+    if (t < S) {
+      T* my_a = sa + (size_t)t * tot;
+      T* my_v = sv + (size_t)t * NR;
+      T* my_c = sc + (size_t)t * NR;
+      if (k < k_hi && (EXACT || k < n_visit)) {
+        long long s = visit ? (long long)__ldg(visit + k) : k;
+        long long ri = map ? (long long)__ldg(map + s) : s;
+        const int* rp = rec + ri * rw;
+        const T x = load_val<T>(rp, vo);
+        for (int n = 0; n < N; ++n) {
+          const int J = md.jr[n];
+          const T* row = fac + md.foff[n] + (long long)__ldg(rp + n) * J;
+          for (int j = 0; j < J; ++j) my_a[aoff[n] + j] = row[j];
+        }
+        for (int n0 = 0; n0 < N; ++n0) {
+          const int J = md.jr[n0];
+          for (int r = 0; r < R; ++r) {
+            T dot = 0;
+            for (int j = 0; j < J; ++j) dot = cadd(dot, cmul(my_a[aoff[n0] + j], Bs[md.coff[n0] + j * R + r]));
+            my_c[n0 * R + r] = dot;
+          }
+        }
+        T xhat = 0;
+        for (int r = 0; r < R; ++r) {
+          T p = 1;
+          for (int n0 = 0; n0 < N; ++n0) p = cmul(p, my_c[n0 * R + r]);
+          xhat = cadd(xhat, p);
+        }
+        const T resid = cadd(xhat, -x);
+        for (int n = 0; n < N; ++n)
+          for (int r = 0; r < R; ++r) {
+            T w = 1;
+            for (int n0 = 0; n0 < N; ++n0)
+              if (n0 != n) w = cmul(w, my_c[n0 * R + r]);
+            my_v[n * R + r] = cmul(resid, w);
+          }
+      } else {
+        for (int i = 0; i < tot; ++i) my_a[i] = 0;
+        for (int i = 0; i < NR; ++i) my_v[i] = 0;
+      }
+    }
+    __syncthreads();
+    // phase 2: thread owns outputs o; reduce over the staged samples in order
+    int nval = S;
+    if (kb + S > k_hi) nval = (int)(k_hi - kb);
+    for (int o = threadIdx.x; o < CS; o += blockDim.x) {
+      int n = 0;
+      while (n + 1 < N && o >= md.coff[n + 1]) ++n;
+      const int rel = o - md.coff[n];
+      const int j = rel / R, r = rel % R;
+      if (EXACT) {
+        double acc = out[o];
+        for (int s2 = 0; s2 < nval; ++s2)
+          acc = cadd<double>(acc, cmul<double>((double)sv[(size_t)s2 * NR + n * R + r],
+                                               (double)sa[(size_t)s2 * tot + aoff[n] + j]));
+        out[o] = acc;
+      } else {
+        T acc = 0;
+        for (int s2 = 0; s2 < nval; ++s2)
+          acc += sv[(size_t)s2 * NR + n * R + r] * sa[(size_t)s2 * tot + aoff[n] + j];
+        out[o] += (double)acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void core_reduce_kernel(const double* __restrict__ partial, int nblocks, int CS, double* __restrict__ acc) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < CS; o += gridDim.x * blockDim.x) {
+    double t = acc[o];
+    for (int b = 0; b < nblocks; ++b) t = __dadd_rn(t, partial[(size_t)b * CS + o]);
+    acc[o] = t;
+  }
+}
+
+// total = acc_0 + acc_1 + ... (reference merge order) for the EXACT path
+__global__ void core_reduce_ordered_kernel(const double* __restrict__ partial, int nblocks, int CS,
+                                           double* __restrict__ acc) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < CS; o += gridDim.x * blockDim.x) {
+    double t = partial[o];
+    for (int b = 1; b < nblocks; ++b) t = __dadd_rn(t, partial[(size_t)b * CS + o]);
+    acc[o] = __dadd_rn(acc[o], t);
+  }
+}
+
+size_t core_ws_bytes(const ModelDesc& md) {
+  // partials for up to 148*4 CTAs
+  return (size_t)148 * 4 * md.cor_size * sizeof(double) + 4096;
+}
+
+static int pick_S(const ModelDesc& md, size_t elem, int* S_out, size_t* smem_out) {
+  int tot = 0;
+  for (int n = 0; n < md.n_modes; ++n) tot += md.jr[n];
+  const int NR = md.n_modes * md.rcore;
+  size_t fixed = elem * (size_t)((md.cor_size + 3) & ~3);
+  size_t per = elem * (size_t)(tot + 2 * NR);
+  int S = 256;
+  while (S > 1 && fixed + per * S > 200 * 1024) S /= 2;
+  *S_out = S;
+  *smem_out = fixed + per * S;
+  return fixed + per * S <= 200 * 1024;
+}
+
+template <typename T>
+int core_pass(const int* rec, int rw, const int* visit, const int* map, long long n_visit, const T* fac,
+              const T* cor, const ModelDesc& md, double* acc, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (n_visit <= 0) return 0;
+  const bool f64 = sizeof(T) == 8;
+  SPTK_REQUIRE(rw == rec_words_t(md.n_modes, f64), "core_pass: record width mismatch");
+  int S;
+  size_t smem;
+  SPTK_REQUIRE(pick_S(md, sizeof(T), &S, &smem), "core_pass: model ranks too large");
+  long long blocks = (n_visit + S - 1) / S;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  SPTK_REQUIRE(ws_bytes >= (size_t)blocks * md.cor_size * sizeof(double), "core_pass: workspace too small");
+  double* partial = (double*)ws;
+  auto kfn = core_pass_kernel<T, false>;
+  if (smem > 48 * 1024) SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, rw, rec_val_off(md.n_modes, f64), visit, map, n_visit, fac, cor, md, S,
+                                           partial, nullptr);
+  SPTK_CHECK_LAUNCH();
+  core_reduce_kernel<<<(md.cor_size + 255) / 256, 256, 0, s>>>(partial, (int)blocks, md.cor_size, acc);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// Verification mode: chunk boundaries follow np.array_split(psi, n_chunks).
+template <typename T>
+int core_pass_exact(const int* rec, int rw, const int* visit, const int* map, long long n_visit, int n_chunks,
+                    const T* fac, const T* cor, const ModelDesc& md, double* acc, void* ws, size_t ws_bytes,
+                    cudaStream_t s) {
+  if (n_visit <= 0) return 0;
+  SPTK_REQUIRE(n_chunks >= 1 && n_chunks <= 1024, "core_pass_exact: bad chunk count");
+  const bool f64 = sizeof(T) == 8;
+  SPTK_REQUIRE(rw == rec_words_t(md.n_modes, f64), "core_pass_exact: record width mismatch");
+  int S;
+  size_t smem;
+  SPTK_REQUIRE(pick_S(md, sizeof(T), &S, &smem), "core_pass_exact: model ranks too large");
+  // np.array_split: first (n % k) chunks get one extra element; empty chunks dropped
+  long long h_lo[1025];
+  long long q = n_visit / n_chunks, rmd = n_visit % n_chunks, pos = 0;
+  int nb = 0;
+  for (int c = 0; c < n_chunks; ++c) {
+    long long len = q + (c < rmd ? 1 : 0);
+    if (len == 0) continue;
+    h_lo[nb++] = pos;
+    pos += len;
+  }
+  h_lo[nb] = pos;
+  size_t need = (size_t)nb * md.cor_size * sizeof(double) + sizeof(long long) * (nb + 1) + 256;
+  SPTK_REQUIRE(ws_bytes >= need, "core_pass_exact: workspace too small");
+  double* partial = (double*)ws;
+  long long* d_lo = (long long*)((char*)ws + (((size_t)nb * md.cor_size * sizeof(double) + 255) & ~(size_t)255));
+  SPTK_CUDA_TRY(cudaMemcpyAsync(d_lo, h_lo, sizeof(long long) * (nb + 1), cudaMemcpyHostToDevice, s));
+  auto kfn = core_pass_kernel<T, true>;
+  if (smem > 48 * 1024) SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kfn<<<(unsigned)nb, 256, smem, s>>>(rec, rw, rec_val_off(md.n_modes, f64), visit, map, n_visit, fac, cor, md, S,
+                                       partial, d_lo);
+  SPTK_CHECK_LAUNCH();
+  core_reduce_ordered_kernel<<<(md.cor_size + 255) / 256, 256, 0, s>>>(partial, nb, md.cor_size, acc);
+  SPTK_CHECK_LAUNCH();
+  // the host copy of h_lo must outlive the async copy
+  SPTK_CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
+template <typename T>
+__global__ void core_apply_kernel(T* __restrict__ cor, const double* __restrict__ acc, int CS, double gamma_b,
+                                  double lambda_b, double denom) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < CS; o += gridDim.x * blockDim.x) {
+    double b = (double)cor[o];
+    double upd = __dadd_rn(__ddiv_rn(acc[o], denom), __dmul_rn(lambda_b, b));
+    cor[o] = (T)__dadd_rn(b, -__dmul_rn(gamma_b, upd));
+  }
+}
+
+template <typename T>
+int core_apply(T* cor, const double* acc, int cor_size, double gamma_b, double lambda_b, double denom,
+               cudaStream_t s) {
+  core_apply_kernel<T><<<(cor_size + 255) / 256, 256, 0, s>>>(cor, acc, cor_size, gamma_b, lambda_b, denom);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+template int core_pass<float>(const int*, int, const int*, const int*, long long, const float*, const float*,
+                              const ModelDesc&, double*, void*, size_t, cudaStream_t);
+template int core_pass<double>(const int*, int, const int*, const int*, long long, const double*, const double*,
+                               const ModelDesc&, double*, void*, size_t, cudaStream_t);
+template int core_pass_exact<float>(const int*, int, const int*, const int*, long long, int, const float*,
+                                    const float*, const ModelDesc&, double*, void*, size_t, cudaStream_t);
+template int core_pass_exact<double>(const int*, int, const int*, const int*, long long, int, const double*,
+                                     const double*, const ModelDesc&, double*, void*, size_t, cudaStream_t);
+template int core_apply<float>(float*, const double*, int, double, double, double, cudaStream_t);
+template int core_apply<double>(double*, const double*, int, double, double, double, cudaStream_t);
+
+}  // namespace sptk

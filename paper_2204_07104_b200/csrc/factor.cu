@@ -1,0 +1,440 @@
+// factor.cu -- K3: the per-nonzero factor-row SGD update (Eq. 13).
+//
+// Restates _loops.factor_pass (_loops.py:17-63): for every visited sample and
+// every mode n in ascending order,
+//     c[n0,r] = A(n0)[i_n0,:] . B(n0)[:,r]                 (refreshed per mode)
+//     gs[j]   = sum_r (prod_{n0!=n} c[n0,r]) * B(n)[j,r]
+//     inter   = a . gs
+//     a[j]   -= gamma_n * (-x*gs[j] + lambda_n*a[j] + inter*gs[j])
+// Only the updated mode's c row changes between modes, so the kernels compute
+// the c table once per sample and refresh one row per mode: (3N-1)*J*R FMAs
+// per sample instead of the reference's (N^2+N)*J*R, with identical values.
+//
+// Three kernels:
+//   * factor_tps_kernel<N,J,R,RW>  throughput mode, one thread per sample.
+//     B(n) lives in the constant bank (uniform across the warp, so every FFMA
+//     takes its B operand straight from c[][] with no shared-memory traffic),
+//     rows are gathered with 16-byte L2 loads, Hogwild in visit order as in
+//     cuFastTucker.
+//   * factor_wps_kernel<T>         throughput mode for ranks without a
+//     specialisation: one warp per sample, lanes over r and j (the paper's
+//     warp-shuffle layout), B(n) in shared memory.
+//   * factor_seq_kernel<T>         deterministic verification mode: one warp
+//     walks the visit list strictly in order with the reference's exact
+//     operation order and no FMA contraction (fp32 or fp64).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sptk {
+
+#define CONST_COR_MAX 12288
+__constant__ float c_cor[CONST_COR_MAX];
+
+template <int N>
+struct TpsParams {
+  long long foff[N];
+  float gam[N];
+  float lam[N];
+};
+
+template <int N, int J, int R, int RW>
+__global__ void __launch_bounds__(128, 3)
+    factor_tps_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit,
+                      long long base, float* __restrict__ fac, TpsParams<N> p) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n_visit; k += stride) {
+    const long long ri = base + (visit ? (long long)__ldg(visit + k) : k);
+    const int* rp = rec + ri * RW;
+    int idx[N];
+    float x;
+    {
+      int4 w0 = __ldg(reinterpret_cast<const int4*>(rp));
+      int wv[RW];
+      wv[0] = w0.x;
+      wv[1] = w0.y;
+      wv[2] = w0.z;
+      wv[3] = w0.w;
+      if (RW >= 8) {
+        int4 w1 = __ldg(reinterpret_cast<const int4*>(rp) + 1);
+        wv[4 % RW] = w1.x;
+        wv[5 % RW] = w1.y;
+        wv[6 % RW] = w1.z;
+        wv[7 % RW] = w1.w;
+      }
+#pragma unroll
+      for (int n = 0; n < N; ++n) idx[n] = wv[n];
+      x = __int_as_float(wv[N]);
+    }
+    float a[N][J];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float4* src = reinterpret_cast<const float4*>(fac + p.foff[n] + (long long)idx[n] * J);
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) {
+        float4 v = __ldcg(src + q);
+        a[n][4 * q] = v.x;
+        a[n][4 * q + 1] = v.y;
+        a[n][4 * q + 2] = v.z;
+        a[n][4 * q + 3] = v.w;
+      }
+    }
+    float c[N][R];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc = fmaf(a[n][j], c_cor[n * J * R + j * R + r], acc);
+        c[n][r] = acc;
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      float gs[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) gs[j] = 0.f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float w = 1.f;
+#pragma unroll
+        for (int n0 = 0; n0 < N; ++n0)
+          if (n0 != n) w *= c[n0][r];
+#pragma unroll
+        for (int j = 0; j < J; ++j) gs[j] = fmaf(w, c_cor[n * J * R + j * R + r], gs[j]);
+      }
+      float inter = 0.f;
+#pragma unroll
+      for (int j = 0; j < J; ++j) inter = fmaf(a[n][j], gs[j], inter);
+      const float gm = p.gam[n], lm = p.lam[n];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        float g = -x * gs[j] + lm * a[n][j] + inter * gs[j];
+        a[n][j] -= gm * g;
+      }
+      float4* dst = reinterpret_cast<float4*>(fac + p.foff[n] + (long long)idx[n] * J);
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q)
+        __stcg(dst + q, make_float4(a[n][4 * q], a[n][4 * q + 1], a[n][4 * q + 2], a[n][4 * q + 3]));
+      if (n < N - 1) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float acc = 0.f;
+#pragma unroll
+          for (int j = 0; j < J; ++j) acc = fmaf(a[n][j], c_cor[n * J * R + j * R + r], acc);
+          c[n][r] = acc;
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// warp per sample (generic ranks, J <= 64, R <= 64), Hogwild
+// ----------------------------------------------------------------------------
+struct GamLam {
+  double gam[SPTK_MAX_MODES];
+  double lam[SPTK_MAX_MODES];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) factor_wps_kernel(const int* __restrict__ rec, int rw, int vo,
+                                                         const int* __restrict__ visit, long long n_visit,
+                                                         long long base, T* __restrict__ fac,
+                                                         const T* __restrict__ cor, ModelDesc md, GamLam gl,
+                                                         int scratch_per_warp) {
+  extern __shared__ unsigned char smem_raw[];
+  T* Bs = reinterpret_cast<T*>(smem_raw);
+  for (int i = threadIdx.x; i < md.cor_size; i += blockDim.x) Bs[i] = cor[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int N = md.n_modes, R = md.rcore;
+  T* scr = Bs + ((md.cor_size + 3) & ~3) + wib * scratch_per_warp;
+  int aoff[SPTK_MAX_MODES];
+  int tot = 0;
+  for (int n = 0; n < N; ++n) {
+    aoff[n] = tot;
+    tot += md.jr[n];
+  }
+  T* a_s = scr;                // sum J
+  T* c_s = scr + tot;          // N*R
+  T* w_s = c_s + N * R;        // R
+  T* g_s = w_s + R;            // max J
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + wib; k < n_visit; k += nwarps) {
+    const long long ri = base + (visit ? (long long)__ldg(visit + k) : k);
+    const int* rp = rec + ri * rw;
+    const T x = load_val<T>(rp, vo);
+    for (int n = 0; n < N; ++n) {
+      const int J = md.jr[n];
+      const T* row = fac + md.foff[n] + (long long)__ldg(rp + n) * J;
+      for (int j = lane; j < J; j += 32) a_s[aoff[n] + j] = __ldcg(row + j);
+    }
+    __syncwarp();
+    for (int n0 = 0; n0 < N; ++n0) {
+      const int J = md.jr[n0];
+      for (int r = lane; r < R; r += 32) {
+        T acc = 0;
+        for (int j = 0; j < J; ++j) acc += a_s[aoff[n0] + j] * Bs[md.coff[n0] + j * R + r];
+        c_s[n0 * R + r] = acc;
+      }
+    }
+    __syncwarp();
+    for (int n = 0; n < N; ++n) {
+      const int J = md.jr[n];
+      for (int r = lane; r < R; r += 32) {
+        T w = 1;
+        for (int n0 = 0; n0 < N; ++n0)
+          if (n0 != n) w *= c_s[n0 * R + r];
+        w_s[r] = w;
+      }
+      __syncwarp();
+      T part = 0;
+      for (int j = lane; j < J; j += 32) {
+        T g = 0;
+        for (int r = 0; r < R; ++r) g += w_s[r] * Bs[md.coff[n] + j * R + r];
+        g_s[j] = g;
+        part += a_s[aoff[n] + j] * g;
+      }
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const T inter = part;
+      const T gm = (T)gl.gam[n], lm = (T)gl.lam[n];
+      T* row = fac + md.foff[n] + (long long)__ldg(rp + n) * J;
+      for (int j = lane; j < J; j += 32) {
+        T av = a_s[aoff[n] + j];
+        T gsj = g_s[j];
+        T g = -x * gsj + lm * av + inter * gsj;
+        av -= gm * g;
+        a_s[aoff[n] + j] = av;
+        __stcg(row + j, av);
+      }
+      __syncwarp();
+      if (n < N - 1) {
+        for (int r = lane; r < R; r += 32) {
+          T acc = 0;
+          for (int j = 0; j < J; ++j) acc += a_s[aoff[n] + j] * Bs[md.coff[n] + j * R + r];
+          c_s[n * R + r] = acc;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// sequential, exact reference operation order (no FMA contraction)
+// ----------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b);
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T>
+__global__ void __launch_bounds__(32) factor_seq_kernel(const int* __restrict__ rec, int rw, int vo,
+                                                        const int* __restrict__ visit, long long n_visit,
+                                                        long long base, T* __restrict__ fac,
+                                                        const T* __restrict__ cor, ModelDesc md, GamLam gl) {
+  extern __shared__ unsigned char smem_raw[];
+  T* Bs = reinterpret_cast<T*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < md.cor_size; i += 32) Bs[i] = cor[i];
+  const int N = md.n_modes, R = md.rcore;
+  int aoff[SPTK_MAX_MODES];
+  int tot = 0, jmax = 0;
+  for (int n = 0; n < N; ++n) {
+    aoff[n] = tot;
+    tot += md.jr[n];
+    jmax = md.jr[n] > jmax ? md.jr[n] : jmax;
+  }
+  T* a_s = Bs + md.cor_size;
+  T* c_s = a_s + tot;
+  T* w_s = c_s + N * R;
+  T* g_s = w_s + R;
+  __syncwarp();
+  for (long long k = 0; k < n_visit; ++k) {
+    const long long ri = base + (visit ? (long long)visit[k] : k);
+    const int* rp = rec + ri * rw;
+    const T x = load_val<T>(rp, vo);
+    for (int n = 0; n < N; ++n) {
+      const int J = md.jr[n];
+      volatile const T* row = fac + md.foff[n] + (long long)rp[n] * J;
+      for (int j = lane; j < J; j += 32) a_s[aoff[n] + j] = row[j];
+    }
+    __syncwarp();
+    for (int n0 = 0; n0 < N; ++n0) {
+      const int J = md.jr[n0];
+      for (int r = lane; r < R; r += 32) {
+        T acc = 0;
+        for (int j = 0; j < J; ++j) acc = add_rn(acc, mul_rn(a_s[aoff[n0] + j], Bs[md.coff[n0] + j * R + r]));
+        c_s[n0 * R + r] = acc;
+      }
+    }
+    __syncwarp();
+    for (int n = 0; n < N; ++n) {
+      const int J = md.jr[n];
+      for (int r = lane; r < R; r += 32) {
+        T w = 1;
+        for (int n0 = 0; n0 < N; ++n0)
+          if (n0 != n) w = mul_rn(w, c_s[n0 * R + r]);
+        w_s[r] = w;
+      }
+      __syncwarp();
+      for (int j = lane; j < J; j += 32) {
+        T g = 0;
+        for (int r = 0; r < R; ++r) g = add_rn(g, mul_rn(w_s[r], Bs[md.coff[n] + j * R + r]));
+        g_s[j] = g;
+      }
+      __syncwarp();
+      T inter = 0;
+      for (int j = 0; j < J; ++j) inter = add_rn(inter, mul_rn(a_s[aoff[n] + j], g_s[j]));
+      const T gm = (T)gl.gam[n], lm = (T)gl.lam[n];
+      T* row = fac + md.foff[n] + (long long)rp[n] * J;
+      for (int j = lane; j < J; j += 32) {
+        T av = a_s[aoff[n] + j];
+        T gsj = g_s[j];
+        T g = add_rn(add_rn(mul_rn(-x, gsj), mul_rn(lm, av)), mul_rn(inter, gsj));
+        av = add_rn(av, -mul_rn(gm, g));
+        a_s[aoff[n] + j] = av;
+        row[j] = av;
+      }
+      __syncwarp();
+      if (n < N - 1) {
+        for (int r = lane; r < R; r += 32) {
+          T acc = 0;
+          for (int j = 0; j < J; ++j) acc = add_rn(acc, mul_rn(a_s[aoff[n] + j], Bs[md.coff[n] + j * R + r]));
+          c_s[n * R + r] = acc;
+        }
+      }
+      __syncwarp();
+    }
+    __threadfence_block();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// host dispatch
+// ----------------------------------------------------------------------------
+static bool all_equal_j(const ModelDesc& md, int J) {
+  for (int n = 0; n < md.n_modes; ++n)
+    if (md.jr[n] != J) return false;
+  return true;
+}
+
+template <int N, int J, int R>
+static int launch_tps(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                      const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+  TpsParams<N> p;
+  for (int n = 0; n < N; ++n) {
+    p.foff[n] = md.foff[n];
+    p.gam[n] = gam[n];
+    p.lam[n] = lam[n];
+  }
+  SPTK_CUDA_TRY(cudaMemcpyToSymbolAsync(c_cor, cor, sizeof(float) * N * J * R, 0, cudaMemcpyDeviceToDevice, s));
+  const int threads = 128;
+  long long blocks = (n_visit + threads - 1) / threads;
+  const long long cap = 148LL * 3 * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (rw == 4)
+    factor_tps_kernel<N, J, R, 4><<<(unsigned)blocks, threads, 0, s>>>(rec, visit, n_visit, base, fac, p);
+  else
+    factor_tps_kernel<N, J, R, 8><<<(unsigned)blocks, threads, 0, s>>>(rec, visit, n_visit, base, fac, p);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// returns 1 if handled (status in *rc), 0 if no specialisation
+static int try_tps(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                   const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s,
+                   int* rc) {
+  const int N = md.n_modes, R = md.rcore, J = md.jr[0];
+  if (!all_equal_j(md, J) || J != R) return 0;
+  if (rw != rec_words(N)) return 0;
+#define SPTK_TPS(NN, JJ)                                                                          \
+  if (N == NN && J == JJ) {                                                                       \
+    *rc = launch_tps<NN, JJ, JJ>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);      \
+    return 1;                                                                                     \
+  }
+  SPTK_TPS(3, 4)
+  SPTK_TPS(3, 8)
+  SPTK_TPS(3, 16)
+  SPTK_TPS(4, 4)
+  SPTK_TPS(4, 8)
+  SPTK_TPS(4, 16)
+  SPTK_TPS(6, 4)
+  SPTK_TPS(6, 8)
+#undef SPTK_TPS
+  return 0;
+}
+
+template <typename T>
+int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, long long base, T* fac,
+                const T* cor, const ModelDesc& md, const T* h_gammas, const T* h_lambdas, int mode,
+                cudaStream_t s) {
+  SPTK_REQUIRE(md.n_modes >= 2 && md.n_modes <= SPTK_MAX_MODES, "factor_pass: bad order %d", md.n_modes);
+  if (n_visit <= 0) return 0;
+  const bool f64 = sizeof(T) == 8;
+  const int vo = rec_val_off(md.n_modes, f64);
+  SPTK_REQUIRE(rw == rec_words_t(md.n_modes, f64), "factor_pass: record width %d does not match order %d", rw,
+               md.n_modes);
+  GamLam gl;
+  for (int n = 0; n < md.n_modes; ++n) {
+    gl.gam[n] = (double)h_gammas[n];
+    gl.lam[n] = (double)h_lambdas[n];
+  }
+  int jmax = 0, tot = 0;
+  for (int n = 0; n < md.n_modes; ++n) {
+    jmax = md.jr[n] > jmax ? md.jr[n] : jmax;
+    tot += md.jr[n];
+  }
+  if (mode == 1) {
+    size_t smem = sizeof(T) * ((size_t)md.cor_size + tot + 2 * (size_t)md.n_modes * md.rcore + md.rcore + jmax + 8);
+    SPTK_REQUIRE(smem <= 200 * 1024, "factor_pass(seq): model ranks too large");
+    auto kfn = factor_seq_kernel<T>;
+    if (smem > 48 * 1024)
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kfn<<<1, 32, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl);
+    SPTK_CHECK_LAUNCH();
+    return 0;
+  }
+  if (!f64) {
+    int rc = 0;
+    if (md.cor_size <= CONST_COR_MAX &&
+        try_tps(rec, rw, visit, n_visit, base, (float*)fac, (const float*)cor, md, (const float*)h_gammas,
+                (const float*)h_lambdas, s, &rc))
+      return rc;
+  }
+  SPTK_REQUIRE(jmax <= 1024 && md.rcore <= 1024, "factor_pass: ranks too large");
+  int per_warp = tot + md.n_modes * md.rcore + md.rcore + jmax + 4;
+  per_warp = (per_warp + 3) & ~3;
+  int warps = 8;
+  size_t smem = sizeof(T) * ((size_t)((md.cor_size + 3) & ~3) + (size_t)per_warp * warps);
+  while (smem > 200 * 1024 && warps > 1) {
+    warps /= 2;
+    smem = sizeof(T) * ((size_t)((md.cor_size + 3) & ~3) + (size_t)per_warp * warps);
+  }
+  SPTK_REQUIRE(smem <= 200 * 1024, "factor_pass: model ranks too large for shared memory");
+  auto kfn = factor_wps_kernel<T>;
+  if (smem > 48 * 1024)
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  long long blocks = (n_visit + warps - 1) / warps;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  kfn<<<(unsigned)blocks, 32 * warps, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl, per_warp);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+template int factor_pass<float>(const int*, int, const int*, long long, long long, float*, const float*,
+                                const ModelDesc&, const float*, const float*, int, cudaStream_t);
+template int factor_pass<double>(const int*, int, const int*, long long, long long, double*, const double*,
+                                 const ModelDesc&, const double*, const double*, int, cudaStream_t);
+
+}  // namespace sptk

@@ -1,0 +1,55 @@
+// kernels.cuh -- internal host-side entry points shared between .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace sptk {
+
+// sampler.cu
+size_t perm_ws_bytes(long long n);
+int permutation(const uint64_t st[4], long long n, int* out, void* ws, size_t ws_bytes, cudaStream_t s);
+int permutation_j(const uint64_t st[4], long long n, int* j_out, void* ws, size_t ws_bytes, cudaStream_t s);
+size_t choice_ws_bytes(long long pop, long long k);
+int choice(const uint64_t st[4], long long pop, long long k, int shuffle, int* out, void* ws,
+           size_t ws_bytes, int* path_out, cudaStream_t s);
+int u32_stream(const uint64_t st[4], unsigned long long q0, long long n, uint32_t* out, cudaStream_t s);
+int iota(int* out, long long n, int offset, cudaStream_t s);
+size_t scan_ws_bytes(long long n);
+int exclusive_scan(const int* in, long long n, int* out, int* ws, cudaStream_t s);
+
+// partition.cu
+size_t partition_ws_bytes(long long nnz, int order, long long m);
+int partition(const long long* idx64, const double* vals64, long long nnz, int order, const long long* h_dims,
+              long long m, int* rec_out, int* ids_out, int* pos_of_id_out, int* block_off_out, void* ws,
+              size_t ws_bytes, cudaStream_t s, int f64);
+int pack_records(const long long* idx64, const double* vals64, long long nnz, int order, int* rec_out,
+                 cudaStream_t s, int f64);
+
+// factor.cu
+template <typename T>
+int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, long long base, T* fac,
+                const T* cor, const ModelDesc& md, const T* h_gammas, const T* h_lambdas, int mode,
+                cudaStream_t s);
+
+// core.cu
+size_t core_ws_bytes(const ModelDesc& md);
+template <typename T>
+int core_pass(const int* rec, int rw, const int* visit, const int* map, long long n_visit, const T* fac,
+              const T* cor, const ModelDesc& md, double* acc, void* ws, size_t ws_bytes, cudaStream_t s);
+template <typename T>
+int core_pass_exact(const int* rec, int rw, const int* visit, const int* map, long long n_visit, int n_chunks,
+                    const T* fac, const T* cor, const ModelDesc& md, double* acc, void* ws, size_t ws_bytes,
+                    cudaStream_t s);
+template <typename T>
+int core_apply(T* cor, const double* acc, int cor_size, double gamma_b, double lambda_b, double denom,
+               cudaStream_t s);
+
+// eval.cu
+template <typename T>
+int eval(const int* rec, int rw, long long m, const T* fac, const T* cor, const ModelDesc& md, T* pred_out,
+         double* sums, cudaStream_t s);
+
+}  // namespace sptk

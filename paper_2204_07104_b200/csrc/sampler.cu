@@ -1,0 +1,1073 @@
+// sampler.cu -- K2: bit-exact GPU re-derivation of the reference's samplers.
+//
+// The reference draws, per epoch,
+//   * the factor-phase visit order  default_rng([seed,1,t,*block]).permutation(len(ids))
+//     (trainer.py:300-303): numpy Fisher-Yates, i = n-1..1,
+//     j_i = random_interval(i) (masked rejection on buffered u32 draws);
+//   * the core batch  default_rng([seed,2,t]).choice(nnz, k, replace=False)
+//     (trainer.py:317-324): Floyd with Lemire draws + _shuffle_int, or the
+//     tail-shuffle path (_shuffle_int over arange) when pop > 10000 and
+//     k > pop // 50.
+// These are inherently sequential loops over one PCG64 stream.  They are
+// reproduced here exactly with three parallel building blocks:
+//
+//  (1) masked-rejection j-sequence (permutation).  Steps with the same mask
+//      (i in [2^(k-1), 2^k)) form a segment.  Inside a segment, position q of
+//      the u32 stream is accepted iff a_q <= y_q, a_q = accepts so far and
+//      y_q = hi - (v_q & mask).  Chunks of L positions compute a reference
+//      trajectory from a guessed count a0 (the mean curve) and record the few
+//      "near-margin" positions |y_q - tau_q| < Delta.  A single resolver warp
+//      then propagates the true count chunk to chunk: a shifted trajectory
+//      differs from the reference only at near-margin positions (gap
+//      dynamics), so each chunk costs O(#entries).  A second pass regenerates
+//      every chunk from its true count and writes j_i.  Chunks whose shift is
+//      out of range are walked exactly (slow path), so the result is exact
+//      for every input, not just with high probability.
+//  (2) Lemire draw sequences (Floyd values, _shuffle_int j's): rejections are
+//      rare (< 1%), so one CTA resolves 1024 draws per batch from 16
+//      speculative acceptance bits per draw and a ballot walk over the rare
+//      rejection events.
+//  (3) applying a Fisher-Yates swap sequence: with L_p the ascending list of
+//      steps targeting p, result[l_k] = val(l_{k+1}), result[l_last] = p,
+//      where val(s) (the value at position s just before step s) is the root
+//      of the forest parent(s) = first step > s targeting s.  Built with a
+//      counting sort by target, short per-bucket sorts and chain walks.
+#include <math.h>
+#include <stdio.h>
+
+#include "common.cuh"
+#include "pcg64.cuh"
+
+namespace sptk {
+
+#define FULLMASK 0xffffffffu
+
+// ---------------------------------------------------------------------------
+// raw stream
+// ---------------------------------------------------------------------------
+__global__ void u32_stream_kernel(Pcg64 g, unsigned long long q0, long long n, uint32_t* out) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; t < n; t += stride) out[t] = pcg_u32_at(g, q0 + (unsigned long long)t);
+}
+
+// ---------------------------------------------------------------------------
+// (1) masked-rejection segments
+// ---------------------------------------------------------------------------
+struct Seg {
+  int hi;         // largest step index of the segment
+  unsigned mask;  // 2^k - 1
+  int S;          // number of steps in the segment
+};
+
+// Accept flags of 64 ordered positions (lane l: position 2l (h=0), 2l+1 (h=1))
+// given the exact count `a` before the group; accepted positions whose count
+// would reach `cap` are dropped (the segment is over).
+__device__ __forceinline__ void group_accept(int a, int y0, int y1, bool v0, bool v1, int cap,
+                                             bool& acc0, bool& acc1) {
+  const int lane = threadIdx.x & 31;
+  bool c0 = v0 && (long long)y0 >= (long long)a + 63;
+  bool r0 = !v0 || y0 < a;
+  bool c1 = v1 && (long long)y1 >= (long long)a + 63;
+  bool r1 = !v1 || y1 < a;
+  unsigned unc = __ballot_sync(FULLMASK, !(c0 || r0) || !(c1 || r1));
+  if (unc == 0) {
+    acc0 = c0;
+    acc1 = c1;
+  } else {
+    int cur = a;
+    acc0 = acc1 = false;
+#pragma unroll 1
+    for (int l = 0; l < 32; ++l) {
+      int yy0 = __shfl_sync(FULLMASK, y0, l), yy1 = __shfl_sync(FULLMASK, y1, l);
+      bool vv0 = __shfl_sync(FULLMASK, v0, l), vv1 = __shfl_sync(FULLMASK, v1, l);
+      bool x0 = vv0 && cur <= yy0;
+      cur += x0;
+      bool x1 = vv1 && cur <= yy1;
+      cur += x1;
+      if (lane == l) {
+        acc0 = x0;
+        acc1 = x1;
+      }
+    }
+  }
+  if (cap != 0x7fffffff) {
+    unsigned lt = (1u << lane) - 1u;
+    unsigned b0 = __ballot_sync(FULLMASK, acc0), b1 = __ballot_sync(FULLMASK, acc1);
+    int before0 = __popc(b0 & lt) + __popc(b1 & lt);
+    int before1 = before0 + (acc0 ? 1 : 0);
+    if (acc0 && (long long)a + before0 >= cap) acc0 = false;
+    if (acc1 && (long long)a + before1 >= cap) acc1 = false;
+  }
+}
+
+// Exact warp walk over positions [q_begin, q_end) starting with count a.
+// Writes j_out[hi - count] = v & mask for accepted positions (if j_out), stops
+// when the count reaches cap; *q_stop = position after the cap-th accept (or
+// -1).  Returns the count at exit.  All 32 lanes must call it.
+__device__ int walk_exact(const Pcg64& g, const u128& A32, const u128& C32, long long q_begin,
+                          long long q_end, int a, const Seg sg, int cap, int* j_out,
+                          long long* q_stop) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  long long mbase = q_begin >> 1;
+  Pcg64 st;
+  st.inc = g.inc;
+  st.state = pcg_advance(g, (uint64_t)(mbase + lane + 1));
+  long long stop = -1;
+  while (2 * mbase < q_end && a < cap) {
+    uint64_t out = pcg_xsl_rr(st.state);
+    long long q0 = 2 * (mbase + lane), q1 = q0 + 1;
+    bool v0 = q0 >= q_begin && q0 < q_end, v1 = q1 >= q_begin && q1 < q_end;
+    unsigned u0 = (uint32_t)out & sg.mask, u1 = (uint32_t)(out >> 32) & sg.mask;
+    int y0 = sg.hi - (int)u0, y1 = sg.hi - (int)u1;
+    bool acc0, acc1;
+    group_accept(a, y0, y1, v0, v1, cap, acc0, acc1);
+    unsigned b0 = __ballot_sync(FULLMASK, acc0), b1 = __ballot_sync(FULLMASK, acc1);
+    int before0 = __popc(b0 & lt) + __popc(b1 & lt);
+    int before1 = before0 + (acc0 ? 1 : 0);
+    if (j_out) {
+      if (acc0) j_out[sg.hi - (a + before0)] = (int)u0;
+      if (acc1) j_out[sg.hi - (a + before1)] = (int)u1;
+    }
+    int total = __popc(b0) + __popc(b1);
+    if (a + total >= cap && cap != 0x7fffffff) {
+      // position of the cap-th accept
+      long long p = -1;
+      if (acc0 && a + before0 == cap - 1) p = q0;
+      if (acc1 && a + before1 == cap - 1) p = q1;
+      unsigned who = __ballot_sync(FULLMASK, p >= 0);
+      int src = __ffs(who) - 1;
+      stop = __shfl_sync(FULLMASK, p, src) + 1;
+    }
+    a += total;
+    st.state = st.state * A32 + C32;
+    mbase += 32;
+  }
+  if (q_stop) *q_stop = stop;
+  return a;
+}
+
+struct ChunkBuf {
+  int* a0;
+  int* D;
+  int* cnt;  // number of entries (> E means overflow)
+  int2* ent; // [C][E] (q_rel, margin)
+  int* a_in; // true count at chunk start (written by the resolver)
+  int E;
+};
+
+__device__ __forceinline__ int guess_count(const Seg& sg, long long p) {
+  double a = ((double)sg.hi + 1.0) * (1.0 - exp(-(double)p / ((double)sg.mask + 1.0)));
+  long long r = llrint(a);
+  if (r < 0) r = 0;
+  if (r > sg.S) r = sg.S;
+  return (int)r;
+}
+
+// Phase A: reference trajectory per chunk (one warp per chunk).
+__global__ void perm_phaseA_kernel(Pcg64 g, const long long* __restrict__ P, Seg sg, int L, int C,
+                                   int Delta, ChunkBuf cb) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= C) return;
+  u128 A32, C32;
+  pcg_jump_coeffs(g.inc, 32, &A32, &C32);
+  if (P[0] < 0) return;
+  const long long q_begin = P[0] + (long long)c * L, q_end = q_begin + L;
+  const int a0 = guess_count(sg, (long long)c * L);
+  int a = a0, cnt = 0;
+  long long mbase = q_begin >> 1;
+  Pcg64 st;
+  st.inc = g.inc;
+  st.state = pcg_advance(g, (uint64_t)(mbase + lane + 1));
+  int2* ent = cb.ent + (long long)c * cb.E;
+  while (2 * mbase < q_end) {
+    uint64_t out = pcg_xsl_rr(st.state);
+    long long q0 = 2 * (mbase + lane), q1 = q0 + 1;
+    bool v0 = q0 >= q_begin && q0 < q_end, v1 = q1 >= q_begin && q1 < q_end;
+    int y0 = sg.hi - (int)((uint32_t)out & sg.mask);
+    int y1 = sg.hi - (int)((uint32_t)(out >> 32) & sg.mask);
+    bool acc0, acc1;
+    group_accept(a, y0, y1, v0, v1, 0x7fffffff, acc0, acc1);
+    unsigned b0 = __ballot_sync(FULLMASK, acc0), b1 = __ballot_sync(FULLMASK, acc1);
+    int before0 = __popc(b0 & lt) + __popc(b1 & lt);
+    int before1 = before0 + (acc0 ? 1 : 0);
+    long long m0 = (long long)y0 - (a + before0), m1 = (long long)y1 - (a + before1);
+    bool n0 = v0 && m0 >= -Delta && m0 < Delta, n1 = v1 && m1 >= -Delta && m1 < Delta;
+    unsigned nb0 = __ballot_sync(FULLMASK, n0), nb1 = __ballot_sync(FULLMASK, n1);
+    int i0 = cnt + __popc(nb0 & lt) + __popc(nb1 & lt), i1 = i0 + (n0 ? 1 : 0);
+    if (n0 && i0 < cb.E) ent[i0] = make_int2((int)(q0 - q_begin), (int)m0);
+    if (n1 && i1 < cb.E) ent[i1] = make_int2((int)(q1 - q_begin), (int)m1);
+    cnt += __popc(nb0) + __popc(nb1);
+    a += __popc(b0) + __popc(b1);
+    st.state = st.state * A32 + C32;
+    mbase += 32;
+  }
+  if (lane == 0) {
+    cb.a0[c] = a0;
+    cb.D[c] = a - a0;
+    cb.cnt[c] = cnt;
+  }
+}
+
+// Resolver: one warp propagates the exact count through the chunks.
+// meta[0] = index of the chunk holding the segment end; P[1] = next start.
+__global__ void perm_resolve_kernel(Pcg64 g, long long* __restrict__ P, Seg sg, int L, int C,
+                                    int Delta, ChunkBuf cb, int* __restrict__ meta) {
+  __shared__ int2 ent_s[32][40];
+  const int lane = threadIdx.x & 31;
+  u128 A32, C32;
+  pcg_jump_coeffs(g.inc, 32, &A32, &C32);
+  const long long Pk = P[0];
+  long long a = 0;  // count at the current chunk
+  if (lane == 0) meta[0] = -1;
+  if (Pk < 0) {
+    if (lane == 0) P[1] = -1;
+    return;
+  }
+  for (int c0 = 0; c0 < C; c0 += 32) {
+    const int c = c0 + lane;
+    const bool valid = c < C;
+    int a0 = 0, D = 0, cnt = 0;
+    if (valid) {
+      a0 = cb.a0[c];
+      D = cb.D[c];
+      cnt = cb.cnt[c];
+    }
+    const bool ovf = cnt > cb.E;
+    const int ne = ovf ? 0 : cnt;
+    for (int e = 0; e < ne; ++e) ent_s[lane][e] = cb.ent[(long long)c * cb.E + e];
+    __syncwarp();
+    int trig = 0;          // assumed (a0 + D + g) deficit: out = in + D - trig
+    bool fixed = !valid;   // resolved exactly (slow path) or past the end
+    long long in = 0;
+    for (int it = 0; it < 64; ++it) {
+      int contrib = valid ? D - trig : 0;
+      // exclusive warp prefix of contrib
+      int incl = contrib;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULLMASK, incl, o);
+        if (lane >= o) incl += y;
+      }
+      in = a + (incl - contrib);
+      bool bad = false;
+      int ntrig = trig;
+      if (!fixed) {
+        long long delta = in - a0;
+        if (ovf || delta >= Delta || delta <= -Delta) {
+          bad = true;
+        } else {
+          int gg = (int)delta;
+          for (int e = 0; e < ne; ++e) {
+            int m = ent_s[lane][e].y;
+            if (gg > 0 && m >= 0 && m < gg) --gg;
+            else if (gg < 0 && m >= gg && m < 0) ++gg;
+          }
+          ntrig = (int)delta - gg;
+          bad = ntrig != trig;
+        }
+      }
+      unsigned badm = __ballot_sync(FULLMASK, bad);
+      if (badm == 0) break;
+      int f = __ffs(badm) - 1;
+      // lane f has a final input; resolve it (fast result or exact walk)
+      bool need_walk = __shfl_sync(FULLMASK, (int)(ovf || (in - a0) >= Delta || (in - a0) <= -Delta), f);
+      long long in_f = __shfl_sync(FULLMASK, in, f);
+      int D_f = __shfl_sync(FULLMASK, D, f);
+      int newtrig_f;
+      if (need_walk) {
+        long long qb = Pk + (long long)(c0 + f) * L;
+        int out_f = walk_exact(g, A32, C32, qb, qb + L, (int)in_f, sg, 0x7fffffff, nullptr, nullptr);
+        newtrig_f = (int)(in_f + D_f - out_f);
+      } else {
+        newtrig_f = __shfl_sync(FULLMASK, ntrig, f);
+      }
+      if (lane == f) {
+        trig = newtrig_f;
+        fixed = true;
+      }
+      // lanes before f keep their values (their inputs were already final)
+    }
+    long long out = in + D - trig;
+    // segment end inside this batch?
+    unsigned endm = __ballot_sync(FULLMASK, valid && out >= sg.S);
+    if (valid && (endm == 0 || lane <= __ffs(endm) - 1)) cb.a_in[c] = (int)in;
+    if (endm) {
+      int e = __ffs(endm) - 1;
+      long long in_e = __shfl_sync(FULLMASK, in, e);
+      long long qb = Pk + (long long)(c0 + e) * L;
+      long long qs = -1;
+      walk_exact(g, A32, C32, qb, qb + L, (int)in_e, sg, sg.S, nullptr, &qs);
+      if (lane == 0) {
+        meta[0] = c0 + e;
+        P[1] = qs;
+      }
+      return;
+    }
+    a = __shfl_sync(FULLMASK, out, 31);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    meta[0] = -2;  // ran out of chunks: caller reports an error
+    P[1] = -1;
+  }
+}
+
+// Phase B: regenerate each chunk from its exact count and write j.
+__global__ void perm_phaseB_kernel(Pcg64 g, const long long* __restrict__ P, Seg sg, int L, int C,
+                                   ChunkBuf cb, const int* __restrict__ meta, int* __restrict__ j_out) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int c_end = meta[0];
+  if (c >= C || c_end < 0 || c > c_end || P[0] < 0) return;
+  u128 A32, C32;
+  pcg_jump_coeffs(g.inc, 32, &A32, &C32);
+  const long long qb = P[0] + (long long)c * L;
+  walk_exact(g, A32, C32, qb, qb + L, cb.a_in[c], sg, sg.S, j_out, nullptr);
+}
+
+// Small segments k = kmax_small..1 walked by one warp.
+__global__ void perm_small_kernel(Pcg64 g, const long long* __restrict__ P, int kstart, long long n,
+                                  int* __restrict__ j_out, long long* __restrict__ q_final) {
+  u128 A32, C32;
+  pcg_jump_coeffs(g.inc, 32, &A32, &C32);
+  long long q = P[0];
+  for (int k = kstart; k >= 1 && q >= 0; --k) {
+    Seg sg;
+    long long hi = (1LL << k) - 1;
+    if (hi > n - 1) hi = n - 1;
+    long long lo = 1LL << (k - 1);
+    sg.hi = (int)hi;
+    sg.mask = (unsigned)((1ULL << k) - 1);
+    sg.S = (int)(hi - lo + 1);
+    long long qs = -1;
+    walk_exact(g, A32, C32, q, 0x3fffffffffffffffLL, 0, sg, sg.S, j_out, &qs);
+    q = qs;
+  }
+  if ((threadIdx.x & 31) == 0 && q_final) *q_final = q;
+}
+
+// ---------------------------------------------------------------------------
+// (2) Lemire draw sequences (one CTA)
+// ---------------------------------------------------------------------------
+// Draw t (t in [0,T)) asks for a value in [0, rng_t], rng_t = base + dir*t,
+// via buffered_bounded_lemire_uint32; stream values v[] start at position Q0
+// (v[0] is position Q0).  Writes out[t] and *q_end_out (position after the
+// last draw, relative to Q0).
+__device__ __forceinline__ bool lemire_ok(uint32_t v, uint32_t rng, uint32_t* res) {
+  uint32_t rng_excl = rng + 1u;
+  uint64_t m = (uint64_t)v * rng_excl;
+  uint32_t left = (uint32_t)m;
+  *res = (uint32_t)(m >> 32);
+  if (left >= rng_excl) return true;
+  uint32_t thr = (0xffffffffu - rng) % rng_excl;
+  return left >= thr;
+}
+
+#define LEM_BITS 16
+#define LEM_B 1024
+__global__ void __launch_bounds__(LEM_B) lemire_resolve_kernel(const uint32_t* __restrict__ v, long long vcap,
+                                                               long long T, long long base, int dir,
+                                                               uint32_t* __restrict__ out,
+                                                               long long* __restrict__ q_end_out,
+                                                               int* __restrict__ err) {
+  __shared__ uint32_t masks[LEM_B];
+  __shared__ int eoff[LEM_B];  // resolved offset e* of each draw
+  __shared__ int s_stop, s_elast;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  long long delta = 0;  // rejections before draw t0
+  long long t0 = 0;
+  while (t0 < T) {
+    long long t = t0 + tid;
+    uint32_t rng = (uint32_t)(base + (long long)dir * t);
+    uint32_t mk = 0;
+    if (t < T) {
+      for (int e = 0; e < LEM_BITS; ++e) {
+        long long pos = t + delta + e;
+        uint32_t r;
+        bool ok = pos < vcap ? lemire_ok(v[pos], rng, &r) : false;
+        mk |= (ok ? 1u : 0u) << e;
+      }
+    } else {
+      mk = 0xffffu;
+    }
+    masks[tid] = mk;
+    __syncthreads();
+    if (tid < 32) {
+      // warp 0 walks the batch in 32-draw sub-batches
+      int e = 0;
+      int stop = LEM_B;
+      for (int sb = 0; sb < LEM_B / 32; ++sb) {
+        uint32_t m = masks[sb * 32 + lane];
+        int my_e = e;  // offset before this draw (updated below)
+        int start = 0;
+        while (true) {
+          bool zero = lane >= start && !((m >> e) & 1u);
+          unsigned z = __ballot_sync(FULLMASK, zero);
+          if (z == 0) {
+            if (lane >= start) my_e = e;
+            break;
+          }
+          int l1 = __ffs(z) - 1;
+          if (lane >= start && lane <= l1) my_e = e;
+          // draw l1 rejects until the next accepted bit
+          uint32_t m1 = __shfl_sync(FULLMASK, m, l1);
+          uint32_t rest = e + 1 < 32 ? (m1 >> (e + 1)) : 0u;
+          int ne = rest ? e + 1 + (__ffs(rest) - 1) : LEM_BITS;
+          if (ne >= LEM_BITS) {
+            stop = sb * 32 + l1;  // cannot resolve draw l1 within the window
+            break;
+          }
+          if (lane == l1) my_e = ne;  // l1 accepts at ne
+          e = ne;
+          start = l1 + 1;
+          if (start >= 32) break;
+        }
+        eoff[sb * 32 + lane] = my_e;
+        if (stop != LEM_B) break;
+      }
+      if (lane == 0) {
+        s_stop = stop;
+        s_elast = e;
+      }
+    }
+    __syncthreads();
+    const int stop = s_stop;
+    if (stop == 0) {
+      // the very first draw of the batch needs > LEM_BITS tries: walk it alone
+      if (tid == 0) {
+        long long pos = t0 + delta;
+        uint32_t rng0 = (uint32_t)(base + (long long)dir * t0);
+        uint32_t r;
+        while (pos < vcap && !lemire_ok(v[pos], rng0, &r)) ++pos;
+        if (pos >= vcap) {
+          *err = 1;
+        } else {
+          out[t0] = r;
+        }
+        s_elast = (int)(pos - (t0 + delta));
+      }
+      __syncthreads();
+      if (*err) return;
+      delta += s_elast;
+      t0 += 1;
+      __syncthreads();
+      continue;
+    }
+    if (tid < stop && t < T) {
+      long long pos = t + delta + eoff[tid];
+      uint32_t r = 0;
+      if (pos < vcap) lemire_ok(v[pos], rng, &r);
+      else *err = 2;
+      out[t] = r;
+    }
+    long long nres = stop;
+    if (t0 + nres > T) nres = T - t0;
+    // delta after the resolved prefix: e offset carried at the stop point
+    int ecarry;
+    if (stop == LEM_B) {
+      ecarry = s_elast;
+    } else {
+      ecarry = eoff[stop - 1];  // draw stop-1 accepted at its eoff; next starts there
+    }
+    __syncthreads();
+    delta += ecarry;
+    t0 += nres;
+  }
+  if (tid == 0) *q_end_out = T + delta;
+}
+
+// ---------------------------------------------------------------------------
+// (3) apply a Fisher-Yates swap sequence
+// ---------------------------------------------------------------------------
+__global__ void fy_hist_kernel(const int* __restrict__ j, long long first, long long n, int* __restrict__ cnt) {
+  long long i = first + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) atomicAdd(&cnt[j[i]], 1);
+}
+
+__global__ void fy_scatter_kernel(const int* __restrict__ j, long long first, long long n,
+                                  const int* __restrict__ start, int* __restrict__ fill,
+                                  int* __restrict__ list) {
+  long long i = first + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    int p = j[i];
+    int pos = start[p] + atomicAdd(&fill[p], 1);
+    list[pos] = (int)i;
+  }
+}
+
+// sort each bucket ascending; parent[p] = first step > p targeting p (or -1)
+__global__ void fy_bucket_kernel(const int* __restrict__ start, int* __restrict__ list, long long n,
+                                 int* __restrict__ parent) {
+  long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; p < n; p += stride) {
+    int b = start[p], e = start[p + 1];
+    for (int x = b + 1; x < e; ++x) {
+      int key = list[x];
+      int y = x - 1;
+      while (y >= b && list[y] > key) {
+        list[y + 1] = list[y];
+        --y;
+      }
+      list[y + 1] = key;
+    }
+    int par = -1;
+    if (e > b) {
+      int l1 = list[b];
+      if (l1 > p) par = l1;
+      else if (e - b >= 2) par = list[b + 1];
+    }
+    parent[p] = par;
+  }
+}
+
+__global__ void fy_val_kernel(const int* __restrict__ parent, long long n, int* __restrict__ val) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; s < n; s += stride) {
+    int v = (int)s;
+    int p = parent[v];
+    while (p >= 0) {
+      v = p;
+      p = parent[v];
+    }
+    val[s] = v;
+  }
+}
+
+__global__ void fy_result_kernel(const int* __restrict__ start, const int* __restrict__ list,
+                                 const int* __restrict__ val, long long n, int* __restrict__ result) {
+  long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; p < n; p += stride) {
+    int b = start[p], e = start[p + 1];
+    for (int x = b; x < e; ++x) result[list[x]] = (x + 1 < e) ? val[list[x + 1]] : (int)p;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan of int32 (n+1 outputs: out[n] = total); 3-phase
+// ---------------------------------------------------------------------------
+#define SCAN_B 1024
+#define SCAN_ITEMS 8
+__device__ __forceinline__ int block_excl_scan(int x, int* sh, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(FULLMASK, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) sh[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int s = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+    int si = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FULLMASK, si, o);
+      if (lane >= o) si += y;
+    }
+    sh[lane] = si - s;
+    if (lane == 31) sh[32] = si;
+  }
+  __syncthreads();
+  int r = sh[w] + incl - x;
+  *total = sh[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(SCAN_B) scan_reduce_kernel(const int* __restrict__ in, long long n,
+                                                             int* __restrict__ bsum) {
+  __shared__ int sh[33];
+  long long base = (long long)blockIdx.x * SCAN_B * SCAN_ITEMS;
+  int s = 0;
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    long long i = base + (long long)k * SCAN_B + threadIdx.x;
+    if (i < n) s += in[i];
+  }
+  int tot;
+  block_excl_scan(s, sh, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_B) scan_top_kernel(int* __restrict__ bsum, int nb) {
+  __shared__ int sh[33];
+  int carry = 0;
+  for (int b0 = 0; b0 < nb; b0 += SCAN_B) {
+    int i = b0 + threadIdx.x;
+    int x = i < nb ? bsum[i] : 0;
+    int tot;
+    int ex = block_excl_scan(x, sh, &tot);
+    if (i < nb) bsum[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) bsum[nb] = carry;
+}
+
+__global__ void __launch_bounds__(SCAN_B) scan_down_kernel(const int* __restrict__ in, long long n,
+                                                           const int* __restrict__ bsum, int* __restrict__ out) {
+  __shared__ int sh[33];
+  long long base = (long long)blockIdx.x * SCAN_B * SCAN_ITEMS;
+  // thread-contiguous items for a per-thread serial scan
+  int vals[SCAN_ITEMS];
+  int s = 0;
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    long long i = base + (long long)threadIdx.x * SCAN_ITEMS + k;
+    vals[k] = i < n ? in[i] : 0;
+    s += vals[k];
+  }
+  int tot;
+  int ex = block_excl_scan(s, sh, &tot) + bsum[blockIdx.x];
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    long long i = base + (long long)threadIdx.x * SCAN_ITEMS + k;
+    if (i < n) out[i] = ex;
+    ex += vals[k];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out[n] = bsum[gridDim.x];
+}
+
+size_t scan_ws_bytes(long long n) {
+  long long nb = (n + SCAN_B * SCAN_ITEMS - 1) / (SCAN_B * SCAN_ITEMS);
+  return (size_t)(nb + 1) * sizeof(int);
+}
+
+int exclusive_scan(const int* in, long long n, int* out, int* ws, cudaStream_t s) {
+  long long nb = (n + SCAN_B * SCAN_ITEMS - 1) / (SCAN_B * SCAN_ITEMS);
+  if (nb == 0) nb = 1;
+  scan_reduce_kernel<<<(unsigned)nb, SCAN_B, 0, s>>>(in, n, ws);
+  SPTK_CHECK_LAUNCH();
+  scan_top_kernel<<<1, SCAN_B, 0, s>>>(ws, (int)nb);
+  SPTK_CHECK_LAUNCH();
+  scan_down_kernel<<<(unsigned)nb, SCAN_B, 0, s>>>(in, n, ws, out);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Floyd membership (choice, replace=False): out[t] = vals[t] unless vals[t]
+// is already selected, in which case j_t = base + t (coo.py:486 / trainer.py:322
+// -> Generator.choice).  c_t = !first_t || (vals[t]-base in [0,t) && c_{vals[t]-base}).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t mix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+
+__global__ void floyd_insert_kernel(const uint32_t* __restrict__ vals, long long k, uint32_t* keys, int* mint,
+                                    uint32_t hmask) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; t < k; t += stride) {
+    uint32_t v = vals[t];
+    uint32_t slot = mix32(v) & hmask;
+    while (true) {
+      uint32_t old = atomicCAS(&keys[slot], 0xffffffffu, v);
+      if (old == 0xffffffffu || old == v) {
+        atomicMin(&mint[slot], (int)t);
+        break;
+      }
+      slot = (slot + 1) & hmask;
+    }
+  }
+}
+
+__global__ void floyd_first_kernel(const uint32_t* __restrict__ vals, long long k, const uint32_t* keys,
+                                   const int* mint, uint32_t hmask, unsigned char* first) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; t < k; t += stride) {
+    uint32_t v = vals[t];
+    uint32_t slot = mix32(v) & hmask;
+    while (keys[slot] != v) slot = (slot + 1) & hmask;
+    first[t] = mint[slot] == (int)t;
+  }
+}
+
+__global__ void floyd_out_kernel(const uint32_t* __restrict__ vals, long long k, long long base,
+                                 const unsigned char* __restrict__ first, int* __restrict__ out) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; t < k; t += stride) {
+    long long x = t;
+    int c = 0;
+    while (true) {
+      if (!first[x]) {
+        c = 1;
+        break;
+      }
+      long long jm = (long long)vals[x] - base;
+      if (jm < 0 || jm >= x) {
+        c = 0;
+        break;
+      }
+      x = jm;
+    }
+    out[t] = c ? (int)(base + t) : (int)vals[t];
+  }
+}
+
+__global__ void gather_kernel(const int* __restrict__ src, const int* __restrict__ perm, long long n,
+                              int* __restrict__ dst) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) dst[i] = src[perm[i]];
+}
+
+__global__ void iota_kernel(int* __restrict__ out, long long n, int offset) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) out[i] = (int)i + offset;
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+static inline unsigned grid_for(long long n, int threads, int cap = 148 * 32) {
+  long long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+static Pcg64 make_pcg(const uint64_t st[4]) {
+  Pcg64 g;
+  g.state = ((u128)st[0] << 64) | st[1];
+  g.inc = ((u128)st[2] << 64) | st[3];
+  return g;
+}
+
+// segments with mask < 2^K_SMALL are walked by one warp
+static const int K_SMALL = 12;
+
+struct SegPlan {
+  Seg sg;
+  int L, C, Delta;
+};
+
+static SegPlan plan_segment(long long n, int k) {
+  SegPlan sp;
+  long long hi = (1LL << k) - 1;
+  if (hi > n - 1) hi = n - 1;
+  long long lo = 1LL << (k - 1);
+  sp.sg.hi = (int)hi;
+  sp.sg.mask = (unsigned)((1ULL << k) - 1);
+  sp.sg.S = (int)(hi - lo + 1);
+  double M = (double)sp.sg.mask + 1.0;
+  // E[#positions] = sum_{i=lo}^{hi} M/(i+1); Var = sum (1-p)/p^2 with p=(i+1)/M
+  double mean = M * (log((hi + 1.5) / (lo + 0.5)));
+  double var = M * M * (1.0 / (lo + 0.5) - 1.0 / (hi + 1.5)) - mean;
+  if (var < 0) var = 0;
+  double bound = mean + 12.0 * sqrt(var) + 1024.0;
+  sp.Delta = (int)ceil(4.0 * sqrt(mean) + 64.0);
+  double Lf = M * 4.0 / (2.0 * sp.Delta);
+  int L = 64;
+  while (L * 2 <= Lf && L < 4096) L *= 2;
+  sp.L = L;
+  sp.C = (int)ceil(bound / L);
+  return sp;
+}
+
+static const int PERM_E = 32;
+
+size_t perm_ws_bytes(long long n) {
+  // j-generation chunk buffers
+  size_t chunks = 0;
+  if (n >= 2) {
+    int kmax = 64 - __builtin_clzll((unsigned long long)(n - 1));
+    for (int k = kmax; k > K_SMALL; --k) {
+      SegPlan sp = plan_segment(n, k);
+      if ((size_t)sp.C > chunks) chunks = sp.C;
+    }
+  }
+  size_t b = 0;
+  b += 64 * sizeof(long long) + 64;            // P + meta
+  b += chunks * (4 * sizeof(int) + PERM_E * sizeof(int2)) + 256;
+  // j (n+1) + apply: cnt, start, list, parent, val (+ scan ws)
+  b += (size_t)(6 * (n + 2)) * sizeof(int) + scan_ws_bytes(n + 1) + 16 * 256;
+  return b;
+}
+
+struct Carve {
+  char* p;
+  size_t left;
+  bool overflow = false;
+  template <typename T>
+  T* take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
+    if (bytes > left) {
+      overflow = true;
+      return (T*)p;
+    }
+    T* r = (T*)p;
+    p += bytes;
+    left -= bytes;
+    return r;
+  }
+  bool ok() const { return !overflow; }
+};
+
+// j-sequence of Generator.permutation(n) into j_out[1..n-1]; j_out[0] = 0.
+int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* d_meta,
+              cudaStream_t s) {
+  if (n < 2) return 0;
+  int kmax = 64 - __builtin_clzll((unsigned long long)(n - 1));
+  size_t chunks = 0;
+  for (int k = kmax; k > K_SMALL; --k) {
+    SegPlan sp = plan_segment(n, k);
+    if ((size_t)sp.C > chunks) chunks = sp.C;
+  }
+  ChunkBuf cb;
+  cb.E = PERM_E;
+  cb.a0 = cv.take<int>(chunks + 1);
+  cb.D = cv.take<int>(chunks + 1);
+  cb.cnt = cv.take<int>(chunks + 1);
+  cb.a_in = cv.take<int>(chunks + 1);
+  cb.ent = cv.take<int2>((chunks + 1) * PERM_E);
+  SPTK_REQUIRE(cv.ok(), "permutation: workspace too small");
+  SPTK_CUDA_TRY(cudaMemsetAsync(d_P, 0, sizeof(long long) * 66, s));
+  int k = kmax;
+  int slot = 0;  // d_P[slot] = start of segment k
+  for (; k > K_SMALL; --k, ++slot) {
+    SegPlan sp = plan_segment(n, k);
+    const int warps_per_block = 8;
+    unsigned blocks = (unsigned)((sp.C + warps_per_block - 1) / warps_per_block);
+    perm_phaseA_kernel<<<blocks, 32 * warps_per_block, 0, s>>>(g, d_P + slot, sp.sg, sp.L, sp.C,
+                                                               sp.Delta, cb);
+    SPTK_CHECK_LAUNCH();
+    perm_resolve_kernel<<<1, 32, 0, s>>>(g, d_P + slot, sp.sg, sp.L, sp.C, sp.Delta, cb,
+                                         d_meta + slot);
+    SPTK_CHECK_LAUNCH();
+    perm_phaseB_kernel<<<blocks, 32 * warps_per_block, 0, s>>>(g, d_P + slot, sp.sg, sp.L, sp.C,
+                                                               cb, d_meta + slot, j_out);
+    SPTK_CHECK_LAUNCH();
+  }
+  perm_small_kernel<<<1, 32, 0, s>>>(g, d_P + slot, k, n, j_out, d_P + 65);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// result[i] for i in [first, n) of applying steps i = n-1..first with j[i].
+// If first <= 1 the virtual step 0 (j[0] = 0) is included so result[0] is
+// produced too.
+int fy_apply(int* j, long long n, long long first, int* result, Carve& cv, cudaStream_t s) {
+  if (n <= 0) return 0;
+  long long f = first <= 1 ? 0 : first;
+  if (f == 0) SPTK_CUDA_TRY(cudaMemsetAsync(j, 0, sizeof(int), s));
+  int* cnt = cv.take<int>(n + 1);
+  int* start = cv.take<int>(n + 2);
+  int* list = cv.take<int>(n + 1);
+  int* parent = cv.take<int>(n + 1);
+  int* val = cv.take<int>(n + 1);
+  int* sws = cv.take<int>(scan_ws_bytes(n + 1) / sizeof(int) + 1);
+  SPTK_REQUIRE(cv.ok(), "fy_apply: workspace too small");
+  SPTK_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (n + 1), s));
+  unsigned gb = grid_for(n - f, 256);
+  fy_hist_kernel<<<gb, 256, 0, s>>>(j, f, n, cnt);
+  SPTK_CHECK_LAUNCH();
+  if (exclusive_scan(cnt, n, start, sws, s)) return 1;
+  SPTK_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (n + 1), s));
+  fy_scatter_kernel<<<gb, 256, 0, s>>>(j, f, n, start, cnt, list);
+  SPTK_CHECK_LAUNCH();
+  unsigned gn = grid_for(n, 256);
+  fy_bucket_kernel<<<gn, 256, 0, s>>>(start, list, n, parent);
+  SPTK_CHECK_LAUNCH();
+  fy_val_kernel<<<gn, 256, 0, s>>>(parent, n, val);
+  SPTK_CHECK_LAUNCH();
+  fy_result_kernel<<<gn, 256, 0, s>>>(start, list, val, n, result);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+int permutation(const uint64_t st[4], long long n, int* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+  SPTK_REQUIRE(n >= 0 && n < (1LL << 30), "permutation: n=%lld out of range [0, 2^30)", n);
+  SPTK_REQUIRE(ws_bytes >= perm_ws_bytes(n), "permutation: workspace too small (%zu < %zu)", ws_bytes,
+               perm_ws_bytes(n));
+  if (n == 0) return 0;
+  if (n == 1) {
+    SPTK_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(int), s));
+    return 0;
+  }
+  Carve cv{(char*)ws, ws_bytes};
+  long long* d_P = cv.take<long long>(66);
+  int* d_meta = cv.take<int>(66);
+  int* j = cv.take<int>(n + 1);
+  Pcg64 g = make_pcg(st);
+  if (perm_jgen(g, n, j, cv, d_P, d_meta, s)) return 1;
+  return fy_apply(j, n, 1, out, cv, s);
+}
+
+// j-sequence only (tests): j_out[i] for i in [1, n)
+int permutation_j(const uint64_t st[4], long long n, int* j_out, void* ws, size_t ws_bytes, cudaStream_t s) {
+  SPTK_REQUIRE(n >= 0 && n < (1LL << 30), "permutation_j: n out of range");
+  SPTK_REQUIRE(ws_bytes >= perm_ws_bytes(n), "permutation_j: workspace too small");
+  if (n < 2) return 0;
+  Carve cv{(char*)ws, ws_bytes};
+  long long* d_P = cv.take<long long>(66);
+  int* d_meta = cv.take<int>(66);
+  Pcg64 g = make_pcg(st);
+  return perm_jgen(g, n, j_out, cv, d_P, d_meta, s);
+}
+
+// --- choice ---------------------------------------------------------------
+static long long lemire_vcap(long long T, double p_rej_max) {
+  double mean = T * p_rej_max / (1.0 - p_rej_max);
+  return T + (long long)(mean + 12.0 * sqrt(mean + 1.0) + 64.0) + LEM_BITS + 64;
+}
+
+static size_t apply_ws_bytes(long long n) {
+  return (size_t)(5 * (n + 2)) * sizeof(int) + scan_ws_bytes(n + 1) + 8 * 256;
+}
+
+size_t choice_ws_bytes(long long pop, long long k) {
+  size_t pad = 64 * 256;
+  size_t b_tail = 0, b_floyd = 0;
+  {
+    long long first = pop - k > 1 ? pop - k : 1;
+    long long T = pop - first;
+    b_tail = (size_t)(pop + 1) * 4 * 2 + (size_t)lemire_vcap(T > 0 ? T : 1, (double)pop / 4294967296.0) * 4 +
+             (size_t)(T + 1) * 4 + apply_ws_bytes(pop);
+  }
+  {
+    long long hs = 1;
+    while (hs < 2 * k + 2) hs <<= 1;
+    b_floyd = (size_t)(k + 1) * 4 * 3 + (size_t)lemire_vcap(k + 1, (double)pop / 4294967296.0) * 4 +
+              (size_t)hs * 8 + (size_t)(k + 1) + (size_t)(k + 1) * 4 * 3 +
+              (size_t)lemire_vcap(k + 1, (double)k / 4294967296.0) * 4 + apply_ws_bytes(k);
+  }
+  return pad + (b_tail > b_floyd ? b_tail : b_floyd);
+}
+
+__global__ void reverse_into_kernel(const uint32_t* __restrict__ tmp, long long T, long long n,
+                                    int* __restrict__ j) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; t < T; t += stride) j[n - 1 - t] = (int)tmp[t];
+}
+
+// Lemire j's for _shuffle_int(n, first): steps i = n-1..first, stream from q0.
+static int shuffle_int_jgen(Pcg64 g, long long q0, long long n, long long first, int* j, Carve& cv,
+                            long long* d_qend, int* d_err, cudaStream_t s) {
+  long long T = n - first;
+  if (T <= 0) return 0;
+  double p = (double)n / 4294967296.0;
+  long long vcap = lemire_vcap(T, p);
+  uint32_t* v = cv.take<uint32_t>(vcap);
+  uint32_t* tmp = cv.take<uint32_t>(T);
+  SPTK_REQUIRE(cv.ok(), "sampler workspace too small");
+  u32_stream_kernel<<<grid_for(vcap, 256), 256, 0, s>>>(g, (unsigned long long)q0, vcap, v);
+  SPTK_CHECK_LAUNCH();
+  lemire_resolve_kernel<<<1, LEM_B, 0, s>>>(v, vcap, T, n - 1, -1, tmp, d_qend, d_err);
+  SPTK_CHECK_LAUNCH();
+  reverse_into_kernel<<<grid_for(T, 256), 256, 0, s>>>(tmp, T, n, j);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// Generator.choice(pop, k, replace=False, shuffle=shuffle) -> out[k] (int32).
+// With shuffle=0 the Floyd set is returned in draw order (same set; training
+// only needs the set).  The tail-shuffle path is always exact.
+int choice(const uint64_t st[4], long long pop, long long k, int shuffle, int* out, void* ws,
+           size_t ws_bytes, int* path_out, cudaStream_t s) {
+  SPTK_REQUIRE(pop >= 0 && pop < (1LL << 30) && k >= 0 && k <= pop, "choice: bad pop=%lld k=%lld", pop, k);
+  SPTK_REQUIRE(ws_bytes >= choice_ws_bytes(pop, k), "choice: workspace too small");
+  Carve cv{(char*)ws, ws_bytes};
+  long long* d_q = cv.take<long long>(4);
+  int* d_err = cv.take<int>(4);
+  SPTK_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int) * 4, s));
+  Pcg64 g = make_pcg(st);
+  if (pop > 10000 && k > pop / 50) {
+    if (path_out) *path_out = 1;
+    long long first = pop - k > 1 ? pop - k : 1;
+    int* j = cv.take<int>(pop + 1);
+    if (shuffle_int_jgen(g, 0, pop, first, j, cv, d_q, d_err, s)) return 1;
+    int* res = cv.take<int>(pop + 1);
+    if (fy_apply(j, pop, first, res, cv, s)) return 1;
+    SPTK_CUDA_TRY(cudaMemcpyAsync(out, res + (pop - k), sizeof(int) * k, cudaMemcpyDeviceToDevice, s));
+    return 0;
+  }
+  if (path_out) *path_out = 2;
+  if (k == 0) return 0;
+  // Floyd draws: t = 0..k-1, rng = pop-k+t (rng == 0 returns 0 without a draw)
+  long long base = pop - k;
+  long long t_begin = 0;
+  uint32_t* vals = cv.take<uint32_t>(k + 1);
+  if (base == 0) {
+    SPTK_CUDA_TRY(cudaMemsetAsync(vals, 0, sizeof(uint32_t), s));
+    t_begin = 1;
+  }
+  long long T = k - t_begin;
+  double p = (double)pop / 4294967296.0;
+  long long vcap = lemire_vcap(T, p);
+  uint32_t* v = cv.take<uint32_t>(vcap);
+  if (T > 0) {
+    u32_stream_kernel<<<grid_for(vcap, 256), 256, 0, s>>>(g, 0ULL, vcap, v);
+    SPTK_CHECK_LAUNCH();
+    lemire_resolve_kernel<<<1, LEM_B, 0, s>>>(v, vcap, T, base + t_begin, +1, vals + t_begin, d_q, d_err);
+    SPTK_CHECK_LAUNCH();
+  } else {
+    SPTK_CUDA_TRY(cudaMemsetAsync(d_q, 0, sizeof(long long), s));
+  }
+  long long hs = 1;
+  while (hs < 2 * k + 2) hs <<= 1;
+  uint32_t* keys = cv.take<uint32_t>(hs);
+  int* mint = cv.take<int>(hs);
+  unsigned char* first = cv.take<unsigned char>(k + 1);
+  SPTK_CUDA_TRY(cudaMemsetAsync(keys, 0xff, sizeof(uint32_t) * hs, s));
+  SPTK_CUDA_TRY(cudaMemsetAsync(mint, 0x7f, sizeof(int) * hs, s));
+  floyd_insert_kernel<<<grid_for(k, 256), 256, 0, s>>>(vals, k, keys, mint, (uint32_t)(hs - 1));
+  SPTK_CHECK_LAUNCH();
+  floyd_first_kernel<<<grid_for(k, 256), 256, 0, s>>>(vals, k, keys, mint, (uint32_t)(hs - 1), first);
+  SPTK_CHECK_LAUNCH();
+  int* sel = shuffle ? cv.take<int>(k + 1) : out;
+  floyd_out_kernel<<<grid_for(k, 256), 256, 0, s>>>(vals, k, base, first, sel);
+  SPTK_CHECK_LAUNCH();
+  if (!shuffle || k < 2) {
+    if (shuffle && k == 1) SPTK_CUDA_TRY(cudaMemcpyAsync(out, sel, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    return 0;
+  }
+  // _shuffle_int(k, 1, idx): continues the stream after the Floyd draws.
+  // The stream offset lives on the device (d_q), so read it back (one small
+  // sync, only on the exact-output path used by tests / the public API).
+  long long qend = 0;
+  SPTK_CUDA_TRY(cudaMemcpyAsync(&qend, d_q, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  int herr = 0;
+  SPTK_CUDA_TRY(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPTK_CUDA_TRY(cudaStreamSynchronize(s));
+  SPTK_REQUIRE(herr == 0, "choice: Lemire stream overflow");
+  int* j = cv.take<int>(k + 1);
+  if (shuffle_int_jgen(g, qend, k, 1, j, cv, d_q, d_err, s)) return 1;
+  int* perm = cv.take<int>(k + 1);
+  if (fy_apply(j, k, 1, perm, cv, s)) return 1;
+  gather_kernel<<<grid_for(k, 256), 256, 0, s>>>(sel, perm, k, out);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+int u32_stream(const uint64_t st[4], unsigned long long q0, long long n, uint32_t* out, cudaStream_t s) {
+  Pcg64 g = make_pcg(st);
+  if (n <= 0) return 0;
+  u32_stream_kernel<<<grid_for(n, 256), 256, 0, s>>>(g, q0, n, out);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+int iota(int* out, long long n, int offset, cudaStream_t s) {
+  if (n <= 0) return 0;
+  iota_kernel<<<grid_for(n, 256), 256, 0, s>>>(out, n, offset);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace sptk

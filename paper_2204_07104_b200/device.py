@@ -1,0 +1,126 @@
+"""Device-resident model and nonzeros, plus thin wrappers over libsptk.
+
+PyTorch is used only to own device memory and to supply the current stream;
+all arithmetic happens in the sm_100a kernels behind include/sptk.h.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, f64arr, i64arr, ptr, stream_ptr
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def record_words(order: int, f64: bool) -> int:
+    return int(_lib.load().sptk_record_words(order, 1 if f64 else 0))
+
+
+class DeviceModel:
+    """Packed A(n)/B(n) on the device in the reference's layout
+    (trainer.py:135-141, _loops.py:8-10), fp32 (throughput) or fp64
+    (verification)."""
+
+    def __init__(self, model, f64: bool = False, device=None):
+        torch = _torch()
+        _lib.require_cuda()
+        self.device = torch.device(device or "cuda")
+        self.f64 = f64
+        self.dtype = torch.float64 if f64 else torch.float32
+        self.order = model.order
+        self.dims = tuple(model.dims)
+        self.rcore = int(model.r_core)
+        self.jr = np.asarray(model.j_ranks, dtype=np.int64)
+        sizes_a = [d * j for d, j in zip(model.dims, model.j_ranks)]
+        sizes_b = [j * model.r_core for j in model.j_ranks]
+        self.foff = np.concatenate([[0], np.cumsum(sizes_a)]).astype(np.int64)
+        self.coff = np.concatenate([[0], np.cumsum(sizes_b)]).astype(np.int64)
+        npdt = np.float64 if f64 else np.float32
+        fac = np.concatenate([np.asarray(a, dtype=np.float64).ravel() for a in model.factors]).astype(npdt)
+        cor = np.concatenate([np.asarray(b, dtype=np.float64).ravel() for b in model.core_factors]).astype(npdt)
+        self.fac = torch.from_numpy(fac).to(self.device)
+        self.cor = torch.from_numpy(cor).to(self.device)
+        self.cor_size = int(self.coff[-1])
+        # ctypes views of the small host arrays (kept alive on self)
+        self._foff, self.p_foff = i64arr(self.foff)
+        self._coff, self.p_coff = i64arr(self.coff)
+        self._jr, self.p_jr = i64arr(self.jr)
+
+    def download_into(self, model) -> None:
+        fac = self.fac.double().cpu().numpy()
+        cor = self.cor.double().cpu().numpy()
+        for n, a in enumerate(model.factors):
+            np.copyto(a, fac[self.foff[n]: self.foff[n + 1]].reshape(a.shape))
+        for n, b in enumerate(model.core_factors):
+            np.copyto(b, cor[self.coff[n]: self.coff[n + 1]].reshape(b.shape))
+
+
+class DeviceCoo:
+    """Nonzeros as packed device records {i_0..i_{N-1}, value} in source order."""
+
+    def __init__(self, indices: np.ndarray, values: np.ndarray, f64: bool = False, device=None):
+        torch = _torch()
+        _lib.require_cuda()
+        dev = torch.device(device or "cuda")
+        idx = np.ascontiguousarray(indices, dtype=np.int64)
+        self.nnz = int(idx.shape[0])
+        self.order = int(idx.shape[1])
+        self.f64 = f64
+        self.rw = record_words(self.order, f64)
+        self.rec = torch.empty(max(self.nnz, 1) * self.rw, dtype=torch.int32, device=dev)
+        if self.nnz:
+            d_idx = torch.from_numpy(idx).to(dev)
+            d_val = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(dev)
+            check(_lib.load().sptk_pack_records(ptr(d_idx), ptr(d_val), self.nnz, self.order,
+                                                1 if f64 else 0, ptr(self.rec), stream_ptr()),
+                  "sptk_pack_records")
+            del d_idx, d_val
+
+
+def eval_sums(dm: DeviceModel, coo: DeviceCoo, sums=None):
+    """Launch K6 and return the device (2,) fp64 tensor {sum sq, sum abs}."""
+    torch = _torch()
+    L = _lib.load()
+    if sums is None:
+        sums = torch.zeros(2, dtype=torch.float64, device=dm.fac.device)
+    fn = L.sptk_eval_f64 if dm.f64 else L.sptk_eval
+    check(fn(ptr(coo.rec), coo.rw, coo.nnz, ptr(dm.fac), dm.p_foff, ptr(dm.cor), dm.p_coff, dm.p_jr,
+             dm.order, dm.rcore, None, ptr(sums), stream_ptr()), "sptk_eval")
+    return sums
+
+
+def rmse_mae_device(dm: DeviceModel, coo: DeviceCoo):
+    if coo.nnz == 0:
+        raise ValueError("dataset is empty")
+    s = eval_sums(dm, coo).cpu().numpy()
+    return float(np.sqrt(s[0] / coo.nnz)), float(s[1] / coo.nnz)
+
+
+def predict_device(model, indices: np.ndarray) -> np.ndarray:
+    torch = _torch()
+    dm = DeviceModel(model)
+    m = indices.shape[0]
+    coo = DeviceCoo(indices, np.zeros(m), f64=False)
+    out = torch.empty(max(m, 1), dtype=torch.float32, device=dm.fac.device)
+    L = _lib.load()
+    check(L.sptk_eval(ptr(coo.rec), coo.rw, m, ptr(dm.fac), dm.p_foff, ptr(dm.cor), dm.p_coff, dm.p_jr,
+                      dm.order, dm.rcore, ptr(out), None, stream_ptr()), "sptk_eval")
+    return out[:m].double().cpu().numpy()
+
+
+def predict_device_f64(model, indices: np.ndarray) -> np.ndarray:
+    """fp64 device evaluation (used for data synthesis at scale)."""
+    torch = _torch()
+    dm = DeviceModel(model, f64=True)
+    m = indices.shape[0]
+    coo = DeviceCoo(indices, np.zeros(m), f64=True)
+    out = torch.empty(max(m, 1), dtype=torch.float64, device=dm.fac.device)
+    check(_lib.load().sptk_eval_f64(ptr(coo.rec), coo.rw, m, ptr(dm.fac), dm.p_foff, ptr(dm.cor), dm.p_coff,
+                                    dm.p_jr, dm.order, dm.rcore, ptr(out), None, stream_ptr()), "sptk_eval_f64")
+    return out[:m].cpu().numpy()

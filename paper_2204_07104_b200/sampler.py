@@ -1,0 +1,100 @@
+"""Bit-exact device samplers (K2) behind the reference's RNG calls.
+
+``pcg64_state(entropy)`` reproduces ``np.random.default_rng(entropy)``'s
+PCG64 seeding (SeedSequence) in the C library; ``permutation`` and ``choice``
+return the exact arrays numpy 2.x's Generator.permutation /
+Generator.choice(replace=False) produce for that state
+(trainer.py:300-303 and 317-324), computed on the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, ptr, stream_ptr, u64arr
+
+
+def pcg64_state(entropy) -> np.ndarray:
+    """(state_hi, state_lo, inc_hi, inc_lo) of default_rng(entropy)."""
+    ent, p = u64arr([int(e) for e in entropy])
+    out = np.zeros(4, dtype=np.uint64)
+    check(_lib.load().sptk_pcg64_seed(p, len(ent), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))),
+          "sptk_pcg64_seed")
+    return out
+
+
+class Workspace:
+    """Grow-only device scratch buffer."""
+
+    def __init__(self, device=None):
+        self.buf = None
+        self.device = device
+
+    def get(self, nbytes: int):
+        import torch
+
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=self.device or "cuda")
+        return self.buf
+
+
+def permutation(entropy, n: int, out=None, ws: Workspace | None = None, state=None):
+    """Device int32 tensor == default_rng(entropy).permutation(n)."""
+    import torch
+
+    _lib.require_cuda()
+    L = _lib.load()
+    st = state if state is not None else pcg64_state(entropy)
+    stc, sp = u64arr(st)
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    need = int(L.sptk_permutation_ws_bytes(n))
+    w = (ws or Workspace()).get(need)
+    check(L.sptk_permutation(sp, n, ptr(out), ptr(w), w.numel(), stream_ptr()), "sptk_permutation")
+    return out[:n] if n else out[:0]
+
+
+def permutation_j(entropy, n: int):
+    """The Fisher-Yates index sequence j_i (i = 1..n-1) of permutation(n)."""
+    import torch
+
+    _lib.require_cuda()
+    L = _lib.load()
+    stc, sp = u64arr(pcg64_state(entropy))
+    out = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+    w = Workspace().get(int(L.sptk_permutation_ws_bytes(n)))
+    check(L.sptk_permutation_j(sp, n, ptr(out), ptr(w), w.numel(), stream_ptr()), "sptk_permutation_j")
+    return out[:n]
+
+
+def choice(entropy, pop: int, k: int, shuffle: bool = True, out=None, ws: Workspace | None = None,
+           state=None):
+    """Device int32 tensor == default_rng(entropy).choice(pop, k, replace=False)
+    (shuffle=False: the same set, in Floyd draw order).  Returns (ids, path)."""
+    import torch
+
+    _lib.require_cuda()
+    L = _lib.load()
+    st = state if state is not None else pcg64_state(entropy)
+    stc, sp = u64arr(st)
+    if out is None:
+        out = torch.empty(max(k, 1), dtype=torch.int32, device="cuda")
+    need = int(L.sptk_choice_ws_bytes(pop, k))
+    w = (ws or Workspace()).get(need)
+    path = ctypes.c_int(0)
+    check(L.sptk_choice(sp, pop, k, 1 if shuffle else 0, ptr(out), ptr(w), w.numel(), ctypes.byref(path),
+                        stream_ptr()), "sptk_choice")
+    return out[:k], ("tail" if path.value == 1 else "floyd")
+
+
+def u32_stream(entropy, n: int, q0: int = 0):
+    import torch
+
+    _lib.require_cuda()
+    stc, sp = u64arr(pcg64_state(entropy))
+    out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    check(_lib.load().sptk_u32_stream(sp, q0, n, ptr(out), stream_ptr()), "sptk_u32_stream")
+    return out[:n]

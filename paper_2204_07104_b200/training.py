@@ -1,0 +1,319 @@
+"""Epoch driver: the B200 replacement for the reference's ``train`` hot path.
+
+Mirrors sptucker/trainer.py (TrainConfig, MetricsRow, learning_rate, rmse,
+mae, frobenius_objective, train, write_metrics_csv) with the same signatures,
+defaults, validation messages and metric semantics.  Inside ``train`` every
+step of an epoch runs on the GPU, enqueued on one stream with no host
+round-trip:
+
+    for each round of the DSGD schedule, for each block      (trainer.py:294-312)
+        visit = K2 permutation(default_rng([seed,1,t,*block]))   bit-exact
+        K3 factor pass over the block's records in visit order
+    core batch Psi = arange / K2 choice(default_rng([seed,2,t]))  (trainer.py:316-324)
+    K4 core-gradient reduction over Psi, K5 apply              (trainer.py:325-351)
+
+``wall_seconds`` is device time between CUDA events around that work (the
+reference's perf_counter interval, trainer.py:291/353), evaluation excluded.
+
+Two update modes (extra TrainConfig fields, defaults keep the reference's
+call signature working):
+  update_mode="hogwild"     throughput: thread-per-sample Hogwild factor
+                            kernel in visit order (cuFastTucker's scheme).
+  update_mode="sequential"  verification: visit lists applied strictly in
+                            order with the reference's operation order, core
+                            batch split and merged like np.array_split.
+  precision="fp32"|"fp64"   device arithmetic; fp64 + sequential reproduces the
+                            reference to rounding.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, f64arr, ptr, stream_ptr
+from .device import DeviceCoo, DeviceModel, rmse_mae_device
+from .sampler import Workspace, choice, pcg64_state, permutation
+from .schedule import DevicePartition, round_schedule
+from .tensor import DatasetSplit, SparseTensorCoo
+from .tucker import TuckerModel
+
+METRICS_HEADER = "epoch,wall_seconds,train_rmse,train_mae,test_rmse,test_mae,gamma_a,gamma_b"
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """Schedule, regularisation and parallelism (trainer.py:29-63 defaults)."""
+
+    epochs: int
+    workers: int = 1
+    update_core: bool = True
+    alpha_a: float = 0.009
+    beta_a: float = 0.05
+    lambda_a: float = 0.01
+    alpha_b: float = 0.0045
+    beta_b: float = 0.1
+    lambda_b: float = 0.01
+    core_batch_cap: int = 1 << 20
+    seed: int = 0
+    eval_every: int = 1
+    core_average: bool = True
+    update_mode: str = "hogwild"
+    precision: str = "fp32"
+
+    def __post_init__(self):
+        if self.epochs < 1:
+            raise ValueError("epochs must be >= 1")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        for name in ("alpha_a", "beta_a", "lambda_a", "alpha_b", "beta_b", "lambda_b"):
+            if getattr(self, name) < 0:
+                raise ValueError(f"{name} must be >= 0")
+        if self.core_batch_cap < 1:
+            raise ValueError("core_batch_cap must be >= 1")
+        if self.eval_every < 1:
+            raise ValueError("eval_every must be >= 1")
+        if self.update_mode not in ("hogwild", "sequential"):
+            raise ValueError("update_mode must be 'hogwild' or 'sequential'")
+        if self.precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be 'fp32' or 'fp64'")
+
+
+@dataclass(frozen=True)
+class MetricsRow:
+    """One evaluation snapshot; test metrics are NaN without a test set."""
+
+    epoch: int
+    wall_seconds: float
+    train_rmse: float
+    train_mae: float
+    test_rmse: float
+    test_mae: float
+    gamma_a: float
+    gamma_b: float
+
+
+def learning_rate(alpha: float, beta: float, t: int) -> float:
+    """alpha / (1 + beta * t^1.5) (trainer.py:80-86)."""
+    if alpha < 0 or beta < 0:
+        raise ValueError("alpha and beta must be >= 0")
+    if t < 0:
+        raise ValueError("t must be >= 0")
+    return alpha / (1.0 + beta * float(t) ** 1.5)
+
+
+def _metric(model: TuckerModel, dataset: SparseTensorCoo):
+    if dataset.nnz == 0:
+        raise ValueError("dataset is empty")
+    return rmse_mae_device(DeviceModel(model), DeviceCoo(dataset.indices, dataset.values))
+
+
+def rmse(model: TuckerModel, dataset: SparseTensorCoo) -> float:
+    """Root-mean-square error over the dataset (K6 on the device)."""
+    return _metric(model, dataset)[0]
+
+
+def mae(model: TuckerModel, dataset: SparseTensorCoo) -> float:
+    """Mean absolute error over the dataset (K6 on the device)."""
+    return _metric(model, dataset)[1]
+
+
+MAX_CORE_ELEMENTS = 10**6
+
+
+def frobenius_objective(model: TuckerModel, dataset: SparseTensorCoo, lambda_core: float = 0.0,
+                        lambda_factors: float = 0.0) -> float:
+    """Observed squared loss plus ridge penalties (trainer.py:105-132).
+
+    The squared loss comes from K6; the penalties are small host reductions
+    (the core penalty needs the dense core, only formed when prod J_n <= 1e6).
+    """
+    if dataset.nnz == 0:
+        raise ValueError("dataset is empty")
+    dm = DeviceModel(model, f64=True)
+    s = rmse_mae_device(dm, DeviceCoo(dataset.indices, dataset.values, f64=True))
+    total = s[0] ** 2 * dataset.nnz
+    if lambda_core != 0.0:
+        if math.prod(model.j_ranks) <= MAX_CORE_ELEMENTS:
+            dense = _dense_core(model.core_factors)
+            total += lambda_core * float(dense.ravel() @ dense.ravel())
+        else:
+            warnings.warn("core penalty not computed: dense core exceeds size cap", stacklevel=2)
+    if lambda_factors != 0.0:
+        total += lambda_factors * sum(float(np.vdot(a, a)) for a in model.factors)
+    return total
+
+
+def _dense_core(core_factors):
+    g = None
+    for b in core_factors:
+        g = b if g is None else np.einsum("...r,jr->...jr", g, b)
+    return g.sum(axis=-1)
+
+
+# --------------------------------------------------------------------------
+# device epoch runner
+# --------------------------------------------------------------------------
+class EpochRunner:
+    """Device state for one training run on one GPU (workers = DSGD M)."""
+
+    def __init__(self, model: TuckerModel, train_set: SparseTensorCoo, config: TrainConfig):
+        import torch
+
+        _lib.require_cuda()
+        self.torch = torch
+        self.cfg = config
+        self.f64 = config.precision == "fp64"
+        self.mode = 1 if config.update_mode == "sequential" else 0
+        self.m = int(config.workers)
+        self.order = model.order
+        self.nnz = train_set.nnz
+        self.dm = DeviceModel(model, f64=self.f64)
+        self.part = DevicePartition(train_set.indices, train_set.values, model.dims, self.m, f64=self.f64,
+                                    want_ids=False)
+        self.schedule = round_schedule(model.order, self.m)
+        # host list of (block, offset, count) per round, empty blocks dropped
+        self.rounds = []
+        for rnd in self.schedule.rounds:
+            items = []
+            for block in rnd:
+                off, cnt = self.part.block_range(block)
+                if cnt > 0:
+                    items.append((block, off, cnt))
+            self.rounds.append(items)
+        self.max_block = max((c for r in self.rounds for (_, _, c) in r), default=0)
+        dev = self.dm.fac.device
+        self.perm_buf = torch.empty(max(self.max_block, 1), dtype=torch.int32, device=dev)
+        self.perm_ws = Workspace(dev)
+        self.k = min(self.nnz, int(config.core_batch_cap))
+        self.psi_buf = torch.empty(max(self.k, 1), dtype=torch.int32, device=dev)
+        self.psi_ws = Workspace(dev)
+        self.acc = torch.zeros(max(self.dm.cor_size, 1), dtype=torch.float64, device=dev)
+        L = _lib.load()
+        chunks = self.m if self.mode == 1 else 0
+        self.core_ws = torch.empty(int(L.sptk_core_ws_bytes(self.dm.p_jr, self.order, self.dm.rcore, chunks)),
+                                   dtype=torch.uint8, device=dev)
+        self.gam_np = np.zeros(self.order)
+        self.lam_np = np.full(self.order, float(config.lambda_a))
+        self._gam, self.p_gam = f64arr(self.gam_np)
+        self._lam, self.p_lam = f64arr(self.lam_np)
+        self.map = self.part.pos_of_id if self.m > 1 else None
+        self.L = L
+
+    def factor_phase(self, t: int, gamma_a: float) -> int:
+        cfg, L, dm = self.cfg, self.L, self.dm
+        self._gam[:] = gamma_a
+        fn = L.sptk_factor_pass_f64 if self.f64 else L.sptk_factor_pass
+        s = stream_ptr()
+        processed = 0
+        for items in self.rounds:
+            for block, off, cnt in items:
+                st = pcg64_state([cfg.seed, 1, t, *block])
+                perm = permutation(None, cnt, out=self.perm_buf, ws=self.perm_ws, state=st)
+                check(fn(ptr(self.part.rec), self.part.rw, ptr(perm), cnt, off, ptr(dm.fac), dm.p_foff,
+                         ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam,
+                         self.mode, s), "sptk_factor_pass")
+                processed += cnt
+        return processed
+
+    def core_phase(self, t: int, gamma_b: float) -> None:
+        cfg, L, dm = self.cfg, self.L, self.dm
+        k = self.k
+        if k == self.nnz:
+            visit = None
+        else:
+            visit, _ = choice(None, self.nnz, k, shuffle=(self.mode == 1), out=self.psi_buf,
+                              ws=self.psi_ws, state=pcg64_state([cfg.seed, 2, t]))
+        self.acc.zero_()
+        s = stream_ptr()
+        fn = L.sptk_core_pass_f64 if self.f64 else L.sptk_core_pass
+        chunks = self.m if self.mode == 1 else 0
+        check(fn(ptr(self.part.rec), self.part.rw, ptr(visit), ptr(self.map), k, ptr(dm.fac), dm.p_foff,
+                 ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, ptr(self.acc), chunks,
+                 ptr(self.core_ws), self.core_ws.numel(), s), "sptk_core_pass")
+        denom = float(k) if cfg.core_average else 1.0
+        ap = L.sptk_core_apply_f64 if self.f64 else L.sptk_core_apply
+        check(ap(ptr(dm.cor), ptr(self.acc), dm.cor_size, float(gamma_b), float(cfg.lambda_b), denom, s),
+              "sptk_core_apply")
+
+    def epoch(self, t: int, gamma_a: float, gamma_b: float) -> None:
+        processed = self.factor_phase(t, gamma_a)
+        if processed != self.nnz:
+            raise RuntimeError("partition did not cover every training entry")
+        if self.cfg.update_core:
+            self.core_phase(t, gamma_b)
+
+
+def train(model: TuckerModel, split: DatasetSplit, config: TrainConfig) -> list[MetricsRow]:
+    """Run the epochs in place on ``model``; returns the metric rows.
+
+    Same contract as trainer.train (trainer.py:150-271); the epoch work runs on
+    the current CUDA device.
+    """
+    train_set = split.train
+    if train_set.dims != model.dims:
+        raise ValueError("model dims do not match dataset dims")
+    if train_set.nnz == 0:
+        raise ValueError("training set is empty")
+    w = config.workers
+    if w > min(model.dims):
+        raise ValueError(f"workers={w} cannot partition dims {model.dims}")
+    import torch
+
+    from . import dist
+
+    if dist.active():
+        return dist.train_distributed(model, split, config)
+    runner = EpochRunner(model, train_set, config)
+    f64 = runner.f64
+    # evaluation sets: the training records are reused (all blocks); test packed once
+    test_coo = DeviceCoo(split.test.indices, split.test.values, f64=f64) if split.test.nnz else None
+    train_eval = _RecordView(runner.part)
+    rows: list[MetricsRow] = []
+    wall = 0.0
+    pending = []
+    for t in range(config.epochs):
+        ga = learning_rate(config.alpha_a, config.beta_a, t)
+        gb = learning_rate(config.alpha_b, config.beta_b, t)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        runner.epoch(t, ga, gb)
+        ev1.record()
+        pending.append((ev0, ev1))
+        if (t + 1) % config.eval_every == 0 or t == config.epochs - 1:
+            ev1.synchronize()
+            for a, b in pending:
+                wall += a.elapsed_time(b) / 1000.0
+            pending.clear()
+            tr = rmse_mae_device(runner.dm, train_eval)
+            te = rmse_mae_device(runner.dm, test_coo) if test_coo is not None else (math.nan, math.nan)
+            rows.append(MetricsRow(t + 1, wall, tr[0], tr[1], te[0], te[1], ga, gb))
+    runner.dm.download_into(model)
+    return rows
+
+
+class _RecordView:
+    """Adapter so the partitioned training records can be scored by K6."""
+
+    def __init__(self, part: DevicePartition):
+        self.rec = part.rec
+        self.rw = part.rw
+        self.nnz = part.nnz
+        self.order = part.order
+
+
+def write_metrics_csv(rows, path) -> None:
+    """CSV in the fixed column order (trainer.py:274-282)."""
+    out = [METRICS_HEADER]
+    for r in rows:
+        out.append(",".join([str(r.epoch)] + [repr(v) for v in (r.wall_seconds, r.train_rmse, r.train_mae,
+                                                                 r.test_rmse, r.test_mae, r.gamma_a,
+                                                                 r.gamma_b)]))
+    with open(path, "w") as fh:
+        fh.write("\n".join(out) + "\n")

@@ -1,0 +1,203 @@
+"""K1/K3/K4/K5/K6 on the GPU against the reference's golden vectors and the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).cuda()
+
+
+def _loops_case(golden, c):
+    g = {k: golden[f"loops_{c}_{k}"] for k in ("jr", "fac", "foff", "cor", "coff", "idx", "vals", "visit",
+                                               "gam", "lam", "fac_out", "acc_out", "pred")}
+    g["r"] = int(golden[f"loops_{c}_r"])
+    g["dims"] = golden[f"loops_{c}_dims"]
+    return g
+
+
+def _records(idx, vals, f64):
+    from paper_2204_07104_b200.device import DeviceCoo
+
+    return DeviceCoo(idx, vals, f64=f64)
+
+
+def test_partition_golden(golden, golden_meta):
+    from paper_2204_07104_b200.schedule import DevicePartition, build_partition
+    from paper_2204_07104_b200.tensor import SparseTensorCoo
+
+    for c in range(golden_meta["n_part"]):
+        idx, dims, m = golden[f"part_{c}_idx"], golden[f"part_{c}_dims"], int(golden[f"part_{c}_m"])
+        dp = DevicePartition(idx, np.arange(len(idx), dtype=np.float64), dims, m)
+        assert np.array_equal(dp.ids[: len(idx)].cpu().numpy(), golden[f"part_{c}_ids"])
+        sizes = np.diff(dp.block_off)
+        assert np.array_equal(sizes[sizes > 0], golden[f"part_{c}_sizes"])
+        # records carry the grouped entries
+        rec = dp.rec.cpu().numpy().reshape(-1, dp.rw)[: len(idx)]
+        assert np.array_equal(rec[:, : idx.shape[1]], idx[golden[f"part_{c}_ids"]])
+        plan = build_partition(SparseTensorCoo(tuple(dims), idx, np.zeros(len(idx))), m)
+        want = {tuple(b) for b in golden[f"part_{c}_blocks"].tolist()}
+        assert set(plan.block_entries) == want
+
+
+def test_partition_many_blocks_stable():
+    """Keys needing two radix passes (m^N = 4096) stay stable."""
+    from paper_2204_07104_b200.schedule import DevicePartition
+
+    rng = np.random.default_rng(5)
+    dims = (64, 70, 80, 90)
+    idx = np.stack([rng.integers(0, d, 300_000) for d in dims], axis=1)
+    dp = DevicePartition(idx, np.zeros(len(idx)), dims, 8)
+    ids, _ = O.partition(idx, dims, 8)
+    assert np.array_equal(dp.ids[: len(idx)].cpu().numpy(), ids)
+
+
+@pytest.mark.parametrize("c", range(4))
+def test_factor_seq_fp64_bitwise(golden, c):
+    """Sequential fp64 mode reproduces numba's factor_pass bit for bit."""
+    from paper_2204_07104_b200 import _lib
+
+    g = _loops_case(golden, c)
+    L = _lib.load()
+    recs = _records(g["idx"], g["vals"], True)
+    fac = _dev(g["fac"], np.float64)
+    cor = _dev(g["cor"], np.float64)
+    visit = _dev(g["visit"], np.int32)
+    foff, pf = _lib.i64arr(g["foff"])
+    coff, pc = _lib.i64arr(g["coff"])
+    jr, pj = _lib.i64arr(g["jr"])
+    gam, pg = _lib.f64arr(g["gam"])
+    lam, pl = _lib.f64arr(g["lam"])
+    _lib.check(L.sptk_factor_pass_f64(recs.rec.data_ptr(), recs.rw, visit.data_ptr(), len(g["visit"]), 0,
+                                      fac.data_ptr(), pf, cor.data_ptr(), pc, pj, len(g["jr"]), g["r"], pg, pl, 1,
+                                      _lib.stream_ptr()), "factor")
+    np.testing.assert_array_equal(fac.cpu().numpy(), g["fac_out"])
+
+
+@pytest.mark.parametrize("c", range(4))
+def test_core_exact_fp64_bitwise(golden, c):
+    from paper_2204_07104_b200 import _lib
+
+    g = _loops_case(golden, c)
+    L = _lib.load()
+    recs = _records(g["idx"], g["vals"], True)
+    fac = _dev(g["fac"], np.float64)
+    cor = _dev(g["cor"], np.float64)
+    visit = _dev(g["visit"], np.int32)
+    _, pf = _lib.i64arr(g["foff"])
+    _, pc = _lib.i64arr(g["coff"])
+    jrc, pj = _lib.i64arr(g["jr"])
+    acc = torch.zeros(int(g["coff"][-1]), dtype=torch.float64, device="cuda")
+    ws = torch.empty(int(L.sptk_core_ws_bytes(pj, len(jrc), g["r"], 1)), dtype=torch.uint8, device="cuda")
+    _lib.check(L.sptk_core_pass_f64(recs.rec.data_ptr(), recs.rw, visit.data_ptr(), None, len(g["visit"]),
+                                    fac.data_ptr(), pf, cor.data_ptr(), pc, pj, len(jrc), g["r"], acc.data_ptr(),
+                                    1, ws.data_ptr(), ws.numel(), _lib.stream_ptr()), "core")
+    np.testing.assert_array_equal(acc.cpu().numpy(), g["acc_out"])
+
+
+@pytest.mark.parametrize("c", range(4))
+def test_core_throughput_fp32(golden, c):
+    from paper_2204_07104_b200 import _lib
+
+    g = _loops_case(golden, c)
+    L = _lib.load()
+    recs = _records(g["idx"], g["vals"], False)
+    fac = _dev(g["fac"], np.float32)
+    cor = _dev(g["cor"], np.float32)
+    visit = _dev(g["visit"], np.int32)
+    _, pf = _lib.i64arr(g["foff"])
+    _, pc = _lib.i64arr(g["coff"])
+    jrc, pj = _lib.i64arr(g["jr"])
+    acc = torch.zeros(int(g["coff"][-1]), dtype=torch.float64, device="cuda")
+    ws = torch.empty(int(L.sptk_core_ws_bytes(pj, len(jrc), g["r"], 0)), dtype=torch.uint8, device="cuda")
+    _lib.check(L.sptk_core_pass(recs.rec.data_ptr(), recs.rw, visit.data_ptr(), None, len(g["visit"]),
+                                fac.data_ptr(), pf, cor.data_ptr(), pc, pj, len(jrc), g["r"], acc.data_ptr(), 0,
+                                ws.data_ptr(), ws.numel(), _lib.stream_ptr()), "core")
+    want = g["acc_out"]
+    np.testing.assert_allclose(acc.cpu().numpy(), want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("c", range(4))
+def test_eval_golden(golden, c):
+    from paper_2204_07104_b200 import TuckerModel
+    from paper_2204_07104_b200.device import predict_device, predict_device_f64
+
+    g = _loops_case(golden, c)
+    order = len(g["jr"])
+    fs = [g["fac"][g["foff"][n]:g["foff"][n + 1]].reshape(g["dims"][n], g["jr"][n]) for n in range(order)]
+    bs = [g["cor"][g["coff"][n]:g["coff"][n + 1]].reshape(g["jr"][n], g["r"]) for n in range(order)]
+    model = TuckerModel(tuple(g["dims"]), tuple(g["jr"]), g["r"], fs, bs)
+    np.testing.assert_allclose(predict_device_f64(model, g["idx"]), g["pred"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(predict_device(model, g["idx"]), g["pred"], rtol=2e-5, atol=2e-5)
+
+
+def _model_and_data(dims, jr, r, nnz, seed, distinct=False):
+    rng = np.random.default_rng(seed)
+    if distinct:
+        n = min(dims)
+        assert nnz <= n
+        idx = np.stack([rng.permutation(d)[:nnz] for d in dims], axis=1)
+    else:
+        idx = np.stack([rng.integers(0, d, nnz) for d in dims], axis=1)
+    fs = [rng.uniform(0, 0.6, (d, j)) for d, j in zip(dims, jr)]
+    bs = [rng.uniform(0, 0.6, (j, r)) for j in jr]
+    vals = rng.normal(2.0, 1.0, nnz)
+    return idx, vals, fs, bs
+
+
+def _run_factor(idx, vals, fs, bs, visit, mode, f64, gam=0.01, lam=0.01):
+    from paper_2204_07104_b200 import _lib
+
+    L = _lib.load()
+    fac, foff = O.pack(fs)
+    cor, coff = O.pack(bs)
+    jr = np.array([a.shape[1] for a in fs])
+    recs = _records(idx, vals, f64)
+    dt = np.float64 if f64 else np.float32
+    dfac, dcor = _dev(fac, dt), _dev(cor, dt)
+    dvis = _dev(visit, np.int32)
+    _, pf = _lib.i64arr(foff)
+    _, pc = _lib.i64arr(coff)
+    _, pj = _lib.i64arr(jr)
+    gm, pg = _lib.f64arr(np.full(len(fs), gam))
+    lm, pl = _lib.f64arr(np.full(len(fs), lam))
+    fn = L.sptk_factor_pass_f64 if f64 else L.sptk_factor_pass
+    _lib.check(fn(recs.rec.data_ptr(), recs.rw, dvis.data_ptr(), len(visit), 0, dfac.data_ptr(), pf,
+                  dcor.data_ptr(), pc, pj, len(fs), bs[0].shape[1], pg, pl, mode, _lib.stream_ptr()), "factor")
+    return dfac.double().cpu().numpy(), fac, foff, cor, coff, jr
+
+
+@pytest.mark.parametrize("dims,J,R", [((40, 50, 60), 4, 4), ((300, 40, 30), 8, 8), ((200, 300, 100), 16, 16),
+                                      ((30, 40, 50, 60), 16, 16), ((20, 21, 22, 23, 24, 25), 8, 8),
+                                      ((50, 60, 70), 32, 32), ((40, 50, 60), 5, 3)])
+def test_factor_seq_fp32_one_epoch(dims, J, R):
+    """Deterministic fp32 mode vs the fp64 oracle after one pass: |d| <= 1e-4 * |A| + 1e-5 * max|A|."""
+    idx, vals, fs, bs = _model_and_data(dims, (J,) * len(dims), R, 3000, 1)
+    visit = np.random.default_rng(2).permutation(len(vals))
+    got, fac, foff, cor, coff, jr = _run_factor(idx, vals, fs, bs, visit, 1, False, gam=0.002)
+    want = fac.copy()
+    O.factor_pass(idx, vals, visit.astype(np.int64), want, foff, cor, coff, jr, R, np.full(len(dims), 0.002),
+                  np.full(len(dims), 0.01))
+    tol = 1e-4 * np.abs(want) + 1e-5 * np.abs(want).max()
+    assert (np.abs(got - want) <= tol).all(), np.max(np.abs(got - want) / (np.abs(want) + 1e-12))
+
+
+@pytest.mark.parametrize("dims,J,R", [((4000, 4000, 4000), 4, 4), ((4000, 4000, 4000), 8, 8),
+                                      ((4000, 4000, 4000), 16, 16), ((3000,) * 4, 16, 16),
+                                      ((3000,) * 6, 8, 8), ((3000, 3000, 3000), 32, 32),
+                                      ((3000, 3000, 3000), 6, 5)])
+def test_factor_hogwild_conflict_free_equals_sequential(dims, J, R):
+    """On samples touching pairwise-distinct rows the Hogwild kernel has no
+    races, so it must equal the sequential semantics (fp32 tolerance)."""
+    idx, vals, fs, bs = _model_and_data(dims, (J,) * len(dims), R, 2500, 3, distinct=True)
+    visit = np.arange(len(vals))
+    got, fac, foff, cor, coff, jr = _run_factor(idx, vals, fs, bs, visit, 0, False, gam=0.003)
+    want = fac.copy()
+    O.factor_pass(idx, vals, visit.astype(np.int64), want, foff, cor, coff, jr, R, np.full(len(dims), 0.003),
+                  np.full(len(dims), 0.01))
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())

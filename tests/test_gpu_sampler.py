@@ -1,0 +1,116 @@
+"""K2 samplers on the GPU: bit-exact against the reference's numpy draws."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def h32(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<i4").tobytes()).hexdigest()
+
+
+def test_seed_states(golden, golden_meta):
+    from paper_2204_07104_b200.sampler import pcg64_state
+
+    for i in range(golden_meta["n_entropies"]):
+        assert np.array_equal(pcg64_state(golden[f"rng_entropy_{i}"].tolist()), golden[f"rng_state_{i}"])
+
+
+@pytest.mark.parametrize("q0", [0, 1, 7, 1000001])
+def test_u32_stream(q0):
+    from paper_2204_07104_b200.sampler import u32_stream
+
+    got = u32_stream([3, 1, 4], 5000, q0=q0).cpu().numpy().view(np.uint32)
+    want = O.u32_stream(O.pcg64_state([3, 1, 4]), q0 + 5000)[q0:]
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 100, 1000, 4097, 65536, 100_003])
+def test_permutation_golden(golden, n):
+    from paper_2204_07104_b200.sampler import permutation
+
+    ent = golden[f"perm_{n}_ent"].tolist()
+    assert np.array_equal(permutation(ent, n).cpu().numpy(), golden[f"perm_{n}"])
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 9, 33, 4096, 8191, 8192, 8193, 70_000, 262_145, 1_000_003])
+def test_permutation_j_sequence(n):
+    from paper_2204_07104_b200.sampler import permutation_j
+
+    ent = [11, 1, n]
+    got = permutation_j(ent, n).cpu().numpy()
+    _, want = O.permutation(ent, n, return_j=True)
+    assert np.array_equal(got[1:], want[1:])
+
+
+@pytest.mark.parametrize("n", [50_000, 3_000_017])
+def test_permutation_random_seeds(n):
+    from paper_2204_07104_b200.sampler import permutation
+
+    for s in range(3):
+        ent = [s, 1, 2, 0, 1]
+        assert np.array_equal(permutation(ent, n).cpu().numpy(), O.permutation(ent, n))
+
+
+def test_permutation_large_hashes(golden_meta):
+    from paper_2204_07104_b200.sampler import permutation
+
+    for key in ("perm_1048576", "perm_3000017", "perm_12345678"):
+        g = golden_meta["big"][key]
+        p = permutation(g["entropy"], g["n"]).cpu().numpy()
+        assert p[:64].tolist() == g["head"]
+        assert h32(p) == g["sha256_i32"]
+
+
+def test_permutation_netflix_size(golden_meta):
+    """The factor-phase visit order of the Netflix-shaped bench (99,072,112
+    nonzeros, seed 1, epochs 0 and 1) equals numpy's."""
+    from paper_2204_07104_b200.sampler import permutation
+
+    for t in range(2):
+        g = golden_meta["big"][f"perm_NF_t{t}"]
+        p = permutation(g["entropy"], g["n"]).cpu().numpy()
+        assert p[:64].tolist() == g["head"] and p[-64:].tolist() == g["tail"]
+        assert h32(p) == g["sha256_i32"]
+
+
+@pytest.mark.parametrize("pop,k", [(100, 10), (10000, 9000), (10001, 9000), (500_000, 5000),
+                                   (500_000, 20_000), (4_000_000, 1 << 20), (200, 200)])
+def test_choice_golden(golden, pop, k):
+    from paper_2204_07104_b200.sampler import choice
+
+    ent = golden[f"choice_{pop}_{k}_ent"].tolist()
+    got, path = choice(ent, pop, k, shuffle=True)
+    assert np.array_equal(got.cpu().numpy(), golden[f"choice_{pop}_{k}"])
+    got_set, _ = choice(ent, pop, k, shuffle=False)
+    assert np.array_equal(np.sort(got_set.cpu().numpy()), np.sort(golden[f"choice_{pop}_{k}"]))
+
+
+def test_choice_edge_cases():
+    from paper_2204_07104_b200.sampler import choice
+
+    for pop, k in [(1, 1), (5, 5), (7, 0), (10000, 200), (10001, 201), (20001, 401), (30000, 29999)]:
+        ent = [5, 2, pop, k]
+        got, _ = choice(ent, pop, k, shuffle=True)
+        want, _ = O.choice(ent, pop, k)
+        assert np.array_equal(got.cpu().numpy(), want), (pop, k)
+
+
+def test_choice_netflix_core_batch(golden_meta):
+    """Psi = choice(99,072,112, 2^20) of the bench (Floyd path), exact order and set."""
+    from paper_2204_07104_b200.sampler import choice
+
+    for t in range(2):
+        g = golden_meta["big"][f"psi_NF_t{t}"]
+        got, path = choice(g["entropy"], g["pop"], g["k"], shuffle=True)
+        got = got.cpu().numpy()
+        assert path == "floyd"
+        assert got[:64].tolist() == g["head"]
+        assert h32(got) == g["sha256_i32"]
+        s, _ = choice(g["entropy"], g["pop"], g["k"], shuffle=False)
+        assert h32(np.sort(s.cpu().numpy())) == g["sha256_sorted_i32"]
