@@ -19,9 +19,10 @@
 //   * factor_wps_kernel<T>         throughput mode for ranks without a
 //     specialisation: one warp per sample, lanes over r and j (the paper's
 //     warp-shuffle layout), B(n) in shared memory.
-//   * factor_seq_kernel<T>         deterministic verification mode: one warp
-//     walks the visit list strictly in order with the reference's exact
-//     operation order and no FMA contraction (fp32 or fp64).
+//   * factor_seq_kernel<T>         exact mode: reproduces the strictly
+//     sequential loop (conflict-free prefixes of the visit list run in
+//     parallel, the reference's operation order, no FMA contraction; fp32 or
+//     fp64).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -237,85 +238,98 @@ __device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd
 template <>
 __device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
 
+// One CTA walks the visit list in order.  Each step takes the next CAND
+// samples, finds the longest prefix whose samples touch pairwise-distinct rows
+// in every mode (__match_any_sync per mode), and updates that prefix in
+// parallel, one thread per sample.  Samples in such a prefix commute exactly,
+// so the result equals the strictly sequential reference loop, while ~sqrt(I)
+// samples run concurrently.  Per-sample arithmetic follows _loops.py:31-62
+// operation for operation, with no FMA contraction.
 template <typename T>
 __global__ void __launch_bounds__(32) factor_seq_kernel(const int* __restrict__ rec, int rw, int vo,
                                                         const int* __restrict__ visit, long long n_visit,
                                                         long long base, T* __restrict__ fac,
-                                                        const T* __restrict__ cor, ModelDesc md, GamLam gl) {
+                                                        const T* __restrict__ cor, ModelDesc md, GamLam gl,
+                                                        int cand, int per_thread) {
   extern __shared__ unsigned char smem_raw[];
   T* Bs = reinterpret_cast<T*>(smem_raw);
   const int lane = threadIdx.x & 31;
   for (int i = lane; i < md.cor_size; i += 32) Bs[i] = cor[i];
   const int N = md.n_modes, R = md.rcore;
   int aoff[SPTK_MAX_MODES];
-  int tot = 0, jmax = 0;
+  int tot = 0;
   for (int n = 0; n < N; ++n) {
     aoff[n] = tot;
     tot += md.jr[n];
-    jmax = md.jr[n] > jmax ? md.jr[n] : jmax;
   }
-  T* a_s = Bs + md.cor_size;
-  T* c_s = a_s + tot;
-  T* w_s = c_s + N * R;
-  T* g_s = w_s + R;
+  T* my = Bs + ((md.cor_size + 1) & ~1) + (size_t)lane * per_thread;
+  T* a_s = my;             // sum J
+  T* c_s = a_s + tot;      // N*R
+  T* g_s = c_s + N * R;    // max J
   __syncwarp();
-  for (long long k = 0; k < n_visit; ++k) {
-    const long long ri = base + (visit ? (long long)visit[k] : k);
-    const int* rp = rec + ri * rw;
-    const T x = load_val<T>(rp, vo);
+  const unsigned lt = (1u << lane) - 1u;
+  long long pos = 0;
+  while (pos < n_visit) {
+    const long long k = pos + lane;
+    const bool valid = lane < cand && k < n_visit;
+    const int* rp = nullptr;
+    unsigned conflict = 0;
+    if (valid) rp = rec + (base + (visit ? (long long)visit[k] : k)) * rw;
     for (int n = 0; n < N; ++n) {
-      const int J = md.jr[n];
-      volatile const T* row = fac + md.foff[n] + (long long)rp[n] * J;
-      for (int j = lane; j < J; j += 32) a_s[aoff[n] + j] = row[j];
+      int row = valid ? rp[n] : -1 - lane;
+      unsigned peers = __match_any_sync(0xffffffffu, row);
+      if (peers & lt) conflict |= 1u;
     }
-    __syncwarp();
-    for (int n0 = 0; n0 < N; ++n0) {
-      const int J = md.jr[n0];
-      for (int r = lane; r < R; r += 32) {
-        T acc = 0;
-        for (int j = 0; j < J; ++j) acc = add_rn(acc, mul_rn(a_s[aoff[n0] + j], Bs[md.coff[n0] + j * R + r]));
-        c_s[n0 * R + r] = acc;
+    unsigned cm = __ballot_sync(0xffffffffu, conflict || !valid);
+    int P = cm ? __ffs(cm) - 1 : 32;
+    if (P == 0) P = 1;  // cannot happen for a valid lane 0; keeps progress
+    if (lane < P && valid) {
+      const T x = load_val<T>(rp, vo);
+      for (int n = 0; n < N; ++n) {
+        const int J = md.jr[n];
+        volatile const T* row = fac + md.foff[n] + (long long)rp[n] * J;
+        for (int j = 0; j < J; ++j) a_s[aoff[n] + j] = row[j];
       }
-    }
-    __syncwarp();
-    for (int n = 0; n < N; ++n) {
-      const int J = md.jr[n];
-      for (int r = lane; r < R; r += 32) {
-        T w = 1;
-        for (int n0 = 0; n0 < N; ++n0)
-          if (n0 != n) w = mul_rn(w, c_s[n0 * R + r]);
-        w_s[r] = w;
-      }
-      __syncwarp();
-      for (int j = lane; j < J; j += 32) {
-        T g = 0;
-        for (int r = 0; r < R; ++r) g = add_rn(g, mul_rn(w_s[r], Bs[md.coff[n] + j * R + r]));
-        g_s[j] = g;
-      }
-      __syncwarp();
-      T inter = 0;
-      for (int j = 0; j < J; ++j) inter = add_rn(inter, mul_rn(a_s[aoff[n] + j], g_s[j]));
-      const T gm = (T)gl.gam[n], lm = (T)gl.lam[n];
-      T* row = fac + md.foff[n] + (long long)rp[n] * J;
-      for (int j = lane; j < J; j += 32) {
-        T av = a_s[aoff[n] + j];
-        T gsj = g_s[j];
-        T g = add_rn(add_rn(mul_rn(-x, gsj), mul_rn(lm, av)), mul_rn(inter, gsj));
-        av = add_rn(av, -mul_rn(gm, g));
-        a_s[aoff[n] + j] = av;
-        row[j] = av;
-      }
-      __syncwarp();
-      if (n < N - 1) {
-        for (int r = lane; r < R; r += 32) {
+      for (int n0 = 0; n0 < N; ++n0) {
+        const int J = md.jr[n0];
+        for (int r = 0; r < R; ++r) {
           T acc = 0;
-          for (int j = 0; j < J; ++j) acc = add_rn(acc, mul_rn(a_s[aoff[n] + j], Bs[md.coff[n] + j * R + r]));
-          c_s[n * R + r] = acc;
+          for (int j = 0; j < J; ++j) acc = add_rn(acc, mul_rn(a_s[aoff[n0] + j], Bs[md.coff[n0] + j * R + r]));
+          c_s[n0 * R + r] = acc;
         }
       }
-      __syncwarp();
+      for (int n = 0; n < N; ++n) {
+        const int J = md.jr[n];
+        for (int j = 0; j < J; ++j) g_s[j] = 0;
+        for (int r = 0; r < R; ++r) {
+          T w = 1;
+          for (int n0 = 0; n0 < N; ++n0)
+            if (n0 != n) w = mul_rn(w, c_s[n0 * R + r]);
+          for (int j = 0; j < J; ++j) g_s[j] = add_rn(g_s[j], mul_rn(w, Bs[md.coff[n] + j * R + r]));
+        }
+        T inter = 0;
+        for (int j = 0; j < J; ++j) inter = add_rn(inter, mul_rn(a_s[aoff[n] + j], g_s[j]));
+        const T gm = (T)gl.gam[n], lm = (T)gl.lam[n];
+        T* row = fac + md.foff[n] + (long long)rp[n] * J;
+        for (int j = 0; j < J; ++j) {
+          T av = a_s[aoff[n] + j];
+          T g = add_rn(add_rn(mul_rn(-x, g_s[j]), mul_rn(lm, av)), mul_rn(inter, g_s[j]));
+          av = add_rn(av, -mul_rn(gm, g));
+          a_s[aoff[n] + j] = av;
+          row[j] = av;
+        }
+        if (n < N - 1) {
+          for (int r = 0; r < R; ++r) {
+            T acc = 0;
+            for (int j = 0; j < J; ++j) acc = add_rn(acc, mul_rn(a_s[aoff[n] + j], Bs[md.coff[n] + j * R + r]));
+            c_s[n * R + r] = acc;
+          }
+        }
+      }
     }
     __threadfence_block();
+    __syncwarp();
+    pos += P;
   }
 }
 
@@ -396,12 +410,15 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
     tot += md.jr[n];
   }
   if (mode == 1) {
-    size_t smem = sizeof(T) * ((size_t)md.cor_size + tot + 2 * (size_t)md.n_modes * md.rcore + md.rcore + jmax + 8);
-    SPTK_REQUIRE(smem <= 200 * 1024, "factor_pass(seq): model ranks too large");
+    int per_thread = tot + md.n_modes * md.rcore + jmax + 2;
+    per_thread = (per_thread + 1) & ~1;
+    int cand = 32;
+    size_t smem = sizeof(T) * ((size_t)((md.cor_size + 1) & ~1) + (size_t)per_thread * 32);
+    SPTK_REQUIRE(smem <= 200 * 1024, "factor_pass(sequential): model ranks too large for shared memory");
     auto kfn = factor_seq_kernel<T>;
     if (smem > 48 * 1024)
       SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kfn<<<1, 32, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl);
+    kfn<<<1, 32, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl, cand, per_thread);
     SPTK_CHECK_LAUNCH();
     return 0;
   }

@@ -15,15 +15,20 @@ round-trip:
 ``wall_seconds`` is device time between CUDA events around that work (the
 reference's perf_counter interval, trainer.py:291/353), evaluation excluded.
 
-Two update modes (extra TrainConfig fields, defaults keep the reference's
+Update modes (extra TrainConfig fields; the defaults keep the reference's
 call signature working):
-  update_mode="hogwild"     throughput: thread-per-sample Hogwild factor
-                            kernel in visit order (cuFastTucker's scheme).
-  update_mode="sequential"  verification: visit lists applied strictly in
-                            order with the reference's operation order, core
-                            batch split and merged like np.array_split.
-  precision="fp32"|"fp64"   device arithmetic; fp64 + sequential reproduces the
-                            reference to rounding.
+  update_mode="exact"    the reference's sequential semantics: each visit list
+                         is applied in order (conflict-free prefixes run in
+                         parallel, identical results), the reference's
+                         operation order, the core batch split and merged like
+                         np.array_split.  "sequential" is an alias.
+  update_mode="hogwild"  throughput: thread-per-sample Hogwild factor kernel
+                         over the visit order (cuFastTucker's scheme).
+  update_mode="auto"     exact up to 2^22 training nonzeros, hogwild above: on
+                         small tensors a GPU's worth of concurrent samples
+                         would update every row many times per step.
+  precision="fp32"|"fp64"  device arithmetic; fp64 + exact reproduces the
+                         reference to rounding.
 """
 
 from __future__ import annotations
@@ -63,7 +68,7 @@ class TrainConfig:
     seed: int = 0
     eval_every: int = 1
     core_average: bool = True
-    update_mode: str = "hogwild"
+    update_mode: str = "auto"
     precision: str = "fp32"
 
     def __post_init__(self):
@@ -78,8 +83,8 @@ class TrainConfig:
             raise ValueError("core_batch_cap must be >= 1")
         if self.eval_every < 1:
             raise ValueError("eval_every must be >= 1")
-        if self.update_mode not in ("hogwild", "sequential"):
-            raise ValueError("update_mode must be 'hogwild' or 'sequential'")
+        if self.update_mode not in ("auto", "exact", "sequential", "hogwild"):
+            raise ValueError("update_mode must be 'auto', 'exact' (or 'sequential') or 'hogwild'")
         if self.precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
 
@@ -156,6 +161,18 @@ def _dense_core(core_factors):
     return g.sum(axis=-1)
 
 
+AUTO_EXACT_MAX_NNZ = 1 << 22
+
+
+def resolve_mode(update_mode: str, nnz: int) -> int:
+    """libsptk factor-pass mode: 1 = exact, 0 = hogwild."""
+    if update_mode in ("exact", "sequential"):
+        return 1
+    if update_mode == "hogwild":
+        return 0
+    return 1 if nnz <= AUTO_EXACT_MAX_NNZ else 0
+
+
 # --------------------------------------------------------------------------
 # device epoch runner
 # --------------------------------------------------------------------------
@@ -169,7 +186,7 @@ class EpochRunner:
         self.torch = torch
         self.cfg = config
         self.f64 = config.precision == "fp64"
-        self.mode = 1 if config.update_mode == "sequential" else 0
+        self.mode = resolve_mode(config.update_mode, train_set.nnz)
         self.m = int(config.workers)
         self.order = model.order
         self.nnz = train_set.nnz

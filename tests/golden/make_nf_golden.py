@@ -1,0 +1,48 @@
+"""Reference RMSE curve on a Netflix-shaped tensor (build container only).
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_nf_golden.py
+
+Data: paper_2204_07104_b200.synthetic.generate_large (deterministic numpy, so
+the GPU test regenerates identical arrays on the box), Netflix mode sizes
+480,189 x 17,770 x 2,182, J=R=16, 8M training nonzeros and 80K test entries.
+The REFERENCE's own train() (sptucker, numba, workers=1) produces the curve the
+GPU Hogwild path is checked against (north star: test RMSE within 1%).
+"""
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.environ.get("SPTUCKER_REF", "/root/reference/pkg/src"))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+from paper_2204_07104_b200.synthetic import generate_large  # noqa: E402
+from sptucker.coo import DatasetSplit, SparseTensorCoo  # noqa: E402
+from sptucker.model import ModelConfig, default_init_scale, init_model  # noqa: E402
+from sptucker.trainer import TrainConfig, train  # noqa: E402
+
+CASES = {
+    "nf8m": dict(dims=(480189, 17770, 2182), nnz=8_000_000, n_test=80_000, J=16, R=16, epochs=3, seed=7),
+}
+
+out = {}
+for name, c in CASES.items():
+    t0 = time.time()
+    tr, te, _ = generate_large(c["dims"], c["nnz"], (c["J"],) * 3, c["R"], 0.1, seed=c["seed"], n_test=c["n_test"])
+    ds = DatasetSplit(SparseTensorCoo(tr.dims, tr.indices, tr.values), SparseTensorCoo(te.dims, te.indices, te.values))
+    scale = default_init_scale(tr.values, 3)
+    model = init_model(tr.dims, ModelConfig((c["J"],) * 3, c["R"], scale, seed=1))
+    gen = time.time() - t0
+    t0 = time.time()
+    rows = train(model, ds, TrainConfig(epochs=c["epochs"], seed=1))
+    out[name] = dict(c, scale=scale, gen_seconds=gen, train_seconds=time.time() - t0,
+                     rows=[r.__dict__ for r in rows])
+    print(name, out[name]["rows"], flush=True)
+
+with open(os.path.join(ROOT, "tests", "golden", "nf_golden.json"), "w") as fh:
+    json.dump(out, fh, indent=1)

@@ -144,8 +144,8 @@ def _model_and_data(dims, jr, r, nnz, seed, distinct=False):
         idx = np.stack([rng.permutation(d)[:nnz] for d in dims], axis=1)
     else:
         idx = np.stack([rng.integers(0, d, nnz) for d in dims], axis=1)
-    fs = [rng.uniform(0, 0.6, (d, j)) for d, j in zip(dims, jr)]
-    bs = [rng.uniform(0, 0.6, (j, r)) for j in jr]
+    fs = [rng.uniform(0, 1.2 / np.sqrt(j), (d, j)) for d, j in zip(dims, jr)]
+    bs = [rng.uniform(0, 1.2 / np.sqrt(r), (j, r)) for j in jr]
     vals = rng.normal(2.0, 1.0, nnz)
     return idx, vals, fs, bs
 
