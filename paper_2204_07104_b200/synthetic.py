@@ -135,12 +135,13 @@ def generate_synthetic(dims, nnz: int, j_ranks, r_core: int, noise_sigma: float 
 # ------------------------------------------------------------------ large
 
 def large_indices(dims, nnz: int, seed: int) -> np.ndarray:
-    """i.i.d. uniform indices, chunked and prefix-stable."""
+    """i.i.d. uniform indices; one stream per (chunk, mode), so any prefix of a
+    large tensor equals the smaller tensor drawn with the same seed."""
     out = np.empty((nnz, len(dims)), dtype=np.int64)
     for c0 in range(0, nnz, CHUNK):
         n = min(CHUNK, nnz - c0)
-        rng = np.random.default_rng([int(seed), 0xC01, c0 // CHUNK])
         for m, d in enumerate(dims):
+            rng = np.random.default_rng([int(seed), 0xC01, c0 // CHUNK, m])
             out[c0:c0 + n, m] = rng.integers(0, d, size=n)
     return out
 

@@ -221,6 +221,7 @@ class EpochRunner:
         self._lam, self.p_lam = f64arr(self.lam_np)
         self.map = self.part.pos_of_id if self.m > 1 else None
         self.L = L
+        self.factor_events = None  # optional list: (start, end) CUDA events per factor launch
 
     def factor_phase(self, t: int, gamma_a: float) -> int:
         cfg, L, dm = self.cfg, self.L, self.dm
@@ -232,9 +233,16 @@ class EpochRunner:
             for block, off, cnt in items:
                 st = pcg64_state([cfg.seed, 1, t, *block])
                 perm = permutation(None, cnt, out=self.perm_buf, ws=self.perm_ws, state=st)
+                if self.factor_events is not None:
+                    e0 = self.torch.cuda.Event(enable_timing=True)
+                    e0.record()
                 check(fn(ptr(self.part.rec), self.part.rw, ptr(perm), cnt, off, ptr(dm.fac), dm.p_foff,
                          ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam,
                          self.mode, s), "sptk_factor_pass")
+                if self.factor_events is not None:
+                    e1 = self.torch.cuda.Event(enable_timing=True)
+                    e1.record()
+                    self.factor_events.append((e0, e1))
                 processed += cnt
         return processed
 
