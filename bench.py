@@ -40,11 +40,12 @@ METRIC = "sampled nonzeros/sec per SGD epoch (A+B update) at 1/2/4/8 B200; test 
 
 CONFIGS = {
     "nf": dict(workload="netflix-shaped 480189x17770x2182, 99,072,112 nnz, J=R=16",
-               dims=(480189, 17770, 2182), nnz=99_072_112, n_test=1_408_395, J=16, R=16),
+               dims=(480189, 17770, 2182), nnz=99_072_112, n_test=1_408_395, J=16, R=16, alpha_a=0.003),
     "cfg1": dict(workload="synthetic 1Kx1Kx1K, 90K train / 10K test, J=R=8",
                  dims=(1000, 1000, 1000), nnz=90_000, n_test=10_000, J=8, R=8),
     "y4": dict(workload="yahoo-shaped 1000990x624961x3075x133, 250,272,286 nnz, J=R=16",
-               dims=(1_000_990, 624_961, 3_075, 133), nnz=250_272_286, n_test=2_502_723, J=16, R=16),
+               dims=(1_000_990, 624_961, 3_075, 133), nnz=250_272_286, n_test=2_502_723, J=16, R=16,
+               alpha_a=0.003),
     "o6": dict(workload="6-order 10K^6, 1e9 nnz, J=R=8",
                dims=(10_000,) * 6, nnz=1_000_000_000, n_test=1_000_000, J=8, R=8),
 }
@@ -161,7 +162,7 @@ def run_cpu_reference(cfg, sample, epochs, threads):
     rates = []
     for t in range(epochs):
         rows = O.train(fs, bs, tr.indices, tr.values, epochs=1, workers=workers, seed=1, evaluate=False,
-                       dims=cfg["dims"])
+                       dims=cfg["dims"], alpha_a=cfg.get("alpha_a", 0.009))
         rates.append(sample / rows[-1]["wall_seconds"])
     desc = (f"oracle C port (fp64, {workers} DSGD worker threads) on the first {sample:,} nonzeros of the "
             f"same workload, 1 epoch per step")
@@ -213,7 +214,7 @@ def bench_ours(args, cfg):
     scale = default_init_scale(tr.values, order)
     model = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
     tcfg = TrainConfig(epochs=args.warmup + args.steps, seed=1, update_mode=args.mode,
-                       workers=world if world > 1 else 1)
+                       workers=world if world > 1 else 1, alpha_a=cfg.get("alpha_a", 0.009))
     if world > 1:
         from paper_2204_07104_b200 import dist
 
@@ -273,7 +274,8 @@ def bench_ours(args, cfg):
         k2 = args.e2e_epochs
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        train(m2, DatasetSplit(tr, te), TrainConfig(epochs=k2, seed=1, update_mode=args.mode))
+        train(m2, DatasetSplit(tr, te), TrainConfig(epochs=k2, seed=1, update_mode=args.mode,
+                                                    alpha_a=cfg.get("alpha_a", 0.009)))
         torch.cuda.synchronize()
         el = time.perf_counter() - t1
         h2d = tr.indices.nbytes + tr.values.nbytes + te.indices.nbytes + te.values.nbytes + \

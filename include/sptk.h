@@ -59,6 +59,10 @@ int sptk_version(void);
 long long sptk_launch_count(void);
 void sptk_reset_launch_count(void);
 int sptk_record_words(int order, int f64_records);
+/* Throughput factor kernel for J = R in {16, 32}: 0 = CUDA-core FMA kernel,
+ * 1 = tcgen05 TF32, 3 = tcgen05 3xTF32 (default; env SPTK_TC overrides). */
+int sptk_set_tc_mode(int mode);
+int sptk_get_tc_mode(void);
 
 /* ---- K2: samplers (bit-exact with numpy 2.x Generator/PCG64) ----------- */
 /* default_rng(entropy).bit_generator state: {state_hi, state_lo, inc_hi, inc_lo}

@@ -84,6 +84,11 @@ int sptk_version(void) { return 100; }
 long long sptk_launch_count(void) { return g_launches.load(); }
 void sptk_reset_launch_count(void) { g_launches = 0; }
 int sptk_record_words(int order, int f64_records) { return rec_words_t(order, f64_records != 0); }
+int sptk_set_tc_mode(int mode) {
+  SPTK_REQUIRE(set_tc_mode(mode) == 0, "tc mode must be 0 (FMA), 1 (TF32) or 3 (3xTF32)");
+  return 0;
+}
+int sptk_get_tc_mode(void) { return get_tc_mode(); }
 
 int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_out[4]) {
   uint32_t words[512];

@@ -424,6 +424,9 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
   }
   if (!f64) {
     int rc = 0;
+    if (try_factor_tc(rec, rw, visit, n_visit, base, (float*)fac, (const float*)cor, md, (const float*)h_gammas,
+                      (const float*)h_lambdas, s, &rc))
+      return rc;
     if (md.cor_size <= CONST_COR_MAX &&
         try_tps(rec, rw, visit, n_visit, base, (float*)fac, (const float*)cor, md, (const float*)h_gammas,
                 (const float*)h_lambdas, s, &rc))

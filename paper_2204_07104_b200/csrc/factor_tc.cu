@@ -1,0 +1,367 @@
+// factor_tc.cu -- K3 on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// Same update as factor_tps_kernel (_loops.py:17-63, Hogwild over the visit
+// order), with the contractions moved to tcgen05.mma:
+//
+//   c_n  = A_n[tile] (128 x J) . B_n        (128 x R)   K = J
+//   gs_n = W_n       (128 x R) . B_n^T      (128 x J)   K = R,  W_n = prod_{n0!=n} c_n0
+//   c_n' = A_n'      (128 x J) . B_n        refresh after the row update
+//
+// One CTA owns a tile of 128 consecutive visit positions; thread t <-> sample
+// t <-> TMEM lane t, so every elementwise step (products, residual, row update)
+// is register-local and the accumulators come back with one tcgen05.ld per 16
+// columns.  Operands are staged in shared memory in the K-major no-swizzle
+// canonical layout; B(n) (and its transpose) stay resident for the whole
+// launch.  TF32 inputs with fp32 accumulation; SPLIT = 3xTF32 (hi*hi + hi*lo +
+// lo*hi), which restores ~fp32 accuracy of the products at 3x the (cheap)
+// tensor work.  One elected thread issues the MMAs and commits to an mbarrier.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "tc.cuh"
+
+namespace sptk {
+
+template <int N>
+struct TcParams {
+  long long foff[N];
+  float gam[N];
+  float lam[N];
+};
+
+template <int N, int J, int R, bool SPLIT>
+struct TcCfg {
+  static constexpr int M = 128;
+  static constexpr int NB = SPLIT ? 2 : 1;
+  static constexpr int BT = R * J;  // B_n^T: R rows x J (K)
+  static constexpr int BN = J * R;  // B_n  : J rows x R (K)
+  static constexpr int AT = M * J;
+  static constexpr int WT = M * R;
+  static constexpr int OFF_BT = 0;
+  static constexpr int OFF_BN = OFF_BT + N * NB * BT;
+  static constexpr int OFF_AT = OFF_BN + N * NB * BN;
+  static constexpr int OFF_WT = OFF_AT + N * NB * AT;
+  static constexpr int FLOATS = OFF_WT + NB * WT;
+  static constexpr int NEED = N * R + J;
+  static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr size_t SMEM = (size_t)FLOATS * 4;
+};
+
+// float offset of element (row, k) in a K-major canonical operand with ROWS rows
+template <int ROWS>
+__device__ __forceinline__ int canon(int row, int k) {
+  return (k >> 2) * (ROWS * 4) + (row >> 3) * 32 + (row & 7) * 4 + (k & 3);
+}
+
+__device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+
+// write one 4-float K chunk of row `row` (hi and, if SPLIT, lo copies)
+template <int ROWS, bool SPLIT>
+__device__ __forceinline__ void put4(float* base_hi, int lo_off, int row, int k0, float4 v) {
+  float* p = base_hi + canon<ROWS>(row, k0);
+  if (SPLIT) {
+    float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+    *reinterpret_cast<float4*>(p) = h;
+    *reinterpret_cast<float4*>(p + lo_off) = l;
+  } else {
+    *reinterpret_cast<float4*>(p) = v;
+  }
+}
+
+template <int ROWS, bool SPLIT>
+__device__ __forceinline__ float4 get4(const float* base_hi, int lo_off, int row, int k0) {
+  const float* p = base_hi + canon<ROWS>(row, k0);
+  float4 h = *reinterpret_cast<const float4*>(p);
+  if (SPLIT) {
+    float4 l = *reinterpret_cast<const float4*>(p + lo_off);
+    h.x += l.x;
+    h.y += l.y;
+    h.z += l.z;
+    h.w += l.w;
+  }
+  return h;
+}
+
+// D[dcol..] (+)= A(128 x K) . B(NR x K)^T over K in steps of 8 (tf32), with the
+// 3xTF32 split when SPLIT.
+template <int NR, int K, bool SPLIT>
+__device__ __forceinline__ void issue_gemm(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+                                           uint32_t idesc) {
+#pragma unroll
+  for (int kk = 0; kk < K / 8; ++kk) {
+    const uint32_t ao = kk * 2 * (128 * 16), bo = kk * 2 * (NR * 16);
+    const uint64_t ah = tc::smem_desc(a_hi + ao, 128 * 16, 128);
+    const uint64_t bh = tc::smem_desc(b_hi + bo, NR * 16, 128);
+    tc::mma_tf32(d_tmem, ah, bh, idesc, kk > 0 ? 1u : 0u);
+    if (SPLIT) {
+      const uint64_t al = tc::smem_desc(a_lo + ao, 128 * 16, 128);
+      const uint64_t bl = tc::smem_desc(b_lo + bo, NR * 16, 128);
+      tc::mma_tf32(d_tmem, ah, bl, idesc, 1u);
+      tc::mma_tf32(d_tmem, al, bh, idesc, 1u);
+    }
+  }
+}
+
+template <int N, int J, int R, bool SPLIT, int RW>
+__global__ void __launch_bounds__(128, 1)
+    factor_tc_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
+                     float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p) {
+  using C = TcCfg<N, J, R, SPLIT>;
+  extern __shared__ __align__(1024) float sm[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  // resident operands: B_n^T (rows r, K j) and B_n (rows j, K r), hi/lo
+  for (int e = tid; e < N * J * R; e += 128) {
+    const int n = e / (J * R), rem = e - n * (J * R), j = rem / R, r = rem - j * R;
+    const float b = __ldg(cor + e);
+    const float h = SPLIT ? tf32_hi(b) : b;
+    float* bt = sm + C::OFF_BT + n * C::NB * C::BT;
+    float* bn = sm + C::OFF_BN + n * C::NB * C::BN;
+    bt[canon<R>(r, j)] = h;
+    bn[canon<J>(j, r)] = h;
+    if (SPLIT) {
+      bt[C::BT + canon<R>(r, j)] = b - h;
+      bn[C::BN + canon<J>(j, r)] = b - h;
+    }
+  }
+  if (tid == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tslot, C::TCOLS);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = tslot;
+  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);
+  const uint32_t sbase = tc::smem_u32(sm);
+  const uint32_t id_c = tc::idesc_tf32(128, R), id_g = tc::idesc_tf32(128, J);
+  uint32_t phase = 0;
+
+  for (long long tile = blockIdx.x; tile * 128 < n_visit; tile += gridDim.x) {
+    const long long k = tile * 128 + tid;
+    const bool valid = k < n_visit;
+    int idx[N];
+    float x = 0.f;
+    if (valid) {
+      const int* rp = rec + (base + (visit ? (long long)__ldg(visit + k) : k)) * RW;
+      int wv[8];
+      int4 w0 = __ldg(reinterpret_cast<const int4*>(rp));
+      wv[0] = w0.x;
+      wv[1] = w0.y;
+      wv[2] = w0.z;
+      wv[3] = w0.w;
+      if (RW >= 8) {
+        int4 w1 = __ldg(reinterpret_cast<const int4*>(rp) + 1);
+        wv[4] = w1.x;
+        wv[5] = w1.y;
+        wv[6] = w1.z;
+        wv[7] = w1.w;
+      }
+#pragma unroll
+      for (int n = 0; n < N; ++n) idx[n] = wv[n];
+      x = __int_as_float(wv[N]);
+    } else {
+#pragma unroll
+      for (int n = 0; n < N; ++n) idx[n] = 0;
+    }
+    // gather rows into the A tiles
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float4* src = reinterpret_cast<const float4*>(fac + p.foff[n] + (long long)idx[n] * J);
+      float* at = sm + C::OFF_AT + n * C::NB * C::AT;
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) {
+        float4 v = valid ? __ldcg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        put4<128, SPLIT>(at, C::AT, tid, 4 * q, v);
+      }
+    }
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const uint32_t a = sbase + 4 * (C::OFF_AT + n * C::NB * C::AT);
+        const uint32_t b = sbase + 4 * (C::OFF_BT + n * C::NB * C::BT);
+        issue_gemm<R, J, SPLIT>(tbase + n * R, a, a + 4 * C::AT, b, b + 4 * C::BT, id_c);
+      }
+      tc::mma_commit(&mbar);
+    }
+    tc::mbar_wait(&mbar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+    float c[N][R];
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+      for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + n * R + 16 * q, &c[n][16 * q]);
+
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      // W_n = prod_{n0 != n} c_n0 (reference order), into the W tile
+      float* wt = sm + C::OFF_WT;
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q) {
+        float w4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float w = 1.f;
+#pragma unroll
+          for (int n0 = 0; n0 < N; ++n0)
+            if (n0 != n) w *= c[n0][4 * q + u];
+          w4[u] = w;
+        }
+        put4<128, SPLIT>(wt, C::WT, tid, 4 * q, make_float4(w4[0], w4[1], w4[2], w4[3]));
+      }
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t a = sbase + 4 * C::OFF_WT;
+        const uint32_t b = sbase + 4 * (C::OFF_BN + n * C::NB * C::BN);
+        issue_gemm<J, R, SPLIT>(tbase + N * R, a, a + 4 * C::WT, b, b + 4 * C::BN, id_g);
+        tc::mma_commit(&mbar);
+      }
+      tc::mbar_wait(&mbar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      float g[J];
+#pragma unroll
+      for (int q = 0; q < J / 16; ++q) tc::tmem_ld16(tlane + N * R + 16 * q, &g[16 * q]);
+      // row update (register-local)
+      float* at = sm + C::OFF_AT + n * C::NB * C::AT;
+      float a[J];
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) {
+        float4 v = get4<128, SPLIT>(at, C::AT, tid, 4 * q);
+        a[4 * q] = v.x;
+        a[4 * q + 1] = v.y;
+        a[4 * q + 2] = v.z;
+        a[4 * q + 3] = v.w;
+      }
+      float inter = 0.f;
+#pragma unroll
+      for (int j = 0; j < J; ++j) inter = fmaf(a[j], g[j], inter);
+      const float gm = p.gam[n], lm = p.lam[n];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        float gr = -x * g[j] + lm * a[j] + inter * g[j];
+        a[j] -= gm * gr;
+      }
+      if (valid) {
+        float4* dst = reinterpret_cast<float4*>(fac + p.foff[n] + (long long)idx[n] * J);
+#pragma unroll
+        for (int q = 0; q < J / 4; ++q)
+          __stcg(dst + q, make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]));
+      }
+      if (n < N - 1) {
+#pragma unroll
+        for (int q = 0; q < J / 4; ++q)
+          put4<128, SPLIT>(at, C::AT, tid, 4 * q, make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]));
+        tc::fence_async_smem();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (tid == 0) {
+          tc::fence_after_sync();
+          const uint32_t aa = sbase + 4 * (C::OFF_AT + n * C::NB * C::AT);
+          const uint32_t b = sbase + 4 * (C::OFF_BT + n * C::NB * C::BT);
+          issue_gemm<R, J, SPLIT>(tbase + n * R, aa, aa + 4 * C::AT, b, b + 4 * C::BT, id_c);
+          tc::mma_commit(&mbar);
+        }
+        tc::mbar_wait(&mbar, phase);
+        phase ^= 1;
+        tc::fence_after_sync();
+#pragma unroll
+        for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + n * R + 16 * q, &c[n][16 * q]);
+      }
+    }
+    // all TMEM reads and smem reads of this tile done before the next tile
+    tc::fence_before_sync();
+    __syncthreads();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tbase, C::TCOLS);
+  }
+}
+
+static int g_tc_mode = -1;  // 0 off (CUDA-core FMA kernel), 1 tf32, 3 3xTF32
+
+static int tc_mode_env() {
+  if (g_tc_mode < 0) {
+    const char* e = getenv("SPTK_TC");
+    g_tc_mode = e ? atoi(e) : 3;
+  }
+  return g_tc_mode;
+}
+
+int set_tc_mode(int mode) {
+  if (mode != 0 && mode != 1 && mode != 3) return 2;
+  g_tc_mode = mode;
+  return 0;
+}
+int get_tc_mode() { return tc_mode_env(); }
+
+template <int N, int J, int R, bool SPLIT>
+static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                     const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+  using C = TcCfg<N, J, R, SPLIT>;
+  TcParams<N> p;
+  for (int n = 0; n < N; ++n) {
+    p.foff[n] = md.foff[n];
+    p.gam[n] = gam[n];
+    p.lam[n] = lam[n];
+  }
+  auto kfn = rw == 4 ? factor_tc_kernel<N, J, R, SPLIT, 4> : factor_tc_kernel<N, J, R, SPLIT, 8>;
+  static int configured = 0;
+  static int per_sm = 1;
+  if (!configured) {
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc_kernel<N, J, R, SPLIT, 4>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc_kernel<N, J, R, SPLIT, 8>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    int occ = 1;
+    SPTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, C::SMEM));
+    per_sm = occ < 1 ? 1 : occ;
+    if (per_sm * C::TCOLS > 512) per_sm = 512 / C::TCOLS;
+    configured = 1;
+  }
+  long long tiles = (n_visit + 127) / 128;
+  long long blocks = 148LL * per_sm;
+  if (blocks > tiles) blocks = tiles;
+  kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// returns 1 if handled
+int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                  const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc) {
+  const int mode = tc_mode_env();
+  if (mode == 0) return 0;
+  const int N = md.n_modes, R = md.rcore, J = md.jr[0];
+  for (int n = 0; n < N; ++n)
+    if (md.jr[n] != J) return 0;
+  if (J != R || rw != rec_words(N)) return 0;
+#define SPTK_TC_CASE(NN, JJ)                                                                                 \
+  if (N == NN && J == JJ) {                                                                                  \
+    *rc = mode == 1 ? launch_tc<NN, JJ, JJ, false>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s) \
+                    : launch_tc<NN, JJ, JJ, true>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s); \
+    return 1;                                                                                                \
+  }
+  SPTK_TC_CASE(3, 16)
+  SPTK_TC_CASE(4, 16)
+  SPTK_TC_CASE(3, 32)
+#undef SPTK_TC_CASE
+  return 0;
+}
+
+}  // namespace sptk

@@ -34,6 +34,13 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
                 const T* cor, const ModelDesc& md, const T* h_gammas, const T* h_lambdas, int mode,
                 cudaStream_t s);
 
+// factor_tc.cu (tcgen05 path; returns 1 if it handled the launch)
+int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                  const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc);
+
+int set_tc_mode(int mode);
+int get_tc_mode();
+
 // core.cu
 size_t core_ws_bytes(const ModelDesc& md);
 template <typename T>

@@ -150,10 +150,11 @@ def _model_and_data(dims, jr, r, nnz, seed, distinct=False):
     return idx, vals, fs, bs
 
 
-def _run_factor(idx, vals, fs, bs, visit, mode, f64, gam=0.01, lam=0.01):
+def _run_factor(idx, vals, fs, bs, visit, mode, f64, gam=0.01, lam=0.01, tc=3):
     from paper_2204_07104_b200 import _lib
 
     L = _lib.load()
+    _lib.check(L.sptk_set_tc_mode(tc), "tc mode")
     fac, foff = O.pack(fs)
     cor, coff = O.pack(bs)
     jr = np.array([a.shape[1] for a in fs])
@@ -169,7 +170,9 @@ def _run_factor(idx, vals, fs, bs, visit, mode, f64, gam=0.01, lam=0.01):
     fn = L.sptk_factor_pass_f64 if f64 else L.sptk_factor_pass
     _lib.check(fn(recs.rec.data_ptr(), recs.rw, dvis.data_ptr(), len(visit), 0, dfac.data_ptr(), pf,
                   dcor.data_ptr(), pc, pj, len(fs), bs[0].shape[1], pg, pl, mode, _lib.stream_ptr()), "factor")
-    return dfac.double().cpu().numpy(), fac, foff, cor, coff, jr
+    out = dfac.double().cpu().numpy()
+    _lib.check(L.sptk_set_tc_mode(3), "tc mode")
+    return out, fac, foff, cor, coff, jr
 
 
 @pytest.mark.parametrize("dims,J,R", [((40, 50, 60), 4, 4), ((300, 40, 30), 8, 8), ((200, 300, 100), 16, 16),
@@ -191,13 +194,16 @@ def test_factor_seq_fp32_one_epoch(dims, J, R):
                                       ((4000, 4000, 4000), 16, 16), ((3000,) * 4, 16, 16),
                                       ((3000,) * 6, 8, 8), ((3000, 3000, 3000), 32, 32),
                                       ((3000, 3000, 3000), 6, 5)])
-def test_factor_hogwild_conflict_free_equals_sequential(dims, J, R):
-    """On samples touching pairwise-distinct rows the Hogwild kernel has no
-    races, so it must equal the sequential semantics (fp32 tolerance)."""
+@pytest.mark.parametrize("tc", [0, 1, 3])
+def test_factor_hogwild_conflict_free_equals_sequential(dims, J, R, tc):
+    """On samples touching pairwise-distinct rows the Hogwild kernels have no
+    races, so they must equal the sequential semantics: FMA and 3xTF32 tcgen05
+    at fp32 tolerance, single-pass TF32 at TF32 tolerance."""
     idx, vals, fs, bs = _model_and_data(dims, (J,) * len(dims), R, 2500, 3, distinct=True)
     visit = np.arange(len(vals))
-    got, fac, foff, cor, coff, jr = _run_factor(idx, vals, fs, bs, visit, 0, False, gam=0.003)
+    got, fac, foff, cor, coff, jr = _run_factor(idx, vals, fs, bs, visit, 0, False, gam=0.003, tc=tc)
     want = fac.copy()
     O.factor_pass(idx, vals, visit.astype(np.int64), want, foff, cor, coff, jr, R, np.full(len(dims), 0.003),
                   np.full(len(dims), 0.01))
-    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
+    rtol = 5e-3 if tc == 1 else 1e-4
+    np.testing.assert_allclose(got, want, rtol=rtol, atol=rtol * 0.1 * np.abs(want).max())
