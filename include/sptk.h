@@ -63,6 +63,8 @@ int sptk_record_words(int order, int f64_records);
  * 1 = tcgen05 TF32, 3 = tcgen05 3xTF32 (default; env SPTK_TC overrides). */
 int sptk_set_tc_mode(int mode);
 int sptk_get_tc_mode(void);
+/* test hook: per-sample dump of the first tcgen05 tile (c, gs, refreshed c). */
+void sptk_debug_tc_buffer(float* d_buf);
 
 /* ---- K2: samplers (bit-exact with numpy 2.x Generator/PCG64) ----------- */
 /* default_rng(entropy).bit_generator state: {state_hi, state_lo, inc_hi, inc_lo}

@@ -26,7 +26,10 @@ struct TcParams {
   long long foff[N];
   float gam[N];
   float lam[N];
+  float* dbg;  // optional per-sample dump of the first tile (debug hook)
 };
+
+static float* g_tc_debug = nullptr;
 
 template <int N, int J, int R, bool SPLIT>
 struct TcCfg {
@@ -43,7 +46,8 @@ struct TcCfg {
   static constexpr int FLOATS = OFF_WT + NB * WT;
   static constexpr int NEED = N * R + J;
   static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static constexpr size_t SMEM = (size_t)FLOATS * 4;
+  // + 16 bytes for the mbarrier and the TMEM address slot
+  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
 };
 
 // float offset of element (row, k) in a K-major canonical operand with ROWS rows
@@ -107,9 +111,12 @@ __global__ void __launch_bounds__(128, 1)
     factor_tc_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
                      float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p) {
   using C = TcCfg<N, J, R, SPLIT>;
-  extern __shared__ __align__(1024) float sm[];
-  __shared__ __align__(8) uint64_t mbar;
-  __shared__ uint32_t tslot;
+  // Everything lives in the dynamic segment.  Only 16-byte alignment is assumed
+  // (the no-swizzle canonical layout needs no more); assuming more lets the
+  // compiler fold away low address bits that are not zero at run time.
+  extern __shared__ __align__(16) float sm[];
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 2);
   const int tid = threadIdx.x, warp = tid >> 5;
 
   // resident operands: B_n^T (rows r, K j) and B_n (rows j, K r), hi/lo
@@ -200,6 +207,10 @@ __global__ void __launch_bounds__(128, 1)
     for (int n = 0; n < N; ++n)
 #pragma unroll
       for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + n * R + 16 * q, &c[n][16 * q]);
+    const bool dump = p.dbg != nullptr && tile == blockIdx.x && blockIdx.x == 0;
+    if (dump)
+      for (int n = 0; n < N; ++n)
+        for (int r = 0; r < R; ++r) p.dbg[tid * (2 * N * R + N * J) + n * R + r] = c[n][r];
 
 #pragma unroll
     for (int n = 0; n < N; ++n) {
@@ -234,6 +245,8 @@ __global__ void __launch_bounds__(128, 1)
       float g[J];
 #pragma unroll
       for (int q = 0; q < J / 16; ++q) tc::tmem_ld16(tlane + N * R + 16 * q, &g[16 * q]);
+      if (dump)
+        for (int j = 0; j < J; ++j) p.dbg[tid * (2 * N * R + N * J) + N * R + n * J + j] = g[j];
       // row update (register-local)
       float* at = sm + C::OFF_AT + n * C::NB * C::AT;
       float a[J];
@@ -279,6 +292,8 @@ __global__ void __launch_bounds__(128, 1)
         tc::fence_after_sync();
 #pragma unroll
         for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + n * R + 16 * q, &c[n][16 * q]);
+        if (dump)
+          for (int r = 0; r < R; ++r) p.dbg[tid * (2 * N * R + N * J) + N * R + N * J + n * R + r] = c[n][r];
       }
     }
     // all TMEM reads and smem reads of this tile done before the next tile
@@ -309,6 +324,7 @@ int set_tc_mode(int mode) {
   return 0;
 }
 int get_tc_mode() { return tc_mode_env(); }
+void set_tc_debug(float* buf) { g_tc_debug = buf; }
 
 template <int N, int J, int R, bool SPLIT>
 static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
@@ -320,6 +336,7 @@ static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit
     p.gam[n] = gam[n];
     p.lam[n] = lam[n];
   }
+  p.dbg = g_tc_debug;
   auto kfn = rw == 4 ? factor_tc_kernel<N, J, R, SPLIT, 4> : factor_tc_kernel<N, J, R, SPLIT, 8>;
   static int configured = 0;
   static int per_sm = 1;

@@ -40,6 +40,7 @@ int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, l
 
 int set_tc_mode(int mode);
 int get_tc_mode();
+void set_tc_debug(float* buf);
 
 // core.cu
 size_t core_ws_bytes(const ModelDesc& md);
