@@ -39,6 +39,8 @@
  *     nonzero is one 16/32-byte load.
  *   - Model layout is the reference's (_loops.py:8-10): A(n) row i at
  *     fac[h_foff[n] + i*h_jr[n]], B(n)[j][r] at cor[h_coff[n] + j*rcore + r].
+ *     h_foff / h_coff have order+1 entries, exactly the offsets the
+ *     reference's _pack returns (trainer.py:135-141).
  *   - Every function returns 0 on success and nonzero on failure;
  *     sptk_last_error() describes the last failure.  The library never
  *     allocates device memory: callers pass workspaces sized by *_ws_bytes.
@@ -60,7 +62,9 @@ long long sptk_launch_count(void);
 void sptk_reset_launch_count(void);
 int sptk_record_words(int order, int f64_records);
 /* Throughput factor kernel for J = R in {16, 32}: 0 = CUDA-core FMA kernel,
- * 1 = tcgen05 TF32, 3 = tcgen05 3xTF32 (default; env SPTK_TC overrides). */
+ * 1 = tcgen05 TF32 with the folded refresh and cp.async row prefetch
+ * (default), 2 = tcgen05 TF32 straight form, 3 = tcgen05 3xTF32 straight
+ * form.  The environment variable SPTK_TC sets the initial value. */
 int sptk_set_tc_mode(int mode);
 int sptk_get_tc_mode(void);
 /* test hook: per-sample dump of the first tcgen05 tile (c, gs, refreshed c). */

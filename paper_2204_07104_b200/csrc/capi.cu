@@ -56,6 +56,7 @@ static int build_model_desc(ModelDesc* md, const int64_t* h_foff, const int64_t*
     cs += md->jr[n] * rcore;
   }
   md->cor_size = cs;
+  md->fac_size = h_foff[n_modes];
   return 0;
 }
 
@@ -85,7 +86,7 @@ long long sptk_launch_count(void) { return g_launches.load(); }
 void sptk_reset_launch_count(void) { g_launches = 0; }
 int sptk_record_words(int order, int f64_records) { return rec_words_t(order, f64_records != 0); }
 int sptk_set_tc_mode(int mode) {
-  SPTK_REQUIRE(set_tc_mode(mode) == 0, "tc mode must be 0 (FMA), 1 (TF32) or 3 (3xTF32)");
+  SPTK_REQUIRE(set_tc_mode(mode) == 0, "tc mode must be 0 (FMA), 1 (TF32 v2), 2 (TF32 v1) or 3 (3xTF32)");
   return 0;
 }
 int sptk_get_tc_mode(void) { return get_tc_mode(); }

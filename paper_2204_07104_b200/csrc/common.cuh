@@ -24,6 +24,7 @@ struct ModelDesc {
   long long foff[SPTK_MAX_MODES];
   int coff[SPTK_MAX_MODES];
   int cor_size;  // sum_n jr[n] * rcore
+  long long fac_size;  // foff[n_modes]: total factor entries (rows of mode n = (foff[n+1]-foff[n])/jr[n])
 };
 
 // Nonzeros as packed AoS records of `rw` 32-bit words: idx[0..N) (int32)

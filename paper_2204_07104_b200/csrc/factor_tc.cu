@@ -19,6 +19,9 @@
 #include "kernels.cuh"
 #include "tc.cuh"
 
+#include <stdio.h>
+#include <stdlib.h>
+
 namespace sptk {
 
 template <int N>
@@ -27,6 +30,7 @@ struct TcParams {
   float gam[N];
   float lam[N];
   float* dbg;  // optional per-sample dump of the first tile (debug hook)
+  unsigned atomic_mask;  // bit n: mode-n rows are written as red.add deltas (hot, small modes)
 };
 
 static float* g_tc_debug = nullptr;
@@ -269,9 +273,18 @@ __global__ void __launch_bounds__(128, 1)
       }
       if (valid) {
         float4* dst = reinterpret_cast<float4*>(fac + p.foff[n] + (long long)idx[n] * J);
+        if (p.atomic_mask >> n & 1u) {
 #pragma unroll
-        for (int q = 0; q < J / 4; ++q)
-          __stcg(dst + q, make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]));
+          for (int q = 0; q < J / 4; ++q) {
+            float4 o = get4<128, SPLIT>(at, C::AT, tid, 4 * q);
+            tc::red_add_v4(reinterpret_cast<float*>(dst + q), make_float4(a[4 * q] - o.x, a[4 * q + 1] - o.y,
+                                                                          a[4 * q + 2] - o.z, a[4 * q + 3] - o.w));
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < J / 4; ++q)
+            __stcg(dst + q, make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]));
+        }
       }
       if (n < N - 1) {
 #pragma unroll
@@ -308,18 +321,331 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
-static int g_tc_mode = -1;  // 0 off (CUDA-core FMA kernel), 1 tf32, 3 3xTF32
+// CTAs of a 128-thread tcgen05 kernel that fit on one SM: registers, shared
+// memory (228 KB per SM, 1 KB reserved per CTA) and TMEM (512 columns).
+static int resident_ctas(const void* kfn, size_t smem, int tcols) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kfn) != cudaSuccess) return 1;
+  int regs = fa.numRegs < 1 ? 1 : fa.numRegs;
+  int by_regs = 65536 / (((regs * 32 + 255) / 256) * 256 * 4);
+  int by_smem = (int)((228 * 1024) / (smem + fa.sharedSizeBytes + 1024));
+  int by_tmem = 512 / tcols;
+  int n = by_regs < by_smem ? by_regs : by_smem;
+  n = n < by_tmem ? n : by_tmem;
+  if (const char* e = getenv("SPTK_TC_CTAS")) {
+    int cap = atoi(e);
+    if (cap >= 1 && cap < n) n = cap;
+  }
+  if (getenv("SPTK_DEBUG")) fprintf(stderr, "[sptk] tc kernel regs=%d smem=%zu -> %d CTAs/SM\n", regs, smem, n);
+  return n < 1 ? 1 : n;
+}
+
+// Modes with few rows take many concurrent updates per row; their row writes
+// are issued as red.add deltas so no update is lost (Hogwild with atomic
+// deltas).  Default: modes with fewer than 2^18 rows.  SPTK_ATOMIC_MASK
+// overrides (bit n = mode n).
+static unsigned hot_mode_mask(const ModelDesc& md) {
+  if (const char* e = getenv("SPTK_ATOMIC_MASK")) return (unsigned)strtoul(e, nullptr, 0);
+  unsigned m = 0;
+  for (int n = 0; n < md.n_modes; ++n) {
+    const long long end = n + 1 < md.n_modes ? md.foff[n + 1] : md.fac_size;
+    const long long rows = (end - md.foff[n]) / (md.jr[n] > 0 ? md.jr[n] : 1);
+    if (rows < (1LL << 18)) m |= 1u << n;
+  }
+  return m;
+}
+
+// ----------------------------------------------------------------------------
+// v2 (TF32, the default throughput kernel): 1 + N tensor rounds per tile.
+// The c_n refresh after the row update is folded into the same round as gs:
+//   a' = (1 - g*l) a + g (x - inter) gs   =>   c_n' = (1 - g*l) c_n + g (x - inter) (W_n . G_n)
+// with G_n = B_n^T B_n (R x R, resident), so one MMA round per mode yields
+// both gs = W_n . B_n^T and h = W_n . G_n.  Rows of the next tile are gathered
+// with cp.async straight into the canonical A layout of the idle buffer while
+// the current tile computes; the record/visit streams use L2 evict_first and
+// the factor rows L2 evict_last so the 32 MB model stays L2-resident.
+// ----------------------------------------------------------------------------
+template <int N, int J, int R>
+struct Tc2Cfg {
+  static constexpr int M = 128;
+  static constexpr int OFF_BT = 0;                       // N x (R rows x J)
+  static constexpr int OFF_BN = OFF_BT + N * R * J;      // N x (J rows x R)
+  static constexpr int OFF_G = OFF_BN + N * J * R;       // N x (R rows x R)
+  static constexpr int OFF_A = OFF_G + N * R * R;        // N x (128 x J)
+  static constexpr int OFF_W = OFF_A + N * M * J;        // 128 x R
+  static constexpr int FLOATS = OFF_W + M * R;
+  static constexpr int NEED = (N * R > J + R) ? N * R : J + R;
+  static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
+};
+
+template <int N, int RW>
+struct RecReg {
+  int idx[N];
+  float x;
+  bool valid;
+};
+
+// visit-list entry of this thread's sample in `tile` (-1 past the end)
+__device__ __forceinline__ long long load_vis(const int* __restrict__ visit, long long n_visit, long long tile,
+                                              uint64_t pol) {
+  const long long k = tile * 128 + threadIdx.x;
+  if (k >= n_visit) return -1;
+  return visit ? (long long)tc::ld_stream_s32(visit + k, pol) : k;
+}
+
+template <int N, int RW>
+__device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict__ rec, long long v, long long base,
+                                         uint64_t pol) {
+  o.valid = v >= 0;
+  o.x = 0.f;
+#pragma unroll
+  for (int n = 0; n < N; ++n) o.idx[n] = 0;
+  if (o.valid) {
+    const int* rp = rec + (base + v) * RW;
+    int wv[8];
+    int4 w0 = tc::ld_stream_v4(rp, pol);
+    wv[0] = w0.x;
+    wv[1] = w0.y;
+    wv[2] = w0.z;
+    wv[3] = w0.w;
+    if (RW >= 8) {
+      int4 w1 = tc::ld_stream_v4(rp + 4, pol);
+      wv[4] = w1.x;
+      wv[5] = w1.y;
+      wv[6] = w1.z;
+      wv[7] = w1.w;
+    }
+#pragma unroll
+    for (int n = 0; n < N; ++n) o.idx[n] = wv[n];
+    o.x = __int_as_float(wv[N]);
+  }
+}
+
+template <int N, int J, int R, int RW>
+__global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 128 ? 3 : 2)))
+    factor_tc2_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
+                      float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p) {
+  using C = Tc2Cfg<N, J, R>;
+  extern __shared__ __align__(16) float sm[];
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  for (int e = tid; e < N * J * R; e += 128) {
+    const int n = e / (J * R), rem = e - n * (J * R), j = rem / R, r = rem - j * R;
+    const float b = __ldg(cor + e);
+    sm[C::OFF_BT + n * R * J + canon<R>(r, j)] = b;
+    sm[C::OFF_BN + n * J * R + canon<J>(j, r)] = b;
+  }
+  for (int e = tid; e < N * R * R; e += 128) {
+    const int n = e / (R * R), rem = e - n * (R * R), r = rem / R, r2 = rem - r * R;
+    float g = 0.f;
+    for (int j = 0; j < J; ++j) g = fmaf(__ldg(cor + n * J * R + j * R + r), __ldg(cor + n * J * R + j * R + r2), g);
+    sm[C::OFF_G + n * R * R + canon<R>(r, r2)] = g;
+  }
+  if (tid == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tslot, C::TCOLS);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = tslot;
+  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);
+  const uint32_t sbase = tc::smem_u32(sm);
+  const uint32_t id_c = tc::idesc_tf32(128, R), id_g = tc::idesc_tf32(128, J), id_h = tc::idesc_tf32(128, R);
+  const uint64_t pol_keep = tc::policy_evict_last(), pol_stream = tc::policy_evict_first();
+  uint32_t phase = 0;
+
+  auto issue_rows = [&](const RecReg<N, RW>& rr, int buf) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float* src = fac + p.foff[n] + (long long)rr.idx[n] * J;
+      const uint32_t dst = sbase + 4 * (C::OFF_A + (buf * N + n) * 128 * J);  // buf is always 0
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q)
+        tc::cp_async16(dst + 4 * canon<128>(tid, 4 * q), src + 4 * q, rr.valid ? 16u : 0u, pol_keep);
+    }
+  };
+
+  // records run two tiles ahead (registers); rows are gathered fresh at the
+  // start of their own tile (cp.async into the canonical A layout), so the
+  // Hogwild read-to-write window is one tile.
+  // software pipeline over this CTA's tiles t, t+G, t+2G, t+3G: visit entries
+  // three tiles ahead, records two ahead, rows at the tile itself.
+  const long long G = gridDim.x;
+  long long tile = blockIdx.x;
+  RecReg<N, RW> cur, nxt;
+  long long v2 = load_vis(visit, n_visit, tile + 2 * G, pol_stream);
+  load_rec<N, RW>(cur, rec, load_vis(visit, n_visit, tile, pol_stream), base, pol_stream);
+  load_rec<N, RW>(nxt, rec, load_vis(visit, n_visit, tile + G, pol_stream), base, pol_stream);
+  while (tile * 128 < n_visit) {
+    issue_rows(cur, 0);
+    tc::cp_async_commit();
+    RecReg<N, RW> nnxt;
+    load_rec<N, RW>(nnxt, rec, v2, base, pol_stream);
+    v2 = load_vis(visit, n_visit, tile + 3 * G, pol_stream);
+    tc::cp_async_wait_all();
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const uint32_t a = sbase + 4 * (C::OFF_A + n * 128 * J);
+        const uint32_t b = sbase + 4 * (C::OFF_BT + n * R * J);
+        issue_gemm<R, J, false>(tbase + n * R, a, 0, b, 0, id_c);
+      }
+      tc::mma_commit(&mbar);
+    }
+    tc::mbar_wait(&mbar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+    float c[N][R];
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+      for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + n * R + 16 * q, &c[n][16 * q]);
+
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      float* wt = sm + C::OFF_W;
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q) {
+        float w4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float w = 1.f;
+#pragma unroll
+          for (int n0 = 0; n0 < N; ++n0)
+            if (n0 != n) w *= c[n0][4 * q + u];
+          w4[u] = w;
+        }
+        *reinterpret_cast<float4*>(wt + canon<128>(tid, 4 * q)) = make_float4(w4[0], w4[1], w4[2], w4[3]);
+      }
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t a = sbase + 4 * C::OFF_W;
+        issue_gemm<J, R, false>(tbase, a, 0, sbase + 4 * (C::OFF_BN + n * J * R), 0, id_g);
+        issue_gemm<R, R, false>(tbase + J, a, 0, sbase + 4 * (C::OFF_G + n * R * R), 0, id_h);
+        tc::mma_commit(&mbar);
+      }
+      tc::mbar_wait(&mbar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      float g[J], h[R];
+#pragma unroll
+      for (int q = 0; q < J / 16; ++q) tc::tmem_ld16(tlane + 16 * q, &g[16 * q]);
+#pragma unroll
+      for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + J + 16 * q, &h[16 * q]);
+      const float* at = sm + C::OFF_A + n * 128 * J;
+      float a[J];
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) {
+        float4 v = *reinterpret_cast<const float4*>(at + canon<128>(tid, 4 * q));
+        a[4 * q] = v.x;
+        a[4 * q + 1] = v.y;
+        a[4 * q + 2] = v.z;
+        a[4 * q + 3] = v.w;
+      }
+      float inter = 0.f;
+#pragma unroll
+      for (int j = 0; j < J; ++j) inter = fmaf(a[j], g[j], inter);
+      const float gm = p.gam[n], lm = p.lam[n];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        float gr = -cur.x * g[j] + lm * a[j] + inter * g[j];
+        a[j] -= gm * gr;
+      }
+      if (cur.valid) {
+        float* dst = fac + p.foff[n] + (long long)cur.idx[n] * J;
+        if (p.atomic_mask >> n & 1u) {
+#pragma unroll
+          for (int q = 0; q < J / 4; ++q) {
+            float4 o = *reinterpret_cast<const float4*>(at + canon<128>(tid, 4 * q));
+            tc::red_add_v4(dst + 4 * q, make_float4(a[4 * q] - o.x, a[4 * q + 1] - o.y, a[4 * q + 2] - o.z,
+                                                    a[4 * q + 3] - o.w));
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < J / 4; ++q)
+            tc::st_v4_hint(dst + 4 * q, make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]), pol_keep);
+        }
+      }
+      const float keep = 1.f - gm * lm, step = gm * (cur.x - inter);
+#pragma unroll
+      for (int r = 0; r < R; ++r) c[n][r] = fmaf(step, h[r], keep * c[n][r]);
+    }
+    cur = nxt;
+    nxt = nnxt;
+    tile += G;
+    // the next tile's cp.async overwrites the A tiles read above
+    __syncthreads();
+  }
+  tc::cp_async_wait_all();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tbase, C::TCOLS);
+  }
+}
+
+template <int N, int J, int R>
+static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                      const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+  using C = Tc2Cfg<N, J, R>;
+  TcParams<N> p;
+  for (int n = 0; n < N; ++n) {
+    p.foff[n] = md.foff[n];
+    p.gam[n] = gam[n];
+    p.lam[n] = lam[n];
+  }
+  p.dbg = nullptr;
+  p.atomic_mask = hot_mode_mask(md);
+  auto kfn = rw == 4 ? factor_tc2_kernel<N, J, R, 4> : factor_tc2_kernel<N, J, R, 8>;
+  static int configured = 0;
+  static int per_sm = 1;
+  if (!configured) {
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc2_kernel<N, J, R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)C::SMEM));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc2_kernel<N, J, R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)C::SMEM));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc2_kernel<N, J, R, 4>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc2_kernel<N, J, R, 8>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    per_sm = resident_ctas((const void*)kfn, C::SMEM, C::TCOLS);
+    configured = 1;
+  }
+  long long tiles = (n_visit + 127) / 128;
+  long long blocks = 148LL * per_sm;
+  if (blocks > tiles) blocks = tiles;
+  kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// 0 off (CUDA-core FMA kernel), 1 TF32 v2 (default), 2 TF32 v1, 3 3xTF32 v1
+static int g_tc_mode = -1;
 
 static int tc_mode_env() {
   if (g_tc_mode < 0) {
     const char* e = getenv("SPTK_TC");
-    g_tc_mode = e ? atoi(e) : 3;
+    g_tc_mode = e ? atoi(e) : 1;
   }
   return g_tc_mode;
 }
 
 int set_tc_mode(int mode) {
-  if (mode != 0 && mode != 1 && mode != 3) return 2;
+  if (mode < 0 || mode > 3) return 2;
   g_tc_mode = mode;
   return 0;
 }
@@ -337,6 +663,7 @@ static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit
     p.lam[n] = lam[n];
   }
   p.dbg = g_tc_debug;
+  p.atomic_mask = hot_mode_mask(md);
   auto kfn = rw == 4 ? factor_tc_kernel<N, J, R, SPLIT, 4> : factor_tc_kernel<N, J, R, SPLIT, 8>;
   static int configured = 0;
   static int per_sm = 1;
@@ -345,10 +672,11 @@ static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc_kernel<N, J, R, SPLIT, 8>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    int occ = 1;
-    SPTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, C::SMEM));
-    per_sm = occ < 1 ? 1 : occ;
-    if (per_sm * C::TCOLS > 512) per_sm = 512 / C::TCOLS;
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc_kernel<N, J, R, SPLIT, 4>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc_kernel<N, J, R, SPLIT, 8>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    per_sm = resident_ctas((const void*)kfn, C::SMEM, C::TCOLS);
     configured = 1;
   }
   long long tiles = (n_visit + 127) / 128;
@@ -370,8 +698,9 @@ int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, l
   if (J != R || rw != rec_words(N)) return 0;
 #define SPTK_TC_CASE(NN, JJ)                                                                                 \
   if (N == NN && J == JJ) {                                                                                  \
-    *rc = mode == 1 ? launch_tc<NN, JJ, JJ, false>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s) \
-                    : launch_tc<NN, JJ, JJ, true>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s); \
+    *rc = mode == 1   ? launch_tc2<NN, JJ, JJ>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s)        \
+          : mode == 2 ? launch_tc<NN, JJ, JJ, false>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s) \
+                      : launch_tc<NN, JJ, JJ, true>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);  \
     return 1;                                                                                                \
   }
   SPTK_TC_CASE(3, 16)

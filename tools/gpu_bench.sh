@@ -10,6 +10,6 @@ BENCH_PROFILE=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control
    > gpurun_out/ncu_launch.out 2>&1
 echo "ncu launches rc=$?" >> gpurun_out/bench.err
 BENCH_PROFILE=1 timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off \
-   -k regex:factor_tps -c 1 -o gpurun_out/prof_factor python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline ${BENCH_ARGS} \
+   -k regex:factor_t -c 1 -o gpurun_out/prof_factor python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline ${BENCH_ARGS} \
    > gpurun_out/ncu_full.out 2>&1
 echo "ncu full rc=$?" >> gpurun_out/bench.err
