@@ -34,6 +34,7 @@ struct TcParams {
 };
 
 static float* g_tc_debug = nullptr;
+__device__ unsigned g_tile_ctr[64];
 
 template <int N, int J, int R, bool SPLIT>
 struct TcCfg {
@@ -373,7 +374,7 @@ struct Tc2Cfg {
   static constexpr int OFF_G = OFF_BN + N * J * R;       // N x (R rows x R)
   static constexpr int OFF_A = OFF_G + N * R * R;        // N x (128 x J)
   static constexpr int OFF_W = OFF_A + N * M * J;        // 128 x R
-  static constexpr int FLOATS = OFF_W + M * R;
+  static constexpr int FLOATS = OFF_W + M * R;  // + mbarrier (2 words), TMEM slot, claim slot
   static constexpr int NEED = (N * R > J + R) ? N * R : J + R;
   static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
@@ -425,7 +426,8 @@ __device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict
 template <int N, int J, int R, int RW>
 __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 128 ? 3 : 2)))
     factor_tc2_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
-                      float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p) {
+                      float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p,
+                      unsigned* __restrict__ tile_ctr) {
   using C = Tc2Cfg<N, J, R>;
   extern __shared__ __align__(16) float sm[];
   uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
@@ -476,18 +478,25 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   // Hogwild read-to-write window is one tile.
   // software pipeline over this CTA's tiles t, t+G, t+2G, t+3G: visit entries
   // three tiles ahead, records two ahead, rows at the tile itself.
+  // The first three tiles of a CTA are blockIdx + {0,1,2}*G; later ones are
+  // claimed from a per-launch counter, so CTAs that start late (another
+  // stream's kernel holding the SM) or run slow simply take fewer tiles.
   const long long G = gridDim.x;
-  long long tile = blockIdx.x;
+  uint32_t& s_claim = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 3);
+  long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
+  if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
   RecReg<N, RW> cur, nxt;
-  long long v2 = load_vis(visit, n_visit, tile + 2 * G, pol_stream);
+  long long v2 = load_vis(visit, n_visit, t2, pol_stream);
   load_rec<N, RW>(cur, rec, load_vis(visit, n_visit, tile, pol_stream), base, pol_stream);
-  load_rec<N, RW>(nxt, rec, load_vis(visit, n_visit, tile + G, pol_stream), base, pol_stream);
+  load_rec<N, RW>(nxt, rec, load_vis(visit, n_visit, t1, pol_stream), base, pol_stream);
+  __syncthreads();
+  long long t3 = 3 * G + s_claim;
   while (tile * 128 < n_visit) {
     issue_rows(cur, 0);
     tc::cp_async_commit();
     RecReg<N, RW> nnxt;
     load_rec<N, RW>(nnxt, rec, v2, base, pol_stream);
-    v2 = load_vis(visit, n_visit, tile + 3 * G, pol_stream);
+    v2 = load_vis(visit, n_visit, t3, pol_stream);
     tc::cp_async_wait_all();
     tc::fence_async_smem();
     tc::fence_before_sync();
@@ -585,9 +594,13 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     }
     cur = nxt;
     nxt = nnxt;
-    tile += G;
+    tile = t1;
+    t1 = t2;
+    t2 = t3;
+    if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
     // the next tile's cp.async overwrites the A tiles read above
     __syncthreads();
+    t3 = 3 * G + s_claim;
   }
   tc::cp_async_wait_all();
   tc::fence_before_sync();
@@ -628,7 +641,14 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   long long tiles = (n_visit + 127) / 128;
   long long blocks = 148LL * per_sm;
   if (blocks > tiles) blocks = tiles;
-  kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p);
+  // per-launch tile counter from a small rotating pool (launches on one stream
+  // are ordered; the pool only guards against back-to-back reuse)
+  static unsigned slot = 0;
+  unsigned* ctr = nullptr;
+  SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tile_ctr));
+  ctr += (slot++ & 63u);
+  SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+  kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
   SPTK_CHECK_LAUNCH();
   return 0;
 }

@@ -27,6 +27,9 @@ int partition(const long long* idx64, const double* vals64, long long nnz, int o
               size_t ws_bytes, cudaStream_t s, int f64);
 int pack_records(const long long* idx64, const double* vals64, long long nnz, int order, int* rec_out,
                  cudaStream_t s, int f64);
+size_t radix_ws_bytes(long long n);
+int radix_sort_pairs(unsigned* k0, int* v0, unsigned* k1, int* v1, long long n, int bits, void* ws, size_t ws_bytes,
+                     cudaStream_t s, unsigned** kout, int** vout);
 
 // factor.cu
 template <typename T>

@@ -57,26 +57,52 @@ __global__ void __launch_bounds__(RX_THREADS) radix_hist_kernel(const unsigned* 
   hist[(long long)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
+// Stable scatter of one 8-bit digit pass.  Each tile's elements are first
+// ranked (warp match + per-warp counts, round by round, in source order) into
+// a digit-sorted copy in shared memory, then written out so that consecutive
+// threads store consecutive elements of the same digit (coalesced runs).
 __global__ void __launch_bounds__(RX_THREADS) radix_scatter_kernel(const unsigned* __restrict__ kin,
                                                                    const int* __restrict__ vin, long long n,
                                                                    int shift, int ntiles,
                                                                    const int* __restrict__ offs,
+                                                                   const int* __restrict__ hist,
                                                                    unsigned* __restrict__ kout,
                                                                    int* __restrict__ vout) {
-  __shared__ int run[256];
+  __shared__ int run[256];        // next local slot per digit
+  __shared__ int lstart[256];     // tile-local start of each digit
+  __shared__ int gstart[256];     // global start of each digit for this tile
   __shared__ int wcnt[RX_THREADS / 32][256];
+  __shared__ unsigned sk[RX_TILE];
+  __shared__ int sv[RX_TILE];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  run[threadIdx.x] = offs[(long long)threadIdx.x * ntiles + blockIdx.x];
-  for (int q = 0; q < RX_THREADS / 32; ++q) wcnt[q][threadIdx.x] = 0;
-  __syncthreads();
-  long long base = (long long)blockIdx.x * RX_TILE;
+  {
+    // tile-local exclusive scan of this tile's digit counts
+    const int c = hist[(long long)threadIdx.x * ntiles + blockIdx.x];
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wcnt[0][w] = incl;
+    __syncthreads();
+    int pre = 0;
+    for (int q = 0; q < w; ++q) pre += wcnt[0][q];
+    lstart[threadIdx.x] = pre + incl - c;
+    run[threadIdx.x] = pre + incl - c;
+    gstart[threadIdx.x] = offs[(long long)threadIdx.x * ntiles + blockIdx.x];
+    __syncthreads();
+    for (int q = 0; q < RX_THREADS / 32; ++q) wcnt[q][threadIdx.x] = 0;
+    __syncthreads();
+  }
+  const long long base = (long long)blockIdx.x * RX_TILE;
   const unsigned lt = (1u << lane) - 1u;
   for (int k = 0; k < RX_ITEMS; ++k) {
     long long i = base + (long long)k * RX_THREADS + threadIdx.x;
     bool valid = i < n;
     unsigned key = valid ? kin[i] : 0u;
     int val = valid ? vin[i] : 0;
-    int d = valid ? (int)((key >> shift) & 255u) : 256 + lane;  // invalid lanes: unique groups
+    int d = valid ? (int)((key >> shift) & 255u) : 256 + lane;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     int rank = __popc(peers & lt);
     if (valid && rank == 0) wcnt[w][d] = __popc(peers);
@@ -85,8 +111,8 @@ __global__ void __launch_bounds__(RX_THREADS) radix_scatter_kernel(const unsigne
       int pre = 0;
       for (int q = 0; q < w; ++q) pre += wcnt[q][d];
       int pos = run[d] + pre + rank;
-      kout[pos] = key;
-      vout[pos] = val;
+      sk[pos] = key;
+      sv[pos] = val;
     }
     __syncthreads();
     {
@@ -99,6 +125,14 @@ __global__ void __launch_bounds__(RX_THREADS) radix_scatter_kernel(const unsigne
       run[dd] += add;
     }
     __syncthreads();
+  }
+  const long long cnt = (n - base) < RX_TILE ? (n - base) : RX_TILE;
+  for (int e = threadIdx.x; e < cnt; e += RX_THREADS) {
+    const unsigned key = sk[e];
+    const int d = (key >> shift) & 255u;
+    const long long g = (long long)gstart[d] + (e - lstart[d]);
+    kout[g] = key;
+    vout[g] = sv[e];
   }
 }
 
@@ -215,8 +249,8 @@ int partition(const long long* idx64, const double* vals64, long long nnz, int o
       radix_hist_kernel<<<(unsigned)ntiles, RX_THREADS, 0, s>>>(kin, nnz, shift, (int)ntiles, hist);
       SPTK_CHECK_LAUNCH();
       if (exclusive_scan(hist, 256 * ntiles, offs, sws, s)) return 1;
-      radix_scatter_kernel<<<(unsigned)ntiles, RX_THREADS, 0, s>>>(kin, vin, nnz, shift, (int)ntiles, offs, kout,
-                                                                   vout);
+      radix_scatter_kernel<<<(unsigned)ntiles, RX_THREADS, 0, s>>>(kin, vin, nnz, shift, (int)ntiles, offs, hist,
+                                                                   kout, vout);
       SPTK_CHECK_LAUNCH();
       unsigned* tk = kin;
       kin = kout;
@@ -235,6 +269,45 @@ int partition(const long long* idx64, const double* vals64, long long nnz, int o
   } else {
     SPTK_CUDA_TRY(cudaMemsetAsync(block_off_out, 0, sizeof(int) * (nkeys + 1), s));
   }
+  return 0;
+}
+
+size_t radix_ws_bytes(long long n) {
+  long long ntiles = (n + RX_TILE - 1) / RX_TILE;
+  if (ntiles < 1) ntiles = 1;
+  return (size_t)(256 * ntiles + 2) * 4 * 2 + scan_ws_bytes(256 * ntiles + 1) + 4 * 256;
+}
+
+// Stable LSD radix sort of (key, value) pairs on the low `bits` key bits,
+// ping-ponging between (k0, v0) and (k1, v1); *kout / *vout get the result.
+int radix_sort_pairs(unsigned* k0, int* v0, unsigned* k1, int* v1, long long n, int bits, void* ws, size_t ws_bytes,
+                     cudaStream_t s, unsigned** kout, int** vout) {
+  SPTK_REQUIRE(ws_bytes >= radix_ws_bytes(n), "radix_sort_pairs: workspace too small");
+  long long ntiles = (n + RX_TILE - 1) / RX_TILE;
+  if (ntiles < 1) ntiles = 1;
+  Carve2 cv{(char*)ws, ws_bytes};
+  int* hist = cv.take<int>(256 * ntiles + 2);
+  int* offs = cv.take<int>(256 * ntiles + 2);
+  int* sws = cv.take<int>(scan_ws_bytes(256 * ntiles + 1) / 4 + 1);
+  unsigned* kin = k0;
+  unsigned* kb = k1;
+  int* vin = v0;
+  int* vb = v1;
+  for (int shift = 0; shift < bits && n > 0; shift += 8) {
+    radix_hist_kernel<<<(unsigned)ntiles, RX_THREADS, 0, s>>>(kin, n, shift, (int)ntiles, hist);
+    SPTK_CHECK_LAUNCH();
+    if (exclusive_scan(hist, 256 * ntiles, offs, sws, s)) return 1;
+    radix_scatter_kernel<<<(unsigned)ntiles, RX_THREADS, 0, s>>>(kin, vin, n, shift, (int)ntiles, offs, hist, kb, vb);
+    SPTK_CHECK_LAUNCH();
+    unsigned* tk = kin;
+    kin = kb;
+    kb = tk;
+    int* tv = vin;
+    vin = vb;
+    vb = tv;
+  }
+  *kout = kin;
+  *vout = vin;
   return 0;
 }
 

@@ -36,6 +36,7 @@
 #include <stdio.h>
 
 #include "common.cuh"
+#include "kernels.cuh"
 #include "pcg64.cuh"
 
 namespace sptk {
@@ -148,6 +149,7 @@ __device__ int walk_exact(const Pcg64& g, const u128& A32, const u128& C32, long
   return a;
 }
 
+#define PERM_E_DEV 64
 struct ChunkBuf {
   int* a0;
   int* D;
@@ -216,7 +218,7 @@ __global__ void perm_phaseA_kernel(Pcg64 g, const long long* __restrict__ P, Seg
 // meta[0] = index of the chunk holding the segment end; P[1] = next start.
 __global__ void perm_resolve_kernel(Pcg64 g, long long* __restrict__ P, Seg sg, int L, int C,
                                     int Delta, ChunkBuf cb, int* __restrict__ meta) {
-  __shared__ int2 ent_s[32][40];
+  __shared__ int2 ent_s[32][PERM_E_DEV];
   const int lane = threadIdx.x & 31;
   u128 A32, C32;
   pcg_jump_coeffs(g.inc, 32, &A32, &C32);
@@ -241,11 +243,14 @@ __global__ void perm_resolve_kernel(Pcg64 g, long long* __restrict__ P, Seg sg, 
     for (int e = 0; e < ne; ++e) ent_s[lane][e] = cb.ent[(long long)c * cb.E + e];
     __syncwarp();
     int trig = 0;          // assumed (a0 + D + g) deficit: out = in + D - trig
-    bool fixed = !valid;   // resolved exactly (slow path) or past the end
+    bool fixed = !valid;   // input final and trig exact (or past the end)
     long long in = 0;
-    for (int it = 0; it < 64; ++it) {
+    // Jacobi sweeps: every lane re-evaluates its chunk at the input implied by
+    // the current trig values of the lanes before it.  The first lane whose
+    // value changes (or that needs an exact walk) has a final input, so each
+    // sweep fixes at least one lane; in practice 2-4 sweeps settle a batch.
+    for (int it = 0; it < 70; ++it) {
       int contrib = valid ? D - trig : 0;
-      // exclusive warp prefix of contrib
       int incl = contrib;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -253,43 +258,34 @@ __global__ void perm_resolve_kernel(Pcg64 g, long long* __restrict__ P, Seg sg, 
         if (lane >= o) incl += y;
       }
       in = a + (incl - contrib);
-      bool bad = false;
+      const long long delta = in - a0;
+      const bool walk = !fixed && (ovf || delta >= Delta || delta <= -Delta);
       int ntrig = trig;
-      if (!fixed) {
-        long long delta = in - a0;
-        if (ovf || delta >= Delta || delta <= -Delta) {
-          bad = true;
-        } else {
-          int gg = (int)delta;
-          for (int e = 0; e < ne; ++e) {
-            int m = ent_s[lane][e].y;
-            if (gg > 0 && m >= 0 && m < gg) --gg;
-            else if (gg < 0 && m >= gg && m < 0) ++gg;
-          }
-          ntrig = (int)delta - gg;
-          bad = ntrig != trig;
+      if (!fixed && !walk) {
+        int gg = (int)delta;
+        for (int e = 0; e < ne; ++e) {
+          int m = ent_s[lane][e].y;
+          if (gg > 0 && m >= 0 && m < gg) --gg;
+          else if (gg < 0 && m >= gg && m < 0) ++gg;
         }
+        ntrig = (int)delta - gg;
       }
-      unsigned badm = __ballot_sync(FULLMASK, bad);
+      const unsigned badm = __ballot_sync(FULLMASK, walk || ntrig != trig);
       if (badm == 0) break;
-      int f = __ffs(badm) - 1;
-      // lane f has a final input; resolve it (fast result or exact walk)
-      bool need_walk = __shfl_sync(FULLMASK, (int)(ovf || (in - a0) >= Delta || (in - a0) <= -Delta), f);
-      long long in_f = __shfl_sync(FULLMASK, in, f);
-      int D_f = __shfl_sync(FULLMASK, D, f);
-      int newtrig_f;
-      if (need_walk) {
-        long long qb = Pk + (long long)(c0 + f) * L;
-        int out_f = walk_exact(g, A32, C32, qb, qb + L, (int)in_f, sg, 0x7fffffff, nullptr, nullptr);
-        newtrig_f = (int)(in_f + D_f - out_f);
+      const int f = __ffs(badm) - 1;
+      if (__shfl_sync(FULLMASK, (int)walk, f)) {
+        const long long in_f = __shfl_sync(FULLMASK, in, f);
+        const int D_f = __shfl_sync(FULLMASK, D, f);
+        const long long qb = Pk + (long long)(c0 + f) * L;
+        const int out_f = walk_exact(g, A32, C32, qb, qb + L, (int)in_f, sg, 0x7fffffff, nullptr, nullptr);
+        if (lane == f) {
+          trig = (int)(in_f + D_f - out_f);
+          fixed = true;
+        }
       } else {
-        newtrig_f = __shfl_sync(FULLMASK, ntrig, f);
+        if (!walk) trig = ntrig;
+        if (lane == f) fixed = true;
       }
-      if (lane == f) {
-        trig = newtrig_f;
-        fixed = true;
-      }
-      // lanes before f keep their values (their inputs were already final)
     }
     long long out = in + D - trig;
     // segment end inside this batch?
@@ -771,15 +767,20 @@ static SegPlan plan_segment(long long n, int k) {
   if (var < 0) var = 0;
   double bound = mean + 12.0 * sqrt(var) + 1024.0;
   sp.Delta = (int)ceil(4.0 * sqrt(mean) + 64.0);
-  double Lf = M * 4.0 / (2.0 * sp.Delta);
+  // ~24 near-margin entries per chunk (capacity PERM_E = 64)
+  double Lf = M * 24.0 / (2.0 * sp.Delta);
   int L = 64;
-  while (L * 2 <= Lf && L < 4096) L *= 2;
+  while (L * 2 <= Lf && L < 65536) L *= 2;
   sp.L = L;
   sp.C = (int)ceil(bound / L);
   return sp;
 }
 
-static const int PERM_E = 32;
+static const int PERM_E = 64;
+
+static size_t apply_ws_bytes(long long n) {
+  return (size_t)(4 * (n + 2)) * sizeof(int) + radix_ws_bytes(n + 1) + 8 * 256;
+}
 
 size_t perm_ws_bytes(long long n) {
   // j-generation chunk buffers
@@ -794,8 +795,8 @@ size_t perm_ws_bytes(long long n) {
   size_t b = 0;
   b += 64 * sizeof(long long) + 64;            // P + meta
   b += chunks * (4 * sizeof(int) + PERM_E * sizeof(int2)) + 256;
-  // j (n+1) + apply: cnt, start, list, parent, val (+ scan ws)
-  b += (size_t)(6 * (n + 2)) * sizeof(int) + scan_ws_bytes(n + 1) + 16 * 256;
+  // j (n+1) + apply (values, ping-pong keys/values, parent, radix workspace)
+  b += (size_t)(n + 2) * sizeof(int) + apply_ws_bytes(n) + 16 * 256;
   return b;
 }
 
@@ -858,34 +859,80 @@ int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* 
   return 0;
 }
 
-// result[i] for i in [first, n) of applying steps i = n-1..first with j[i].
-// If first <= 1 the virtual step 0 (j[0] = 0) is included so result[0] is
-// produced too.
+__global__ void fy_iota_kernel(int* __restrict__ v, long long cnt, long long first) {
+  long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; x < cnt; x += stride) v[x] = (int)(first + x);
+}
+
+// sorted by (target, step): parent[p] = first step > p targeting p
+__global__ void fy_parent_kernel(const unsigned* __restrict__ key, const int* __restrict__ val, long long cnt,
+                                 int* __restrict__ parent) {
+  long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; x < cnt; x += stride) {
+    const unsigned p = key[x];
+    if (x > 0 && key[x - 1] == p) continue;
+    const int l1 = val[x];
+    int par = -1;
+    if (l1 > (int)p) par = l1;
+    else if (x + 1 < cnt && key[x + 1] == p) par = val[x + 1];
+    parent[p] = par;
+  }
+}
+
+// result[l_k] = root of the parent chain from l_{k+1}; result[l_last] = p
+__global__ void fy_result2_kernel(const unsigned* __restrict__ key, const int* __restrict__ val, long long cnt,
+                                  const int* __restrict__ parent, int* __restrict__ result) {
+  long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; x < cnt; x += stride) {
+    const unsigned p = key[x];
+    int r;
+    if (x + 1 < cnt && key[x + 1] == p) {
+      int v = val[x + 1];
+      int q = parent[v];
+      while (q >= 0) {
+        v = q;
+        q = parent[v];
+      }
+      r = v;
+    } else {
+      r = (int)p;
+    }
+    result[val[x]] = r;
+  }
+}
+
+
+// result[i] for i in [first, n) of applying steps i = n-1..first with j[i]
+// (j is consumed).  If first <= 1 the virtual step 0 (j[0] = 0) is included
+// so result[0] is produced too.  Steps are grouped by target with a stable
+// radix sort of (j_i, i); see the header comment for the chain formula.
 int fy_apply(int* j, long long n, long long first, int* result, Carve& cv, cudaStream_t s) {
   if (n <= 0) return 0;
   long long f = first <= 1 ? 0 : first;
   if (f == 0) SPTK_CUDA_TRY(cudaMemsetAsync(j, 0, sizeof(int), s));
-  int* cnt = cv.take<int>(n + 1);
-  int* start = cv.take<int>(n + 2);
-  int* list = cv.take<int>(n + 1);
+  const long long cnt = n - f;
+  int* v0 = cv.take<int>(cnt + 1);
+  unsigned* k1 = cv.take<unsigned>(cnt + 1);
+  int* v1 = cv.take<int>(cnt + 1);
   int* parent = cv.take<int>(n + 1);
-  int* val = cv.take<int>(n + 1);
-  int* sws = cv.take<int>(scan_ws_bytes(n + 1) / sizeof(int) + 1);
+  size_t rws = radix_ws_bytes(cnt + 1);
+  void* rw = cv.take<char>(rws);
   SPTK_REQUIRE(cv.ok(), "fy_apply: workspace too small");
-  SPTK_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (n + 1), s));
-  unsigned gb = grid_for(n - f, 256);
-  fy_hist_kernel<<<gb, 256, 0, s>>>(j, f, n, cnt);
+  int bits = 1;
+  while ((1LL << bits) < n) ++bits;
+  unsigned gb = grid_for(cnt, 256);
+  fy_iota_kernel<<<gb, 256, 0, s>>>(v0, cnt, f);
   SPTK_CHECK_LAUNCH();
-  if (exclusive_scan(cnt, n, start, sws, s)) return 1;
-  SPTK_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (n + 1), s));
-  fy_scatter_kernel<<<gb, 256, 0, s>>>(j, f, n, start, cnt, list);
+  unsigned* ks;
+  int* vs;
+  if (radix_sort_pairs((unsigned*)(j + f), v0, k1, v1, cnt, bits, rw, rws, s, &ks, &vs)) return 1;
+  SPTK_CUDA_TRY(cudaMemsetAsync(parent, 0xff, sizeof(int) * n, s));
+  fy_parent_kernel<<<gb, 256, 0, s>>>(ks, vs, cnt, parent);
   SPTK_CHECK_LAUNCH();
-  unsigned gn = grid_for(n, 256);
-  fy_bucket_kernel<<<gn, 256, 0, s>>>(start, list, n, parent);
-  SPTK_CHECK_LAUNCH();
-  fy_val_kernel<<<gn, 256, 0, s>>>(parent, n, val);
-  SPTK_CHECK_LAUNCH();
-  fy_result_kernel<<<gn, 256, 0, s>>>(start, list, val, n, result);
+  fy_result2_kernel<<<gb, 256, 0, s>>>(ks, vs, cnt, parent, result);
   SPTK_CHECK_LAUNCH();
   return 0;
 }
@@ -924,10 +971,6 @@ int permutation_j(const uint64_t st[4], long long n, int* j_out, void* ws, size_
 static long long lemire_vcap(long long T, double p_rej_max) {
   double mean = T * p_rej_max / (1.0 - p_rej_max);
   return T + (long long)(mean + 12.0 * sqrt(mean + 1.0) + 64.0) + LEM_BITS + 64;
-}
-
-static size_t apply_ws_bytes(long long n) {
-  return (size_t)(5 * (n + 2)) * sizeof(int) + scan_ws_bytes(n + 1) + 8 * 256;
 }
 
 size_t choice_ws_bytes(long long pop, long long k) {

@@ -41,7 +41,7 @@ class Workspace:
         return self.buf
 
 
-def permutation(entropy, n: int, out=None, ws: Workspace | None = None, state=None):
+def permutation(entropy, n: int, out=None, ws: Workspace | None = None, state=None, stream=None):
     """Device int32 tensor == default_rng(entropy).permutation(n)."""
     import torch
 
@@ -53,7 +53,7 @@ def permutation(entropy, n: int, out=None, ws: Workspace | None = None, state=No
         out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
     need = int(L.sptk_permutation_ws_bytes(n))
     w = (ws or Workspace()).get(need)
-    check(L.sptk_permutation(sp, n, ptr(out), ptr(w), w.numel(), stream_ptr()), "sptk_permutation")
+    check(L.sptk_permutation(sp, n, ptr(out), ptr(w), w.numel(), stream_ptr(stream)), "sptk_permutation")
     return out[:n] if n else out[:0]
 
 
@@ -71,7 +71,7 @@ def permutation_j(entropy, n: int):
 
 
 def choice(entropy, pop: int, k: int, shuffle: bool = True, out=None, ws: Workspace | None = None,
-           state=None):
+           state=None, stream=None):
     """Device int32 tensor == default_rng(entropy).choice(pop, k, replace=False)
     (shuffle=False: the same set, in Floyd draw order).  Returns (ids, path)."""
     import torch
@@ -86,7 +86,7 @@ def choice(entropy, pop: int, k: int, shuffle: bool = True, out=None, ws: Worksp
     w = (ws or Workspace()).get(need)
     path = ctypes.c_int(0)
     check(L.sptk_choice(sp, pop, k, 1 if shuffle else 0, ptr(out), ptr(w), w.numel(), ctypes.byref(path),
-                        stream_ptr()), "sptk_choice")
+                        stream_ptr(stream)), "sptk_choice")
     return out[:k], ("tail" if path.value == 1 else "floyd")
 
 

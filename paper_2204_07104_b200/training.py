@@ -177,9 +177,16 @@ def resolve_mode(update_mode: str, nnz: int) -> int:
 # device epoch runner
 # --------------------------------------------------------------------------
 class EpochRunner:
-    """Device state for one training run on one GPU (workers = DSGD M)."""
+    """Device state for one training run on one GPU (workers = DSGD M).
 
-    def __init__(self, model: TuckerModel, train_set: SparseTensorCoo, config: TrainConfig):
+    Epochs are pipelined over two CUDA streams: while the main stream runs the
+    factor and core phases of epoch t, a side stream draws epoch t+1's visit
+    orders and core batch (they depend only on (seed, t), trainer.py:300/318)
+    into the other half of double-buffered sample arrays.
+    """
+
+    def __init__(self, model: TuckerModel, train_set: SparseTensorCoo, config: TrainConfig,
+                 prefetch: bool = True):
         import torch
 
         _lib.require_cuda()
@@ -203,13 +210,21 @@ class EpochRunner:
                 if cnt > 0:
                     items.append((block, off, cnt))
             self.rounds.append(items)
-        self.max_block = max((c for r in self.rounds for (_, _, c) in r), default=0)
         dev = self.dm.fac.device
-        self.perm_buf = torch.empty(max(self.max_block, 1), dtype=torch.int32, device=dev)
-        self.perm_ws = Workspace(dev)
+        # visit orders of every block of an epoch, laid out like the records
+        self.perm = [torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
         self.k = min(self.nnz, int(config.core_batch_cap))
-        self.psi_buf = torch.empty(max(self.k, 1), dtype=torch.int32, device=dev)
-        self.psi_ws = Workspace(dev)
+        self.psi = [torch.empty(max(self.k, 1), dtype=torch.int32, device=dev) for _ in range(2)]
+        # one preallocated sampler workspace per stream (never regrown while a
+        # kernel on the other stream may still be using it)
+        Lb = _lib.load()
+        max_block = max((c for items in self.rounds for (_, _, c) in items), default=1)
+        need = int(Lb.sptk_permutation_ws_bytes(max_block))
+        if config.update_core and self.k < self.nnz:
+            need = max(need, int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
+        self.ws = [Workspace(dev), Workspace(dev)]
+        for w in self.ws:
+            w.get(need)
         self.acc = torch.zeros(max(self.dm.cor_size, 1), dtype=torch.float64, device=dev)
         L = _lib.load()
         chunks = self.m if self.mode == 1 else 0
@@ -222,22 +237,55 @@ class EpochRunner:
         self.map = self.part.pos_of_id if self.m > 1 else None
         self.L = L
         self.factor_events = None  # optional list: (start, end) CUDA events per factor launch
+        self.prefetch = prefetch
+        self.side = torch.cuda.Stream(device=dev) if prefetch else None
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.sampled_epoch = [None, None]
 
-    def factor_phase(self, t: int, gamma_a: float) -> int:
-        cfg, L, dm = self.cfg, self.L, self.dm
+    # -- samplers (K2) -----------------------------------------------------
+    def draw_samples(self, t: int, slot: int, stream, ws) -> None:
+        """Visit orders of every block and the core batch of epoch t."""
+        cfg = self.cfg
+        for items in self.rounds:
+            for block, off, cnt in items:
+                permutation(None, cnt, out=self.perm[slot][off:off + cnt], ws=ws,
+                            state=pcg64_state([cfg.seed, 1, t, *block]), stream=stream)
+        if cfg.update_core and self.k < self.nnz:
+            choice(None, self.nnz, self.k, shuffle=(self.mode == 1), out=self.psi[slot], ws=ws,
+                   state=pcg64_state([cfg.seed, 2, t]), stream=stream)
+        self.sampled_epoch[slot] = t
+
+    def _ensure_samples(self, t: int) -> int:
+        torch = self.torch
+        slot = t % 2
+        main = torch.cuda.current_stream()
+        if self.sampled_epoch[slot] != t:
+            self.draw_samples(t, slot, main, self.ws[0])
+        else:
+            main.wait_event(self.ready[slot])
+        if self.prefetch and t + 1 < self.cfg.epochs and self.sampled_epoch[1 - slot] != t + 1:
+            # the other slot was last read by epoch t-1, which `done` marks
+            self.side.wait_event(self.done[1 - slot])
+            self.draw_samples(t + 1, 1 - slot, self.side, self.ws[1])
+            self.ready[1 - slot].record(self.side)
+        return slot
+
+    # -- K3 / K4 / K5 ------------------------------------------------------
+    def factor_phase(self, t: int, gamma_a: float, slot: int) -> int:
+        L, dm = self.L, self.dm
         self._gam[:] = gamma_a
         fn = L.sptk_factor_pass_f64 if self.f64 else L.sptk_factor_pass
         s = stream_ptr()
         processed = 0
+        perm = self.perm[slot]
         for items in self.rounds:
             for block, off, cnt in items:
-                st = pcg64_state([cfg.seed, 1, t, *block])
-                perm = permutation(None, cnt, out=self.perm_buf, ws=self.perm_ws, state=st)
                 if self.factor_events is not None:
                     e0 = self.torch.cuda.Event(enable_timing=True)
                     e0.record()
-                check(fn(ptr(self.part.rec), self.part.rw, ptr(perm), cnt, off, ptr(dm.fac), dm.p_foff,
-                         ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam,
+                check(fn(ptr(self.part.rec), self.part.rw, ptr(perm[off:off + cnt]), cnt, off, ptr(dm.fac),
+                         dm.p_foff, ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam,
                          self.mode, s), "sptk_factor_pass")
                 if self.factor_events is not None:
                     e1 = self.torch.cuda.Event(enable_timing=True)
@@ -246,14 +294,10 @@ class EpochRunner:
                 processed += cnt
         return processed
 
-    def core_phase(self, t: int, gamma_b: float) -> None:
+    def core_phase(self, t: int, gamma_b: float, slot: int) -> None:
         cfg, L, dm = self.cfg, self.L, self.dm
         k = self.k
-        if k == self.nnz:
-            visit = None
-        else:
-            visit, _ = choice(None, self.nnz, k, shuffle=(self.mode == 1), out=self.psi_buf,
-                              ws=self.psi_ws, state=pcg64_state([cfg.seed, 2, t]))
+        visit = None if k == self.nnz else self.psi[slot][:k]
         self.acc.zero_()
         s = stream_ptr()
         fn = L.sptk_core_pass_f64 if self.f64 else L.sptk_core_pass
@@ -267,11 +311,13 @@ class EpochRunner:
               "sptk_core_apply")
 
     def epoch(self, t: int, gamma_a: float, gamma_b: float) -> None:
-        processed = self.factor_phase(t, gamma_a)
+        slot = self._ensure_samples(t)
+        processed = self.factor_phase(t, gamma_a, slot)
         if processed != self.nnz:
             raise RuntimeError("partition did not cover every training entry")
         if self.cfg.update_core:
-            self.core_phase(t, gamma_b)
+            self.core_phase(t, gamma_b, slot)
+        self.done[slot].record(self.torch.cuda.current_stream())
 
 
 def train(model: TuckerModel, split: DatasetSplit, config: TrainConfig) -> list[MetricsRow]:
