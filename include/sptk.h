@@ -78,6 +78,14 @@ size_t sptk_permutation_ws_bytes(long long n);
 /* d_out[n] (int32) = Generator.permutation(n) for the generator in h_state. */
 int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, void* d_ws, size_t ws_bytes,
                      void* stream);
+/* Visit-ordered records: d_rec_out[k] = d_rec_src[perm[k]] (rw 32-bit words
+ * each, rw in {4, 8, 16}) with perm = Generator.permutation(n) for h_state;
+ * d_perm_out (may be NULL) also receives perm.  The factor phase's
+ * `visit = ids[perm]` gather (trainer.py:300-303) fused into the sampler, so
+ * the factor pass streams its block's records sequentially.  Workspace:
+ * sptk_permutation_ws_bytes(n). */
+int sptk_permute_records(const uint64_t h_state[4], long long n, const int32_t* d_rec_src, int rw,
+                         int32_t* d_rec_out, int32_t* d_perm_out, void* d_ws, size_t ws_bytes, void* stream);
 /* test hook: the Fisher-Yates index sequence j_i (i = 1..n-1) of permutation(n). */
 int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,
                        void* stream);

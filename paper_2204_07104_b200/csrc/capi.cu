@@ -150,6 +150,11 @@ int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, voi
   return permutation(h_state, n, d_out, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int sptk_permute_records(const uint64_t h_state[4], long long n, const int32_t* d_rec_src, int rw,
+                         int32_t* d_rec_out, int32_t* d_perm_out, void* d_ws, size_t ws_bytes, void* stream) {
+  return permute_records(h_state, n, d_rec_src, rw, d_rec_out, d_perm_out, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
 int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,
                        void* stream) {
   return permutation_j(h_state, n, d_j, d_ws, ws_bytes, (cudaStream_t)stream);

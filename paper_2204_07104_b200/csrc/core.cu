@@ -21,6 +21,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <stdlib.h>
+
 namespace sptk {
 
 template <typename T>
@@ -140,11 +142,16 @@ __global__ void __launch_bounds__(256) core_pass_kernel(const int* __restrict__ 
   }
 }
 
+// acc[o] += sum_b partial[b][o]: one warp per output, lanes over b, fixed
+// shuffle-tree order (deterministic).  Launch with 256-thread blocks.
 __global__ void core_reduce_kernel(const double* __restrict__ partial, int nblocks, int CS, double* __restrict__ acc) {
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < CS; o += gridDim.x * blockDim.x) {
-    double t = acc[o];
-    for (int b = 0; b < nblocks; ++b) t = __dadd_rn(t, partial[(size_t)b * CS + o]);
-    acc[o] = t;
+  const int lane = threadIdx.x & 31;
+  for (int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); o < CS; o += gridDim.x * (blockDim.x >> 5)) {
+    double t = 0.0;
+    for (int b = lane; b < nblocks; b += 32) t += partial[(size_t)b * CS + o];
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) t += __shfl_xor_sync(0xffffffffu, t, k);
+    if (lane == 0) acc[o] += t;
   }
 }
 
@@ -156,6 +163,230 @@ __global__ void core_reduce_ordered_kernel(const double* __restrict__ partial, i
     for (int b = 1; b < nblocks; ++b) t = __dadd_rn(t, partial[(size_t)b * CS + o]);
     acc[o] = __dadd_rn(acc[o], t);
   }
+}
+
+// ----------------------------------------------------------------------------
+// Throughput K4 for uniform ranks (J_n = J for every mode), fp32:
+// core_tp_kernel<N,J,R,RW>.  128 threads, 128 samples staged per round.
+//   phase 1 (thread <-> sample): gather the N rows (16-byte loads), c[n][r]
+//     against B in shared memory (broadcast reads), residual, coefficient
+//     rows v_n[r] = resid * prod_{n0!=n} c[n0][r]; a_n and v_n go to the
+//     stage as [sample][feature] rows.
+//   phase 2 (register-tiled outer products): thread (n, j0..j0+3, r0..r0+3)
+//     accumulates sum_s a_n[s][j] * v_n[s][r] over its half of the stage; the
+//     two halves and the CTA's rounds are summed in registers, then one fp32
+//     partial per CTA (converted to fp64) is written for the ordered reduce.
+// Per sample: 4(N+1) record bytes + 4*N*J row bytes (B_c).
+// ----------------------------------------------------------------------------
+template <int N, int J, int R, int RW>
+__global__ void __launch_bounds__(128, 4)
+    core_tp_kernel(const int* __restrict__ rec, const int* __restrict__ visit, const int* __restrict__ map,
+                   long long n_visit, const float* __restrict__ fac, const float* __restrict__ cor, ModelDesc md,
+                   double* __restrict__ partial) {
+  constexpr int S = 128;
+  constexpr int F = N * J + N * R;  // stage row: a_0..a_{N-1}, v_0..v_{N-1}
+  constexpr int FP = F + 4;         // padded row (16-byte aligned, shifts banks)
+  constexpr int TJ = J / 4, TR = R / 4, TILES = N * TJ * TR;
+  extern __shared__ __align__(16) float smc[];
+  float* Bs = smc;                      // N*J*R
+  float* st = smc + ((N * J * R + 3) & ~3);  // S x FP
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N * J * R; i += 128) Bs[i] = cor[i];
+  // phase-2 role: TILES <= 64: 64 tile owners x 2 sample halves; otherwise
+  // every thread owns NT tiles over the whole stage.
+  constexpr int HALVES = TILES <= 64 ? 2 : 1;
+  constexpr int OWNERS = 128 / HALVES;
+  constexpr int NT = (TILES + OWNERS - 1) / OWNERS;
+  const int half = HALVES == 2 ? tid / 64 : 0, tl = HALVES == 2 ? tid % 64 : tid;
+  int pn[NT], pj[NT], pr[NT];
+  bool p2[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int ti = tl + t * OWNERS;
+    p2[t] = ti < TILES;
+    const int tt = p2[t] ? ti : 0;
+    pn[t] = tt / (TJ * TR);
+    const int rem = tt % (TJ * TR);
+    pj[t] = 4 * (rem / TR);
+    pr[t] = 4 * (rem % TR);
+  }
+  float acc[NT][4][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[t][u][v] = 0.f;
+  __syncthreads();
+  for (long long kb = (long long)blockIdx.x * S; kb < n_visit; kb += (long long)gridDim.x * S) {
+    const long long k = kb + tid;
+    float* row = st + tid * FP;
+    if (k < n_visit) {
+      const long long s = visit ? (long long)__ldg(visit + k) : k;
+      const long long ri = map ? (long long)__ldg(map + s) : s;
+      const int* rp = rec + ri * RW;
+      int wv[RW];
+      {
+        const int4 w0 = __ldg(reinterpret_cast<const int4*>(rp));
+        wv[0] = w0.x;
+        wv[1] = w0.y;
+        wv[2] = w0.z;
+        wv[3] = w0.w;
+        if (RW >= 8) {
+          const int4 w1 = __ldg(reinterpret_cast<const int4*>(rp) + 1);
+          wv[4 % RW] = w1.x;
+          wv[5 % RW] = w1.y;
+          wv[6 % RW] = w1.z;
+          wv[7 % RW] = w1.w;
+        }
+      }
+      const float x = __int_as_float(wv[N]);
+      float c[N][R];
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const float4* src = reinterpret_cast<const float4*>(fac + md.foff[n] + (long long)wv[n] * J);
+        float a[J];
+#pragma unroll
+        for (int q = 0; q < J / 4; ++q) {
+          const float4 v = __ldg(src + q);
+          a[4 * q] = v.x;
+          a[4 * q + 1] = v.y;
+          a[4 * q + 2] = v.z;
+          a[4 * q + 3] = v.w;
+          *reinterpret_cast<float4*>(row + n * J + 4 * q) = v;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) c[n][r] = 0.f;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+#pragma unroll
+          for (int q = 0; q < R / 4; ++q) {
+            const float4 b = *reinterpret_cast<const float4*>(Bs + n * J * R + j * R + 4 * q);
+            c[n][4 * q] = fmaf(a[j], b.x, c[n][4 * q]);
+            c[n][4 * q + 1] = fmaf(a[j], b.y, c[n][4 * q + 1]);
+            c[n][4 * q + 2] = fmaf(a[j], b.z, c[n][4 * q + 2]);
+            c[n][4 * q + 3] = fmaf(a[j], b.w, c[n][4 * q + 3]);
+          }
+        }
+      }
+      float xhat = 0.f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float pr_ = c[0][r];
+#pragma unroll
+        for (int n = 1; n < N; ++n) pr_ *= c[n][r];
+        xhat += pr_;
+      }
+      const float resid = xhat - x;
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+#pragma unroll
+        for (int q = 0; q < R / 4; ++q) {
+          float w4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float w = resid;
+#pragma unroll
+            for (int n0 = 0; n0 < N; ++n0)
+              if (n0 != n) w *= c[n0][4 * q + u];
+            w4[u] = w;
+          }
+          *reinterpret_cast<float4*>(row + N * J + n * R + 4 * q) = make_float4(w4[0], w4[1], w4[2], w4[3]);
+        }
+    } else {
+#pragma unroll
+      for (int q = 0; q < F / 4; ++q) *reinterpret_cast<float4*>(row + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      if (!p2[t]) continue;
+#pragma unroll 4
+      for (int s2 = half * (S / HALVES); s2 < (half + 1) * (S / HALVES); ++s2) {
+        const float* rr = st + s2 * FP;
+        const float4 a4 = *reinterpret_cast<const float4*>(rr + pn[t] * J + pj[t]);
+        const float4 v4 = *reinterpret_cast<const float4*>(rr + N * J + pn[t] * R + pr[t]);
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[t][u][v] = fmaf(av[u], vv[v], acc[t][u][v]);
+      }
+    }
+    __syncthreads();
+  }
+  // combine the sample halves through the (now idle) stage, write the partial
+  float* red = st;
+  if (HALVES == 2 && half == 1 && p2[0])
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) red[tl * 16 + u * 4 + v] = acc[0][u][v];
+  __syncthreads();
+  if (half == 0) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      if (!p2[t]) continue;
+      double* out = partial + (size_t)blockIdx.x * md.cor_size + md.coff[pn[t]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          out[(pj[t] + u) * R + pr[t] + v] =
+              (double)acc[t][u][v] + (HALVES == 2 ? (double)red[tl * 16 + u * 4 + v] : 0.0);
+    }
+  }
+}
+
+template <int N, int J, int R>
+static int launch_core_tp(const int* rec, int rw, const int* visit, const int* map, long long n_visit,
+                          const float* fac, const float* cor, const ModelDesc& md, double* acc, void* ws,
+                          size_t ws_bytes, cudaStream_t s) {
+  constexpr int S = 128, F = N * J + N * R, FP = F + 4;
+  const size_t smem = sizeof(float) * (((N * J * R + 3) & ~3) + (size_t)S * FP);
+  constexpr int RW = N <= 3 ? 4 : 8;  // rec_words(N); callers check rw
+  auto kfn = core_tp_kernel<N, J, R, RW>;
+  static bool configured = false;
+  if (!configured) {
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  int per_sm = (int)((220 * 1024) / (smem + 1024));
+  if (per_sm > 4) per_sm = 4;
+  if (per_sm < 1) per_sm = 1;
+  long long blocks = (n_visit + S - 1) / S;
+  if (blocks > 148LL * per_sm) blocks = 148LL * per_sm;
+  SPTK_REQUIRE(ws_bytes >= (size_t)blocks * md.cor_size * sizeof(double), "core_pass: workspace too small");
+  double* partial = (double*)ws;
+  kfn<<<(unsigned)blocks, 128, smem, s>>>(rec, visit, map, n_visit, fac, cor, md, partial);
+  SPTK_CHECK_LAUNCH();
+  core_reduce_kernel<<<(md.cor_size + 7) / 8, 256, 0, s>>>(partial, (int)blocks, md.cor_size, acc);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// returns 1 if a specialised kernel handled the call
+static int try_core_tp(const int* rec, int rw, const int* visit, const int* map, long long n_visit,
+                       const float* fac, const float* cor, const ModelDesc& md, double* acc, void* ws,
+                       size_t ws_bytes, cudaStream_t s, int* rc) {
+  const int N = md.n_modes, J = md.jr[0], R = md.rcore;
+  for (int n = 1; n < N; ++n)
+    if (md.jr[n] != J) return 0;
+  if (J != R || rw != rec_words(N)) return 0;
+#define SPTK_CORE_CASE(NN, JJ)                                                                           \
+  if (N == NN && J == JJ) {                                                                              \
+    *rc = launch_core_tp<NN, JJ, JJ>(rec, rw, visit, map, n_visit, fac, cor, md, acc, ws, ws_bytes, s); \
+    return 1;                                                                                            \
+  }
+  SPTK_CORE_CASE(3, 4)
+  SPTK_CORE_CASE(3, 8)
+  SPTK_CORE_CASE(3, 16)
+  SPTK_CORE_CASE(3, 32)
+  SPTK_CORE_CASE(4, 8)
+  SPTK_CORE_CASE(4, 16)
+  SPTK_CORE_CASE(6, 8)
+#undef SPTK_CORE_CASE
+  return 0;
 }
 
 size_t core_ws_bytes(const ModelDesc& md) {
@@ -182,6 +413,12 @@ int core_pass(const int* rec, int rw, const int* visit, const int* map, long lon
   if (n_visit <= 0) return 0;
   const bool f64 = sizeof(T) == 8;
   SPTK_REQUIRE(rw == rec_words_t(md.n_modes, f64), "core_pass: record width mismatch");
+  if (!f64 && !getenv("SPTK_CORE_GENERIC")) {
+    int rc = 0;
+    if (try_core_tp(rec, rw, visit, map, n_visit, (const float*)fac, (const float*)cor, md, acc, ws, ws_bytes, s,
+                    &rc))
+      return rc;
+  }
   int S;
   size_t smem;
   SPTK_REQUIRE(pick_S(md, sizeof(T), &S, &smem), "core_pass: model ranks too large");
@@ -194,7 +431,7 @@ int core_pass(const int* rec, int rw, const int* visit, const int* map, long lon
   kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, rw, rec_val_off(md.n_modes, f64), visit, map, n_visit, fac, cor, md, S,
                                            partial, nullptr);
   SPTK_CHECK_LAUNCH();
-  core_reduce_kernel<<<(md.cor_size + 255) / 256, 256, 0, s>>>(partial, (int)blocks, md.cor_size, acc);
+  core_reduce_kernel<<<(md.cor_size + 7) / 8, 256, 0, s>>>(partial, (int)blocks, md.cor_size, acc);
   SPTK_CHECK_LAUNCH();
   return 0;
 }

@@ -372,8 +372,8 @@ struct Tc2Cfg {
   static constexpr int OFF_BT = 0;                       // N x (R rows x J)
   static constexpr int OFF_BN = OFF_BT + N * R * J;      // N x (J rows x R)
   static constexpr int OFF_G = OFF_BN + N * J * R;       // N x (R rows x R)
-  static constexpr int OFF_A = OFF_G + N * R * R;        // N x (128 x J)
-  static constexpr int OFF_W = OFF_A + N * M * J;        // 128 x R
+  static constexpr int OFF_A = OFF_G + N * R * R;        // N x (128 x J), + 1 spare for the last mode
+  static constexpr int OFF_W = OFF_A + (N + 1) * M * J;  // 128 x R
   static constexpr int FLOATS = OFF_W + M * R;  // + mbarrier (2 words), TMEM slot, claim slot
   static constexpr int NEED = (N * R > J + R) ? N * R : J + R;
   static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
@@ -462,25 +462,30 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   const uint64_t pol_keep = tc::policy_evict_last(), pol_stream = tc::policy_evict_first();
   uint32_t phase = 0;
 
-  auto issue_rows = [&](const RecReg<N, RW>& rr, int buf) {
+  // A-tile slot of mode n: modes 0..N-2 have one slot each, the last mode
+  // alternates between two (pb).
+  auto a_off = [&](int n, int pb) { return C::OFF_A + (n < N - 1 ? n : N - 1 + pb) * 128 * J; };
+  auto issue_mode = [&](const RecReg<N, RW>& rr, int n, int pb) {
+    const float* src = fac + p.foff[n] + (long long)rr.idx[n] * J;
+    const uint32_t dst = sbase + 4 * a_off(n, pb);
+    // no L2::cache_hint operand here: with it ptxas 12.9 pairs the global
+    // descriptor with an odd uniform register (desc[UR1]) in this loop, which
+    // traps as an illegal instruction (the rows are L2-resident anyway)
 #pragma unroll
-    for (int n = 0; n < N; ++n) {
-      const float* src = fac + p.foff[n] + (long long)rr.idx[n] * J;
-      const uint32_t dst = sbase + 4 * (C::OFF_A + (buf * N + n) * 128 * J);  // buf is always 0
-#pragma unroll
-      for (int q = 0; q < J / 4; ++q)
-        tc::cp_async16(dst + 4 * canon<128>(tid, 4 * q), src + 4 * q, rr.valid ? 16u : 0u, pol_keep);
-    }
+    for (int q = 0; q < J / 4; ++q)
+      tc::cp_async16_nohint(dst + 4 * canon<128>(tid, 4 * q), src + 4 * q, rr.valid ? 16u : 0u);
   };
 
-  // records run two tiles ahead (registers); rows are gathered fresh at the
-  // start of their own tile (cp.async into the canonical A layout), so the
-  // Hogwild read-to-write window is one tile.
-  // software pipeline over this CTA's tiles t, t+G, t+2G, t+3G: visit entries
-  // three tiles ahead, records two ahead, rows at the tile itself.
+  // Software pipeline over this CTA's tiles: visit entries three tiles ahead,
+  // records two ahead (registers), factor rows one ahead: the next tile's
+  // mode-n rows are gathered (cp.async into the canonical A layout) as soon as
+  // this tile's last read of its mode-n slot is behind a barrier, and the
+  // last mode has two slots so its gather is issued at the start of the
+  // tile.  The Hogwild read-to-write window is therefore about one tile.
   // The first three tiles of a CTA are blockIdx + {0,1,2}*G; later ones are
-  // claimed from a per-launch counter, so CTAs that start late (another
-  // stream's kernel holding the SM) or run slow simply take fewer tiles.
+  // claimed from a per-launch counter (claim issued at the start of a tile,
+  // consumed at its end), so CTAs that start late (another stream's kernel
+  // holding the SM) or run slow simply take fewer tiles.
   const long long G = gridDim.x;
   uint32_t& s_claim = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 3);
   long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
@@ -489,11 +494,15 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   long long v2 = load_vis(visit, n_visit, t2, pol_stream);
   load_rec<N, RW>(cur, rec, load_vis(visit, n_visit, tile, pol_stream), base, pol_stream);
   load_rec<N, RW>(nxt, rec, load_vis(visit, n_visit, t1, pol_stream), base, pol_stream);
+  int pb = 0;
+#pragma unroll
+  for (int n = 0; n < N; ++n) issue_mode(cur, n, pb);
+  tc::cp_async_commit();
   __syncthreads();
   long long t3 = 3 * G + s_claim;
   while (tile * 128 < n_visit) {
-    issue_rows(cur, 0);
-    tc::cp_async_commit();
+    unsigned claim = 0;
+    if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
     RecReg<N, RW> nnxt;
     load_rec<N, RW>(nnxt, rec, v2, base, pol_stream);
     v2 = load_vis(visit, n_visit, t3, pol_stream);
@@ -505,12 +514,14 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       tc::fence_after_sync();
 #pragma unroll
       for (int n = 0; n < N; ++n) {
-        const uint32_t a = sbase + 4 * (C::OFF_A + n * 128 * J);
+        const uint32_t a = sbase + 4 * a_off(n, pb);
         const uint32_t b = sbase + 4 * (C::OFF_BT + n * R * J);
         issue_gemm<R, J, false>(tbase + n * R, a, 0, b, 0, id_c);
       }
       tc::mma_commit(&mbar);
     }
+    // the next tile's last-mode rows go to the other slot right away
+    issue_mode(nxt, N - 1, pb ^ 1);
     tc::mbar_wait(&mbar, phase);
     phase ^= 1;
     tc::fence_after_sync();
@@ -546,6 +557,9 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
         issue_gemm<R, R, false>(tbase + J, a, 0, sbase + 4 * (C::OFF_G + n * R * R), 0, id_h);
         tc::mma_commit(&mbar);
       }
+      // every thread is past its mode n-1 update: that slot is free for the
+      // next tile's rows
+      if (n >= 1 && n - 1 < N - 1) issue_mode(nxt, n - 1, 0);
       tc::mbar_wait(&mbar, phase);
       phase ^= 1;
       tc::fence_after_sync();
@@ -554,7 +568,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       for (int q = 0; q < J / 16; ++q) tc::tmem_ld16(tlane + 16 * q, &g[16 * q]);
 #pragma unroll
       for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + J + 16 * q, &h[16 * q]);
-      const float* at = sm + C::OFF_A + n * 128 * J;
+      const float* at = sm + a_off(n, pb);
       float a[J];
 #pragma unroll
       for (int q = 0; q < J / 4; ++q) {
@@ -592,13 +606,14 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
 #pragma unroll
       for (int r = 0; r < R; ++r) c[n][r] = fmaf(step, h[r], keep * c[n][r]);
     }
+    tc::cp_async_commit();
     cur = nxt;
     nxt = nnxt;
     tile = t1;
     t1 = t2;
     t2 = t3;
-    if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
-    // the next tile's cp.async overwrites the A tiles read above
+    pb ^= 1;
+    if (tid == 0) s_claim = claim;
     __syncthreads();
     t3 = 3 * G + s_claim;
   }

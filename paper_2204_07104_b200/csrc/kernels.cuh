@@ -11,6 +11,8 @@ namespace sptk {
 // sampler.cu
 size_t perm_ws_bytes(long long n);
 int permutation(const uint64_t st[4], long long n, int* out, void* ws, size_t ws_bytes, cudaStream_t s);
+int permute_records(const uint64_t st[4], long long n, const int* rec_src, int rw, int* rec_out, int* perm_out,
+                    void* ws, size_t ws_bytes, cudaStream_t s);
 int permutation_j(const uint64_t st[4], long long n, int* j_out, void* ws, size_t ws_bytes, cudaStream_t s);
 size_t choice_ws_bytes(long long pop, long long k);
 int choice(const uint64_t st[4], long long pop, long long k, int shuffle, int* out, void* ws,

@@ -778,9 +778,7 @@ static SegPlan plan_segment(long long n, int k) {
 
 static const int PERM_E = 64;
 
-static size_t apply_ws_bytes(long long n) {
-  return (size_t)(4 * (n + 2)) * sizeof(int) + radix_ws_bytes(n + 1) + 8 * 256;
-}
+static size_t apply_ws_bytes(long long n);
 
 size_t perm_ws_bytes(long long n) {
   // j-generation chunk buffers
@@ -859,82 +857,239 @@ int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* 
   return 0;
 }
 
-__global__ void fy_iota_kernel(int* __restrict__ v, long long cnt, long long first) {
-  long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  for (; x < cnt; x += stride) v[x] = (int)(first + x);
-}
+// ---------------------------------------------------------------------------
+// (3) applying the swap sequence: two bucket partitions around a per-bucket
+// sort, so that every pass is either sequential or L2-local.
+//
+//   B  partition the steps by target bucket (2^lg positions per bucket):
+//      per-CTA shared-memory histograms -> scan -> scatter with shared-memory
+//      cursors (write fronts merge in L2), payload (step, target).
+//   C  one CTA per target bucket: counting sort by target in an L2-resident
+//      scratch, insertion sort of each (short, O(log n)) step list, then
+//      parent[p] = first step > p targeting p, and each entry rewritten as
+//      (step, next step of its target list, or -(p+1) for the last).
+//   D  partition those entries by step bucket (same primitive as B).
+//   E  one CTA per step bucket: v = root of the parent chain from the
+//      successor (or p); result[step] = v, and/or the record gather
+//      out_rec[step] = src_rec[v] -- writes land in the bucket's own
+//      contiguous range, so the visit-ordered records stream out
+//      sequentially and the factor pass reads them without indirection.
+// Random DRAM traffic is one parent read per chain hop (~1 per step on
+// average) plus, for the record gather, one record read per step.
+// ---------------------------------------------------------------------------
+#define PART_G 148
+#define PART_T 1024
 
-// sorted by (target, step): parent[p] = first step > p targeting p
-__global__ void fy_parent_kernel(const unsigned* __restrict__ key, const int* __restrict__ val, long long cnt,
-                                 int* __restrict__ parent) {
-  long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  for (; x < cnt; x += stride) {
-    const unsigned p = key[x];
-    if (x > 0 && key[x - 1] == p) continue;
-    const int l1 = val[x];
-    int par = -1;
-    if (l1 > (int)p) par = l1;
-    else if (x + 1 < cnt && key[x + 1] == p) par = val[x + 1];
-    parent[p] = par;
-  }
-}
-
-// result[l_k] = root of the parent chain from l_{k+1}; result[l_last] = p
-__global__ void fy_result2_kernel(const unsigned* __restrict__ key, const int* __restrict__ val, long long cnt,
-                                  const int* __restrict__ parent, int* __restrict__ result) {
-  long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  for (; x < cnt; x += stride) {
-    const unsigned p = key[x];
-    int r;
-    if (x + 1 < cnt && key[x + 1] == p) {
-      int v = val[x + 1];
-      int q = parent[v];
-      while (q >= 0) {
-        v = q;
-        q = parent[v];
-      }
-      r = v;
-    } else {
-      r = (int)p;
-    }
-    result[val[x]] = r;
-  }
-}
-
-
-// result[i] for i in [first, n) of applying steps i = n-1..first with j[i]
-// (j is consumed).  If first <= 1 the virtual step 0 (j[0] = 0) is included
-// so result[0] is produced too.  Steps are grouped by target with a stable
-// radix sort of (j_i, i); see the header comment for the chain formula.
-int fy_apply(int* j, long long n, long long first, int* result, Carve& cv, cudaStream_t s) {
-  if (n <= 0) return 0;
-  long long f = first <= 1 ? 0 : first;
-  if (f == 0) SPTK_CUDA_TRY(cudaMemsetAsync(j, 0, sizeof(int), s));
-  const long long cnt = n - f;
-  int* v0 = cv.take<int>(cnt + 1);
-  unsigned* k1 = cv.take<unsigned>(cnt + 1);
-  int* v1 = cv.take<int>(cnt + 1);
-  int* parent = cv.take<int>(n + 1);
-  size_t rws = radix_ws_bytes(cnt + 1);
-  void* rw = cv.take<char>(rws);
-  SPTK_REQUIRE(cv.ok(), "fy_apply: workspace too small");
+static inline int fy_bucket_log(long long n) {
   int bits = 1;
   while ((1LL << bits) < n) ++bits;
-  unsigned gb = grid_for(cnt, 256);
-  fy_iota_kernel<<<gb, 256, 0, s>>>(v0, cnt, f);
+  int lg = bits - 13;
+  return lg < 14 ? 14 : lg;
+}
+
+template <bool FROM_J>
+__device__ __forceinline__ int part_key(const int* __restrict__ j, const int2* __restrict__ e, long long i) {
+  return FROM_J ? __ldcs(j + i) : __ldcs(e + i).x;
+}
+
+// in: FROM_J: j[f..n) (key = target, payload (i, j[i])); else e[0..cnt) (key = e.x)
+template <bool FROM_J>
+__global__ void __launch_bounds__(PART_T) part_hist_kernel(const int* __restrict__ j, const int2* __restrict__ e,
+                                                           long long lo, long long hi, int lg, int nbk,
+                                                           int* __restrict__ hist) {
+  extern __shared__ int hsm[];
+  for (int b = threadIdx.x; b < nbk; b += PART_T) hsm[b] = 0;
+  __syncthreads();
+  const long long len = hi - lo, per = (len + gridDim.x - 1) / gridDim.x;
+  const long long a = lo + per * blockIdx.x, z = min(hi, a + per);
+  for (long long i = a + threadIdx.x; i < z; i += PART_T) atomicAdd(&hsm[part_key<FROM_J>(j, e, i) >> lg], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbk; b += PART_T) hist[(size_t)b * gridDim.x + blockIdx.x] = hsm[b];
+}
+
+template <bool FROM_J>
+__global__ void __launch_bounds__(PART_T) part_scatter_kernel(const int* __restrict__ j, const int2* __restrict__ e,
+                                                              long long lo, long long hi, int lg, int nbk,
+                                                              const int* __restrict__ offs, int2* __restrict__ out) {
+  extern __shared__ int csm[];
+  for (int b = threadIdx.x; b < nbk; b += PART_T) csm[b] = offs[(size_t)b * gridDim.x + blockIdx.x];
+  __syncthreads();
+  const long long len = hi - lo, per = (len + gridDim.x - 1) / gridDim.x;
+  const long long a = lo + per * blockIdx.x, z = min(hi, a + per);
+  for (long long i = a + threadIdx.x; i < z; i += PART_T) {
+    int2 v;
+    if (FROM_J) {
+      v.x = (int)i;
+      v.y = __ldcs(j + i);
+    } else {
+      v = __ldcs(e + i);
+    }
+    const int slot = atomicAdd(&csm[(FROM_J ? v.y : v.x) >> lg], 1);
+    __stcg(out + slot, v);
+  }
+}
+
+// C: per target bucket.  Dynamic smem: cnt[B] + cur[B] ints.
+// (cnt/cur live in shared memory for buckets of <= 2^14 positions, else in
+// the per-bucket slice of gcc[2 * 2^lg * nbk].)
+__global__ void __launch_bounds__(1024) fy_target_kernel(const int* __restrict__ offs, int G, long long n, int lg,
+                                                          const int2* __restrict__ ent, int* __restrict__ tmp,
+                                                          int* __restrict__ parent, int2* __restrict__ out,
+                                                          long long cnt_total, int* __restrict__ gcc) {
+  extern __shared__ int tsm[];
+  __shared__ int sh[33];
+  const int B = 1 << lg;
+  int* cnt = gcc ? gcc + ((size_t)blockIdx.x << (lg + 1)) : tsm;
+  int* cur = cnt + B;
+  const int b = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
+  const long long base = (long long)b << lg;
+  const long long e0 = offs[(size_t)b * G];
+  const long long e1 = (size_t)(b + 1) * G < (size_t)gridDim.x * G ? offs[(size_t)(b + 1) * G] : cnt_total;
+  for (int t = tid; t < B; t += T) cnt[t] = 0;
+  __syncthreads();
+  for (long long e = e0 + tid; e < e1; e += T) atomicAdd(&cnt[ent[e].y - (int)base], 1);
+  __syncthreads();
+  // exclusive scan of cnt into cur (thread-contiguous runs of B/T)
+  const int per = B / T;
+  int run = 0;
+  for (int k = 0; k < per; ++k) run += cnt[tid * per + k];
+  int tot;
+  int ex = block_excl_scan(run, sh, &tot);
+  for (int k = 0; k < per; ++k) {
+    cur[tid * per + k] = ex;
+    ex += cnt[tid * per + k];
+  }
+  __syncthreads();
+  for (long long e = e0 + tid; e < e1; e += T) {
+    const int2 v = ent[e];
+    const int slot = atomicAdd(&cur[v.y - (int)base], 1);
+    tmp[e0 + slot] = v.x;
+  }
+  __syncthreads();
+  // cur[t] = end of target t's segment (relative to e0), cnt[t] its length
+  for (int t = tid; t < B; t += T) {
+    const long long p = base + t;
+    if (p >= n) break;
+    const int m = cnt[t];
+    const long long st = e0 + cur[t] - m;
+    int* L = tmp + st;
+    for (int x = 1; x < m; ++x) {
+      const int v = L[x];
+      int c = x - 1;
+      while (c >= 0 && L[c] > v) {
+        L[c + 1] = L[c];
+        --c;
+      }
+      L[c + 1] = v;
+    }
+    int par = -1;
+    if (m > 0) par = L[0] > (int)p ? L[0] : (m > 1 ? L[1] : -1);
+    parent[p] = par;
+    for (int k = 0; k < m; ++k) out[st + k] = make_int2(L[k], k + 1 < m ? L[k + 1] : -(int)(p + 1));
+  }
+}
+
+// E: per step bucket; entries e[lo..hi) are the bucket's steps in any order.
+__global__ void __launch_bounds__(256) fy_emit_kernel(const int* __restrict__ offs, int G, int nbk,
+                                                      const int2* __restrict__ ent, long long cnt_total,
+                                                      const int* __restrict__ parent, int* __restrict__ result,
+                                                      const int4* __restrict__ src, int4* __restrict__ dst,
+                                                      int rq) {
+  const int b = blockIdx.x;
+  const long long e0 = offs[(size_t)b * G];
+  const long long e1 = b + 1 < nbk ? offs[(size_t)(b + 1) * G] : cnt_total;
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int2 v2 = ent[e];
+    int v = v2.y;
+    if (v >= 0) {
+      int q = __ldcg(parent + v);
+      while (q >= 0) {
+        v = q;
+        q = __ldcg(parent + v);
+      }
+    } else {
+      v = -v - 1;
+    }
+    if (result) result[v2.x] = v;
+    if (dst) {
+      const int4* sp = src + (long long)v * rq;
+      int4* dp = dst + (long long)v2.x * rq;
+      for (int k = 0; k < rq; ++k) dp[k] = __ldcs(sp + k);
+    }
+  }
+}
+
+#define FY_SMEM_LG 14
+static size_t apply_ws_bytes(long long n) {
+  const int lg = fy_bucket_log(n > 1 ? n : 2);
+  const long long nbk = (n + (1LL << lg) - 1) >> lg;
+  const long long hs = nbk * PART_G + 2;
+  size_t b = (size_t)(n + 2) * (2 * sizeof(int2) + 2 * sizeof(int)) + (size_t)hs * 2 * sizeof(int) +
+             scan_ws_bytes(hs) + 16 * 256;
+  if (lg > FY_SMEM_LG) b += (((size_t)nbk << (lg + 1)) + 1) * sizeof(int) + 256;
+  return b;
+}
+
+// Apply steps i = n-1..first (target j[i]) to the identity; result[i] (if
+// non-NULL) = final value at position i, and/or dst_rec[i] = src_rec[result[i]]
+// (rq int4 per record), for i in [first, n).  If first <= 1 the virtual step
+// 0 (j[0] = 0) is included so position 0 is produced too.  j is read only.
+static int fy_apply_ex(int* j, long long n, long long first, int* result, const int* src_rec, int* dst_rec, int rq,
+                       Carve& cv, cudaStream_t s) {
+  if (n <= 0) return 0;
+  const long long f = first <= 1 ? 0 : first;
+  if (f == 0) SPTK_CUDA_TRY(cudaMemsetAsync(j, 0, sizeof(int), s));
+  const long long cnt = n - f;
+  const int lg = fy_bucket_log(n > 1 ? n : 2);
+  const int nbk = (int)((n + (1LL << lg) - 1) >> lg);
+  const int G = PART_G;
+  const long long hs = (long long)nbk * G;
+  int2* e1 = cv.take<int2>(cnt + 1);
+  int2* e2 = cv.take<int2>(cnt + 1);
+  int* tmp = cv.take<int>(cnt + 1);
+  int* parent = cv.take<int>(n + 1);
+  int* hist = cv.take<int>(hs + 2);
+  int* offs = cv.take<int>(hs + 2);
+  int* sws = cv.take<int>(scan_ws_bytes(hs + 1) / sizeof(int) + 1);
+  int* gcc = lg > FY_SMEM_LG ? cv.take<int>(((size_t)nbk << (lg + 1)) + 1) : nullptr;
+  SPTK_REQUIRE(cv.ok(), "fy_apply: workspace too small");
+  const size_t hsm = sizeof(int) * (size_t)nbk;
+  static bool configured = false;
+  if (!configured) {
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(part_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(part_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(part_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
+    SPTK_CUDA_TRY(
+        cudaFuncSetAttribute(part_scatter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(fy_target_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 << FY_SMEM_LG));
+    configured = true;
+  }
+  SPTK_REQUIRE(hsm <= (96u << 10), "fy_apply: n=%lld too large", n);
+  const size_t tsm = gcc ? 0 : (size_t)8 << lg;
+  // B: steps by target bucket -> e1
+  part_hist_kernel<true><<<G, PART_T, hsm, s>>>(j, nullptr, f, n, lg, nbk, hist);
   SPTK_CHECK_LAUNCH();
-  unsigned* ks;
-  int* vs;
-  if (radix_sort_pairs((unsigned*)(j + f), v0, k1, v1, cnt, bits, rw, rws, s, &ks, &vs)) return 1;
-  SPTK_CUDA_TRY(cudaMemsetAsync(parent, 0xff, sizeof(int) * n, s));
-  fy_parent_kernel<<<gb, 256, 0, s>>>(ks, vs, cnt, parent);
+  if (exclusive_scan(hist, hs, offs, sws, s)) return 1;
+  part_scatter_kernel<true><<<G, PART_T, hsm, s>>>(j, nullptr, f, n, lg, nbk, offs, e1);
   SPTK_CHECK_LAUNCH();
-  fy_result2_kernel<<<gb, 256, 0, s>>>(ks, vs, cnt, parent, result);
+  // C: per target bucket -> parent, e2 = (step, successor)
+  fy_target_kernel<<<nbk, 1024, tsm, s>>>(offs, G, n, lg, e1, tmp, parent, e2, cnt, gcc);
+  SPTK_CHECK_LAUNCH();
+  // D: entries by step bucket -> e1
+  part_hist_kernel<false><<<G, PART_T, hsm, s>>>(nullptr, e2, 0, cnt, lg, nbk, hist);
+  SPTK_CHECK_LAUNCH();
+  if (exclusive_scan(hist, hs, offs, sws, s)) return 1;
+  part_scatter_kernel<false><<<G, PART_T, hsm, s>>>(nullptr, e2, 0, cnt, lg, nbk, offs, e1);
+  SPTK_CHECK_LAUNCH();
+  // E: roots, results / record gather
+  fy_emit_kernel<<<nbk, 256, 0, s>>>(offs, G, nbk, e1, cnt, parent, result, reinterpret_cast<const int4*>(src_rec),
+                                     reinterpret_cast<int4*>(dst_rec), rq);
   SPTK_CHECK_LAUNCH();
   return 0;
+}
+
+int fy_apply(int* j, long long n, long long first, int* result, Carve& cv, cudaStream_t s) {
+  return fy_apply_ex(j, n, first, result, nullptr, nullptr, 0, cv, s);
 }
 
 int permutation(const uint64_t st[4], long long n, int* out, void* ws, size_t ws_bytes, cudaStream_t s) {
@@ -953,6 +1108,29 @@ int permutation(const uint64_t st[4], long long n, int* out, void* ws, size_t ws
   Pcg64 g = make_pcg(st);
   if (perm_jgen(g, n, j, cv, d_P, d_meta, s)) return 1;
   return fy_apply(j, n, 1, out, cv, s);
+}
+
+// rec_out[k] = rec_src[perm[k]] (rw 32-bit words per record), perm =
+// Generator.permutation(n); perm_out (optional) receives perm itself.
+int permute_records(const uint64_t st[4], long long n, const int* rec_src, int rw, int* rec_out, int* perm_out,
+                    void* ws, size_t ws_bytes, cudaStream_t s) {
+  SPTK_REQUIRE(n >= 0 && n < (1LL << 30), "permute_records: n=%lld out of range [0, 2^30)", n);
+  SPTK_REQUIRE(rw == 4 || rw == 8 || rw == 16, "permute_records: rw=%d not in {4, 8, 16}", rw);
+  SPTK_REQUIRE(ws_bytes >= perm_ws_bytes(n), "permute_records: workspace too small (%zu < %zu)", ws_bytes,
+               perm_ws_bytes(n));
+  if (n == 0) return 0;
+  if (n == 1) {
+    SPTK_CUDA_TRY(cudaMemcpyAsync(rec_out, rec_src, sizeof(int) * rw, cudaMemcpyDeviceToDevice, s));
+    if (perm_out) SPTK_CUDA_TRY(cudaMemsetAsync(perm_out, 0, sizeof(int), s));
+    return 0;
+  }
+  Carve cv{(char*)ws, ws_bytes};
+  long long* d_P = cv.take<long long>(66);
+  int* d_meta = cv.take<int>(66);
+  int* j = cv.take<int>(n + 1);
+  Pcg64 g = make_pcg(st);
+  if (perm_jgen(g, n, j, cv, d_P, d_meta, s)) return 1;
+  return fy_apply_ex(j, n, 1, perm_out, rec_src, rec_out, rw / 4, cv, s);
 }
 
 // j-sequence only (tests): j_out[i] for i in [1, n)

@@ -57,6 +57,21 @@ def permutation(entropy, n: int, out=None, ws: Workspace | None = None, state=No
     return out[:n] if n else out[:0]
 
 
+def permute_records(n: int, src, rw: int, out, ws: Workspace | None = None, state=None, entropy=None,
+                    perm_out=None, stream=None):
+    """out[k] = src[perm[k]] for the records of one block (rw int32 words each),
+    perm = default_rng(entropy).permutation(n): the visit-ordered records of
+    trainer.py:300-303 (``visit = ids[perm]``) in one fused sampler call."""
+    _lib.require_cuda()
+    L = _lib.load()
+    st = state if state is not None else pcg64_state(entropy)
+    stc, sp = u64arr(st)
+    w = (ws or Workspace()).get(int(L.sptk_permutation_ws_bytes(n)))
+    check(L.sptk_permute_records(sp, n, ptr(src), rw, ptr(out), ptr(perm_out), ptr(w), w.numel(),
+                                 stream_ptr(stream)), "sptk_permute_records")
+    return out
+
+
 def permutation_j(entropy, n: int):
     """The Fisher-Yates index sequence j_i (i = 1..n-1) of permutation(n)."""
     import torch

@@ -43,7 +43,7 @@ import numpy as np
 from . import _lib
 from ._lib import check, f64arr, ptr, stream_ptr
 from .device import DeviceCoo, DeviceModel, rmse_mae_device
-from .sampler import Workspace, choice, pcg64_state, permutation
+from .sampler import Workspace, choice, pcg64_state, permutation, permute_records
 from .schedule import DevicePartition, round_schedule
 from .tensor import DatasetSplit, SparseTensorCoo
 from .tucker import TuckerModel
@@ -211,8 +211,20 @@ class EpochRunner:
                     items.append((block, off, cnt))
             self.rounds.append(items)
         dev = self.dm.fac.device
-        # visit orders of every block of an epoch, laid out like the records
-        self.perm = [torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
+        # Visit orders of every block of an epoch (double-buffered), laid out
+        # like the partitioned records.  With gather_records the sampler also
+        # applies them to the records (sptk_permute_records), so the factor
+        # pass streams visit-ordered records with no indirection; otherwise the
+        # factor pass gathers rec[visit[k]] itself.  Both cost one random
+        # record read per sample; which is cheaper depends on whether the
+        # factor kernel or the sampler has DRAM headroom (SPTK_GATHER=1).
+        import os
+
+        self.gather_records = os.environ.get("SPTK_GATHER", "0") == "1"
+        if self.gather_records:
+            self.prec = [torch.empty_like(self.part.rec) for _ in range(2)]
+        else:
+            self.perm = [torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
         self.k = min(self.nnz, int(config.core_batch_cap))
         self.psi = [torch.empty(max(self.k, 1), dtype=torch.int32, device=dev) for _ in range(2)]
         # one preallocated sampler workspace per stream (never regrown while a
@@ -222,9 +234,12 @@ class EpochRunner:
         need = int(Lb.sptk_permutation_ws_bytes(max_block))
         if config.update_core and self.k < self.nnz:
             need = max(need, int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
-        self.ws = [Workspace(dev), Workspace(dev)]
-        for w in self.ws:
+        # [main, side (visit orders), side2 (core batch)]
+        self.ws = [Workspace(dev), Workspace(dev), Workspace(dev)]
+        for w in self.ws[:2]:
             w.get(need)
+        if config.update_core and self.k < self.nnz:
+            self.ws[2].get(int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
         self.acc = torch.zeros(max(self.dm.cor_size, 1), dtype=torch.float64, device=dev)
         L = _lib.load()
         chunks = self.m if self.mode == 1 else 0
@@ -239,21 +254,39 @@ class EpochRunner:
         self.factor_events = None  # optional list: (start, end) CUDA events per factor launch
         self.prefetch = prefetch
         self.side = torch.cuda.Stream(device=dev) if prefetch else None
+        self.side2 = torch.cuda.Stream(device=dev) if prefetch else None
         self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.ready2 = [torch.cuda.Event(), torch.cuda.Event()]
         self.done = [torch.cuda.Event(), torch.cuda.Event()]
         self.sampled_epoch = [None, None]
 
     # -- samplers (K2) -----------------------------------------------------
-    def draw_samples(self, t: int, slot: int, stream, ws) -> None:
-        """Visit orders of every block and the core batch of epoch t."""
+    def draw_core_batch(self, t: int, slot: int, stream, ws) -> None:
+        """Core batch Psi of epoch t (trainer.py:316-324)."""
         cfg = self.cfg
-        for items in self.rounds:
-            for block, off, cnt in items:
-                permutation(None, cnt, out=self.perm[slot][off:off + cnt], ws=ws,
-                            state=pcg64_state([cfg.seed, 1, t, *block]), stream=stream)
         if cfg.update_core and self.k < self.nnz:
             choice(None, self.nnz, self.k, shuffle=(self.mode == 1), out=self.psi[slot], ws=ws,
                    state=pcg64_state([cfg.seed, 2, t]), stream=stream)
+
+    def draw_visit_orders(self, t: int, slot: int, stream, ws) -> None:
+        """Visit orders of every block of epoch t (trainer.py:294-303), applied
+        to the block's records: prec[slot] holds each block's records in the
+        exact order the reference visits them."""
+        cfg = self.cfg
+        rw = self.part.rw
+        for items in self.rounds:
+            for block, off, cnt in items:
+                st = pcg64_state([cfg.seed, 1, t, *block])
+                if self.gather_records:
+                    permute_records(cnt, self.part.rec[off * rw:(off + cnt) * rw], rw,
+                                    self.prec[slot][off * rw:(off + cnt) * rw], ws=ws, state=st, stream=stream)
+                else:
+                    permutation(None, cnt, out=self.perm[slot][off:off + cnt], ws=ws, state=st, stream=stream)
+
+    def draw_samples(self, t: int, slot: int, stream, ws) -> None:
+        """Visit orders of every block and the core batch of epoch t."""
+        self.draw_core_batch(t, slot, stream, self.ws[2])
+        self.draw_visit_orders(t, slot, stream, ws)
         self.sampled_epoch[slot] = t
 
     def _ensure_samples(self, t: int) -> int:
@@ -264,11 +297,19 @@ class EpochRunner:
             self.draw_samples(t, slot, main, self.ws[0])
         else:
             main.wait_event(self.ready[slot])
+            main.wait_event(self.ready2[slot])
         if self.prefetch and t + 1 < self.cfg.epochs and self.sampled_epoch[1 - slot] != t + 1:
-            # the other slot was last read by epoch t-1, which `done` marks
-            self.side.wait_event(self.done[1 - slot])
-            self.draw_samples(t + 1, 1 - slot, self.side, self.ws[1])
-            self.ready[1 - slot].record(self.side)
+            # The other slot was last read by epoch t-1, which `done` marks.  The
+            # core batch (a latency-bound single-CTA resolver) goes first on its
+            # own stream so it runs beside this epoch's factor pass.
+            o = 1 - slot
+            self.side2.wait_event(self.done[o])
+            self.draw_core_batch(t + 1, o, self.side2, self.ws[2])
+            self.ready2[o].record(self.side2)
+            self.side.wait_event(self.done[o])
+            self.draw_visit_orders(t + 1, o, self.side, self.ws[1])
+            self.ready[o].record(self.side)
+            self.sampled_epoch[o] = t + 1
         return slot
 
     # -- K3 / K4 / K5 ------------------------------------------------------
@@ -278,15 +319,18 @@ class EpochRunner:
         fn = L.sptk_factor_pass_f64 if self.f64 else L.sptk_factor_pass
         s = stream_ptr()
         processed = 0
-        perm = self.perm[slot]
         for items in self.rounds:
             for block, off, cnt in items:
                 if self.factor_events is not None:
                     e0 = self.torch.cuda.Event(enable_timing=True)
                     e0.record()
-                check(fn(ptr(self.part.rec), self.part.rw, ptr(perm[off:off + cnt]), cnt, off, ptr(dm.fac),
-                         dm.p_foff, ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam,
-                         self.mode, s), "sptk_factor_pass")
+                if self.gather_records:
+                    rec, visit = self.prec[slot], None
+                else:
+                    rec, visit = self.part.rec, self.perm[slot][off:off + cnt]
+                check(fn(ptr(rec), self.part.rw, ptr(visit), cnt, off, ptr(dm.fac), dm.p_foff, ptr(dm.cor),
+                         dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam, self.mode, s),
+                      "sptk_factor_pass")
                 if self.factor_events is not None:
                     e1 = self.torch.cuda.Event(enable_timing=True)
                     e1.record()

@@ -208,3 +208,34 @@ def test_factor_hogwild_conflict_free_equals_sequential(dims, J, R, tc):
                   np.full(len(dims), 0.01))
     rtol = 5e-3 if tc in (1, 2) else 1e-4
     np.testing.assert_allclose(got, want, rtol=rtol, atol=rtol * 0.1 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("dims,J", [((40, 50, 60), 4), ((300, 40, 30), 8), ((200, 300, 100), 16),
+                                    ((50, 60, 70), 32), ((30, 40, 50, 60), 8), ((30, 40, 50, 60), 16),
+                                    ((20, 21, 22, 23, 24, 25), 8)])
+@pytest.mark.parametrize("nnz,sub", [(5000, None), (3000, 777), (1, None)])
+def test_core_throughput_uniform_ranks(dims, J, nnz, sub):
+    """Specialised K4 (uniform J = R, fp32, register-tiled outer products) vs
+    the fp64 oracle core_pass, with and without a visit subset."""
+    from paper_2204_07104_b200 import _lib
+
+    L = _lib.load()
+    idx, vals, fs, bs = _model_and_data(dims, (J,) * len(dims), J, nnz, 5)
+    fac, foff = O.pack(fs)
+    cor, coff = O.pack(bs)
+    jr = np.array([a.shape[1] for a in fs])
+    visit = np.arange(nnz) if sub is None else np.random.default_rng(9).choice(nnz, sub, replace=False)
+    recs = _records(idx, vals, False)
+    _, pf = _lib.i64arr(foff)
+    _, pc = _lib.i64arr(coff)
+    _, pj = _lib.i64arr(jr)
+    dvis = _dev(visit, np.int32)
+    acc = torch.zeros(int(coff[-1]), dtype=torch.float64, device="cuda")
+    ws = torch.empty(int(L.sptk_core_ws_bytes(pj, len(jr), J, 0)), dtype=torch.uint8, device="cuda")
+    dfac, dcor = _dev(fac, np.float32), _dev(cor, np.float32)  # keep the buffers alive across the call
+    _lib.check(L.sptk_core_pass(recs.rec.data_ptr(), recs.rw, dvis.data_ptr(), None, len(visit), dfac.data_ptr(),
+                                pf, dcor.data_ptr(), pc, pj, len(jr), J, acc.data_ptr(), 0, ws.data_ptr(),
+                                ws.numel(), _lib.stream_ptr()), "core")
+    want = np.zeros(int(coff[-1]))
+    O.core_pass(idx, vals, visit.astype(np.int64), fac, foff, cor, coff, jr, J, want, coff)
+    np.testing.assert_allclose(acc.cpu().numpy(), want, rtol=1e-4, atol=1e-5 * np.abs(want).max())

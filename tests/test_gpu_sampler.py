@@ -114,3 +114,44 @@ def test_choice_netflix_core_batch(golden_meta):
         assert h32(got) == g["sha256_i32"]
         s, _ = choice(g["entropy"], g["pop"], g["k"], shuffle=False)
         assert h32(np.sort(s.cpu().numpy())) == g["sha256_sorted_i32"]
+
+
+@pytest.mark.parametrize("n,order", [(1, 3), (2, 3), (100, 3), (65536, 3), (1_000_003, 3), (70_001, 4),
+                                     (40_000, 6)])
+def test_permute_records_equals_visit_gather(n, order):
+    """sptk_permute_records: the block's records in the order of
+    default_rng(entropy).permutation(n) (trainer.py:300-303), bit for bit,
+    together with the permutation itself."""
+    import torch
+
+    from paper_2204_07104_b200.device import DeviceCoo
+    from paper_2204_07104_b200.sampler import permute_records
+
+    rng = np.random.default_rng(n)
+    idx = rng.integers(0, 1 << 20, (n, order))
+    vals = rng.normal(size=n)
+    recs = DeviceCoo(idx, vals)
+    out = torch.empty_like(recs.rec)
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    ent = [7, 1, 3, n]
+    permute_records(n, recs.rec, recs.rw, out, entropy=ent, perm_out=perm)
+    want = O.permutation(ent, n)
+    assert np.array_equal(perm.cpu().numpy(), want)
+    src = recs.rec.view(-1, recs.rw).cpu().numpy()
+    assert np.array_equal(out.view(-1, recs.rw).cpu().numpy(), src[want])
+
+
+def test_permute_records_netflix_size(golden_meta):
+    """The fused gather at the bench size: the permutation it applies is numpy's."""
+    import torch
+
+    from paper_2204_07104_b200.sampler import permute_records
+
+    g = golden_meta["big"]["perm_NF_t0"]
+    n = g["n"]
+    src = torch.arange(n, dtype=torch.int32, device="cuda").repeat_interleave(4)
+    out = torch.empty_like(src)
+    permute_records(n, src, 4, out, entropy=g["entropy"])
+    p = out.view(-1, 4)[:, 0].cpu().numpy()
+    assert p[:64].tolist() == g["head"] and p[-64:].tolist() == g["tail"]
+    assert h32(p) == g["sha256_i32"]
