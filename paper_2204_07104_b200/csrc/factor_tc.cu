@@ -465,15 +465,24 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   // A-tile slot of mode n: modes 0..N-2 have one slot each, the last mode
   // alternates between two (pb).
   auto a_off = [&](int n, int pb) { return C::OFF_A + (n < N - 1 ? n : N - 1 + pb) * 128 * J; };
+  // Row gather of one mode for this warp's 32 samples: CH = J/4 lanes share a
+  // row (one 16-byte chunk each), so one cp.async instruction covers 32/CH
+  // whole rows and L1 merges each row into a single L2 request.
+  constexpr int CH = J / 4, RPI = 32 / CH;
+  const int lane = tid & 31, wbase = tid & ~31, cq = lane % CH, crow = lane / CH;
   auto issue_mode = [&](const RecReg<N, RW>& rr, int n, int pb) {
-    const float* src = fac + p.foff[n] + (long long)rr.idx[n] * J;
     const uint32_t dst = sbase + 4 * a_off(n, pb);
     // no L2::cache_hint operand here: with it ptxas 12.9 pairs the global
     // descriptor with an odd uniform register (desc[UR1]) in this loop, which
     // traps as an illegal instruction (the rows are L2-resident anyway)
 #pragma unroll
-    for (int q = 0; q < J / 4; ++q)
-      tc::cp_async16_nohint(dst + 4 * canon<128>(tid, 4 * q), src + 4 * q, rr.valid ? 16u : 0u);
+    for (int k = 0; k < CH; ++k) {
+      const int sl = k * RPI + crow;
+      const int row = __shfl_sync(0xffffffffu, rr.idx[n], sl);
+      const int ok = __shfl_sync(0xffffffffu, rr.valid ? 1 : 0, sl);
+      const float* src = fac + p.foff[n] + (long long)row * J + 4 * cq;
+      tc::cp_async16_nohint(dst + 4 * canon<128>(wbase + sl, 4 * cq), src, ok ? 16u : 0u);
+    }
   };
 
   // Software pipeline over this CTA's tiles: visit entries three tiles ahead,
@@ -568,8 +577,8 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       for (int q = 0; q < J / 16; ++q) tc::tmem_ld16(tlane + 16 * q, &g[16 * q]);
 #pragma unroll
       for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + J + 16 * q, &h[16 * q]);
-      const float* at = sm + a_off(n, pb);
-      float a[J];
+      float* at = sm + a_off(n, pb);
+      float a[J], a0[J];
 #pragma unroll
       for (int q = 0; q < J / 4; ++q) {
         float4 v = *reinterpret_cast<const float4*>(at + canon<128>(tid, 4 * q));
@@ -578,6 +587,8 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
         a[4 * q + 2] = v.z;
         a[4 * q + 3] = v.w;
       }
+#pragma unroll
+      for (int j = 0; j < J; ++j) a0[j] = a[j];
       float inter = 0.f;
 #pragma unroll
       for (int j = 0; j < J; ++j) inter = fmaf(a[j], g[j], inter);
@@ -587,19 +598,30 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
         float gr = -cur.x * g[j] + lm * a[j] + inter * g[j];
         a[j] -= gm * gr;
       }
-      if (cur.valid) {
-        float* dst = fac + p.foff[n] + (long long)cur.idx[n] * J;
-        if (p.atomic_mask >> n & 1u) {
+      // Row write-back through the (now dead) A slot: each thread parks its
+      // new row (or, for red.add modes, its delta) in its own slot row, then
+      // CH lanes per row write 16-byte chunks so each row is one request.
+      const bool red = p.atomic_mask >> n & 1u;
 #pragma unroll
-          for (int q = 0; q < J / 4; ++q) {
-            float4 o = *reinterpret_cast<const float4*>(at + canon<128>(tid, 4 * q));
-            tc::red_add_v4(dst + 4 * q, make_float4(a[4 * q] - o.x, a[4 * q + 1] - o.y, a[4 * q + 2] - o.z,
-                                                    a[4 * q + 3] - o.w));
-          }
-        } else {
+      for (int q = 0; q < J / 4; ++q) {
+        float4 v = red ? make_float4(a[4 * q] - a0[4 * q], a[4 * q + 1] - a0[4 * q + 1], a[4 * q + 2] - a0[4 * q + 2],
+                                     a[4 * q + 3] - a0[4 * q + 3])
+                       : make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+        *reinterpret_cast<float4*>(at + canon<128>(tid, 4 * q)) = v;
+      }
+      __syncwarp();
 #pragma unroll
-          for (int q = 0; q < J / 4; ++q)
-            tc::st_v4_hint(dst + 4 * q, make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]), pol_keep);
+      for (int k = 0; k < CH; ++k) {
+        const int sl = k * RPI + crow;
+        const int row = __shfl_sync(0xffffffffu, cur.idx[n], sl);
+        const int ok = __shfl_sync(0xffffffffu, cur.valid ? 1 : 0, sl);
+        const float4 v = *reinterpret_cast<const float4*>(at + canon<128>(wbase + sl, 4 * cq));
+        float* dst = fac + p.foff[n] + (long long)row * J + 4 * cq;
+        if (ok) {
+          if (red)
+            tc::red_add_v4(dst, v);
+          else
+            tc::st_v4_hint(dst, v, pol_keep);
         }
       }
       const float keep = 1.f - gm * lm, step = gm * (cur.x - inter);
