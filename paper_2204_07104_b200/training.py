@@ -186,7 +186,7 @@ class EpochRunner:
     """
 
     def __init__(self, model: TuckerModel, train_set: SparseTensorCoo, config: TrainConfig,
-                 prefetch: bool = True):
+                 prefetch: bool = True, owner_rank: int | None = None):
         import torch
 
         _lib.require_cuda()
@@ -195,6 +195,9 @@ class EpochRunner:
         self.f64 = config.precision == "fp64"
         self.mode = resolve_mode(config.update_mode, train_set.nnz)
         self.m = int(config.workers)
+        # owner_rank = w: this process runs only the blocks (w, ...) of each
+        # round (one GPU of the DSGD data division, dist.py)
+        self.owner_rank = owner_rank
         self.order = model.order
         self.nnz = train_set.nnz
         self.dm = DeviceModel(model, f64=self.f64)
@@ -203,12 +206,16 @@ class EpochRunner:
         self.schedule = round_schedule(model.order, self.m)
         # host list of (block, offset, count) per round, empty blocks dropped
         self.rounds = []
+        self.nnz_local = 0
         for rnd in self.schedule.rounds:
             items = []
             for block in rnd:
+                if owner_rank is not None and block[0] != owner_rank:
+                    continue
                 off, cnt = self.part.block_range(block)
                 if cnt > 0:
                     items.append((block, off, cnt))
+                    self.nnz_local += cnt
             self.rounds.append(items)
         dev = self.dm.fac.device
         # Visit orders of every block of an epoch (double-buffered), laid out
@@ -319,7 +326,7 @@ class EpochRunner:
         fn = L.sptk_factor_pass_f64 if self.f64 else L.sptk_factor_pass
         s = stream_ptr()
         processed = 0
-        for items in self.rounds:
+        for r, items in enumerate(self.rounds):
             for block, off, cnt in items:
                 if self.factor_events is not None:
                     e0 = self.torch.cuda.Event(enable_timing=True)
@@ -336,19 +343,37 @@ class EpochRunner:
                     e1.record()
                     self.factor_events.append((e0, e1))
                 processed += cnt
+            self.after_round(r)
+        self.after_factor_phase()
         return processed
+
+    # -- hooks for the multi-GPU data division (dist.DistRunner) ------------
+    def after_round(self, r: int) -> None:
+        """Called after round r's blocks are enqueued (A-block rotation)."""
+
+    def after_factor_phase(self) -> None:
+        """Called after the last round (A-block allgather)."""
+
+    def core_slice(self, slot: int):
+        """(visit ids or None, count, exact chunk count) of this process's share of Psi."""
+        k = self.k
+        return (None if k == self.nnz else self.psi[slot][:k]), k, (self.m if self.mode == 1 else 0)
+
+    def reduce_core_acc(self) -> None:
+        """Sum the core-gradient accumulators over processes (allreduce)."""
 
     def core_phase(self, t: int, gamma_b: float, slot: int) -> None:
         cfg, L, dm = self.cfg, self.L, self.dm
         k = self.k
-        visit = None if k == self.nnz else self.psi[slot][:k]
+        visit, count, chunks = self.core_slice(slot)
         self.acc.zero_()
         s = stream_ptr()
         fn = L.sptk_core_pass_f64 if self.f64 else L.sptk_core_pass
-        chunks = self.m if self.mode == 1 else 0
-        check(fn(ptr(self.part.rec), self.part.rw, ptr(visit), ptr(self.map), k, ptr(dm.fac), dm.p_foff,
-                 ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, ptr(self.acc), chunks,
-                 ptr(self.core_ws), self.core_ws.numel(), s), "sptk_core_pass")
+        if count > 0:
+            check(fn(ptr(self.part.rec), self.part.rw, ptr(visit), ptr(self.map), count, ptr(dm.fac), dm.p_foff,
+                     ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, ptr(self.acc), chunks,
+                     ptr(self.core_ws), self.core_ws.numel(), s), "sptk_core_pass")
+        self.reduce_core_acc()
         denom = float(k) if cfg.core_average else 1.0
         ap = L.sptk_core_apply_f64 if self.f64 else L.sptk_core_apply
         check(ap(ptr(dm.cor), ptr(self.acc), dm.cor_size, float(gamma_b), float(cfg.lambda_b), denom, s),
@@ -357,7 +382,7 @@ class EpochRunner:
     def epoch(self, t: int, gamma_a: float, gamma_b: float) -> None:
         slot = self._ensure_samples(t)
         processed = self.factor_phase(t, gamma_a, slot)
-        if processed != self.nnz:
+        if processed != self.nnz_local:
             raise RuntimeError("partition did not cover every training entry")
         if self.cfg.update_core:
             self.core_phase(t, gamma_b, slot)
