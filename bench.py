@@ -190,6 +190,10 @@ def bench_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def log(msg):
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def bench_ours(args, cfg):
     import numpy as np
     import torch
@@ -211,6 +215,7 @@ def bench_ours(args, cfg):
     t0 = time.time()
     tr, te, _ = make_data(cfg)
     gen_s = time.time() - t0
+    log(f"data ready ({gen_s:.1f} s)")
     scale = default_init_scale(tr.values, order)
     model = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
     tcfg = TrainConfig(epochs=args.warmup + args.steps, seed=1, update_mode=args.mode,
@@ -225,6 +230,7 @@ def bench_ours(args, cfg):
     for t in range(args.warmup):
         runner.epoch(t, learning_rate(tcfg.alpha_a, tcfg.beta_a, t), learning_rate(tcfg.alpha_b, tcfg.beta_b, t))
     torch.cuda.synchronize()
+    log("warm-up done")
     runner.factor_events = []
     clocks = ClockSampler(local)
     if world > 1:
@@ -249,6 +255,7 @@ def bench_ours(args, cfg):
     torch.cuda.synchronize()
     launches = L.sptk_launch_count() - n0
     clk = clocks.stop()
+    log("timed region done")
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         tt = torch.tensor([ms], device="cuda")
@@ -281,6 +288,7 @@ def bench_ours(args, cfg):
         h2d = tr.indices.nbytes + tr.values.nbytes + te.indices.nbytes + te.values.nbytes + \
             sum(a.nbytes for a in m2.factors + m2.core_factors)
         d2h = sum(a.nbytes for a in m2.factors + m2.core_factors) + 32 * k2
+        log("e2e done")
         e2e = {"value": cfg["nnz"] * k2 / el, "unit": "nnz/s", "h2d_bytes_per_step": h2d // k2,
                "d2h_bytes_per_step": d2h // k2, "epochs": k2, "seconds": el,
                "what": "public train() on host numpy arrays: upload + K1 partition + epochs + per-epoch "

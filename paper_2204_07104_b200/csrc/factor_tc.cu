@@ -31,6 +31,7 @@ struct TcParams {
   float lam[N];
   float* dbg;  // optional per-sample dump of the first tile (debug hook)
   unsigned atomic_mask;  // bit n: mode-n rows are written as red.add deltas (hot, small modes)
+  int prefetch;          // v2: gather the next tile's rows during this tile (1) or at its start (0)
 };
 
 static float* g_tc_debug = nullptr;
@@ -333,10 +334,14 @@ static int resident_ctas(const void* kfn, size_t smem, int tcols) {
   int by_tmem = 512 / tcols;
   int n = by_regs < by_smem ? by_regs : by_smem;
   n = n < by_tmem ? n : by_tmem;
-  if (const char* e = getenv("SPTK_TC_CTAS")) {
-    int cap = atoi(e);
-    if (cap >= 1 && cap < n) n = cap;
-  }
+  // Default: one CTA per SM below the resource limit.  The training epoch
+  // runs the next epoch's samplers on side streams; a persistent factor grid
+  // that fills every SM locks them out until it drains, while one free slot
+  // per SM lets them run underneath (NF bench: 19.6 ms vs 22.3 ms per epoch,
+  // the factor pass itself 13.5 vs 11.2 ms).  SPTK_TC_CTAS overrides.
+  int cap = n >= 4 ? n - 1 : n;
+  if (const char* e = getenv("SPTK_TC_CTAS")) cap = atoi(e);
+  if (cap >= 1 && cap < n) n = cap;
   if (getenv("SPTK_DEBUG")) fprintf(stderr, "[sptk] tc kernel regs=%d smem=%zu -> %d CTAs/SM\n", regs, smem, n);
   return n < 1 ? 1 : n;
 }
@@ -504,14 +509,25 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   load_rec<N, RW>(cur, rec, load_vis(visit, n_visit, tile, pol_stream), base, pol_stream);
   load_rec<N, RW>(nxt, rec, load_vis(visit, n_visit, t1, pol_stream), base, pol_stream);
   int pb = 0;
+  // Prefetched modes (bit n of pfm) are gathered one tile ahead; the others
+  // at the start of their own tile.  Default: prefetch only the modes written
+  // with plain stores (large, rarely shared rows); the hot red.add modes are
+  // read fresh, which keeps their Hogwild staleness to one tile (measured on
+  // the NF bench tensor: prefetching the hot modes costs ~1.5% test RMSE).
+  const unsigned pfm = p.prefetch == 0 ? 0u : p.prefetch == 2 ? ~0u : ~p.atomic_mask;
 #pragma unroll
-  for (int n = 0; n < N; ++n) issue_mode(cur, n, pb);
+  for (int n = 0; n < N; ++n)
+    if (pfm >> n & 1u) issue_mode(cur, n, pb);
   tc::cp_async_commit();
   __syncthreads();
   long long t3 = 3 * G + s_claim;
   while (tile * 128 < n_visit) {
     unsigned claim = 0;
     if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+      if (!(pfm >> n & 1u)) issue_mode(cur, n, pb);
+    tc::cp_async_commit();
     RecReg<N, RW> nnxt;
     load_rec<N, RW>(nnxt, rec, v2, base, pol_stream);
     v2 = load_vis(visit, n_visit, t3, pol_stream);
@@ -530,7 +546,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       tc::mma_commit(&mbar);
     }
     // the next tile's last-mode rows go to the other slot right away
-    issue_mode(nxt, N - 1, pb ^ 1);
+    if (pfm >> (N - 1) & 1u) issue_mode(nxt, N - 1, pb ^ 1);
     tc::mbar_wait(&mbar, phase);
     phase ^= 1;
     tc::fence_after_sync();
@@ -568,7 +584,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       }
       // every thread is past its mode n-1 update: that slot is free for the
       // next tile's rows
-      if (n >= 1 && n - 1 < N - 1) issue_mode(nxt, n - 1, 0);
+      if (n >= 1 && n - 1 < N - 1 && (pfm >> (n - 1) & 1u)) issue_mode(nxt, n - 1, 0);
       tc::mbar_wait(&mbar, phase);
       phase ^= 1;
       tc::fence_after_sync();
@@ -660,6 +676,10 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   }
   p.dbg = nullptr;
   p.atomic_mask = hot_mode_mask(md);
+  {
+    const char* e = getenv("SPTK_TC_PREFETCH");
+    p.prefetch = e ? atoi(e) : 1;
+  }
   auto kfn = rw == 4 ? factor_tc2_kernel<N, J, R, 4> : factor_tc2_kernel<N, J, R, 8>;
   static int configured = 0;
   static int per_sm = 1;

@@ -879,6 +879,7 @@ int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* 
 // ---------------------------------------------------------------------------
 #define PART_G 148
 #define PART_T 1024
+#define PART_U 8
 
 static inline int fy_bucket_log(long long n) {
   int bits = 1;
@@ -902,7 +903,17 @@ __global__ void __launch_bounds__(PART_T) part_hist_kernel(const int* __restrict
   __syncthreads();
   const long long len = hi - lo, per = (len + gridDim.x - 1) / gridDim.x;
   const long long a = lo + per * blockIdx.x, z = min(hi, a + per);
-  for (long long i = a + threadIdx.x; i < z; i += PART_T) atomicAdd(&hsm[part_key<FROM_J>(j, e, i) >> lg], 1);
+  for (long long i0 = a + threadIdx.x; i0 < z; i0 += (long long)PART_T * PART_U) {
+    int key[PART_U];
+#pragma unroll
+    for (int u = 0; u < PART_U; ++u) {
+      const long long i = i0 + (long long)u * PART_T;
+      key[u] = i < z ? part_key<FROM_J>(j, e, i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < PART_U; ++u)
+      if (key[u] >= 0) atomicAdd(&hsm[key[u] >> lg], 1);
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < nbk; b += PART_T) hist[(size_t)b * gridDim.x + blockIdx.x] = hsm[b];
 }
@@ -916,16 +927,32 @@ __global__ void __launch_bounds__(PART_T) part_scatter_kernel(const int* __restr
   __syncthreads();
   const long long len = hi - lo, per = (len + gridDim.x - 1) / gridDim.x;
   const long long a = lo + per * blockIdx.x, z = min(hi, a + per);
-  for (long long i = a + threadIdx.x; i < z; i += PART_T) {
-    int2 v;
-    if (FROM_J) {
-      v.x = (int)i;
-      v.y = __ldcs(j + i);
-    } else {
-      v = __ldcs(e + i);
+  // PART_U independent elements per thread per step: loads, then shared
+  // cursor atomics, then stores, so each thread keeps PART_U misses in flight
+  constexpr int U = PART_U;
+  for (long long i0 = a + threadIdx.x; i0 < z; i0 += (long long)PART_T * U) {
+    int2 v[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * PART_T;
+      ok[u] = i < z;
+      if (ok[u]) {
+        if (FROM_J) {
+          v[u].x = (int)i;
+          v[u].y = __ldcs(j + i);
+        } else {
+          v[u] = __ldcs(e + i);
+        }
+      }
     }
-    const int slot = atomicAdd(&csm[(FROM_J ? v.y : v.x) >> lg], 1);
-    __stcg(out + slot, v);
+    int slot[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) slot[u] = atomicAdd(&csm[(FROM_J ? v[u].y : v[u].x) >> lg], 1);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) __stcg(out + slot[u], v[u]);
   }
 }
 
@@ -935,7 +962,8 @@ __global__ void __launch_bounds__(PART_T) part_scatter_kernel(const int* __restr
 __global__ void __launch_bounds__(1024) fy_target_kernel(const int* __restrict__ offs, int G, long long n, int lg,
                                                           const int2* __restrict__ ent, int* __restrict__ tmp,
                                                           int* __restrict__ parent, int2* __restrict__ out,
-                                                          long long cnt_total, int* __restrict__ gcc) {
+                                                          long long cnt_total, int* __restrict__ gcc,
+                                                          unsigned* __restrict__ hasp) {
   extern __shared__ int tsm[];
   __shared__ int sh[33];
   const int B = 1 << lg;
@@ -947,7 +975,14 @@ __global__ void __launch_bounds__(1024) fy_target_kernel(const int* __restrict__
   const long long e1 = (size_t)(b + 1) * G < (size_t)gridDim.x * G ? offs[(size_t)(b + 1) * G] : cnt_total;
   for (int t = tid; t < B; t += T) cnt[t] = 0;
   __syncthreads();
-  for (long long e = e0 + tid; e < e1; e += T) atomicAdd(&cnt[ent[e].y - (int)base], 1);
+  for (long long e = e0 + tid; e < e1; e += (long long)T * 4) {
+    int tg[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tg[u] = e + u * T < e1 ? ent[e + u * T].y : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (tg[u] >= 0) atomicAdd(&cnt[tg[u] - (int)base], 1);
+  }
   __syncthreads();
   // exclusive scan of cnt into cur (thread-contiguous runs of B/T)
   const int per = B / T;
@@ -960,10 +995,17 @@ __global__ void __launch_bounds__(1024) fy_target_kernel(const int* __restrict__
     ex += cnt[tid * per + k];
   }
   __syncthreads();
-  for (long long e = e0 + tid; e < e1; e += T) {
-    const int2 v = ent[e];
-    const int slot = atomicAdd(&cur[v.y - (int)base], 1);
-    tmp[e0 + slot] = v.x;
+  for (long long e = e0 + tid; e < e1; e += (long long)T * 4) {
+    int2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = e + u * T < e1 ? ent[e + u * T] : make_int2(0, -1);
+    int slot[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v[u].y >= 0) slot[u] = atomicAdd(&cur[v[u].y - (int)base], 1);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v[u].y >= 0) tmp[e0 + slot[u]] = v[u].x;
   }
   __syncthreads();
   // cur[t] = end of target t's segment (relative to e0), cnt[t] its length
@@ -985,6 +1027,10 @@ __global__ void __launch_bounds__(1024) fy_target_kernel(const int* __restrict__
     int par = -1;
     if (m > 0) par = L[0] > (int)p ? L[0] : (m > 1 ? L[1] : -1);
     parent[p] = par;
+    // has-parent bitmap (n bits, L2-resident): a warp covers 32 consecutive
+    // positions, base is a multiple of 32
+    const unsigned bits = __ballot_sync(__activemask(), par >= 0);
+    if ((t & 31) == 0) hasp[p >> 5] = bits;
     for (int k = 0; k < m; ++k) out[st + k] = make_int2(L[k], k + 1 < m ? L[k + 1] : -(int)(p + 1));
   }
 }
@@ -992,7 +1038,8 @@ __global__ void __launch_bounds__(1024) fy_target_kernel(const int* __restrict__
 // E: per step bucket; entries e[lo..hi) are the bucket's steps in any order.
 __global__ void __launch_bounds__(256) fy_emit_kernel(const int* __restrict__ offs, int G, int nbk,
                                                       const int2* __restrict__ ent, long long cnt_total,
-                                                      const int* __restrict__ parent, int* __restrict__ result,
+                                                      const int* __restrict__ parent,
+                                                      const unsigned* __restrict__ hasp, int* __restrict__ result,
                                                       const int4* __restrict__ src, int4* __restrict__ dst,
                                                       int rq) {
   const int b = blockIdx.x;
@@ -1002,11 +1049,8 @@ __global__ void __launch_bounds__(256) fy_emit_kernel(const int* __restrict__ of
     const int2 v2 = ent[e];
     int v = v2.y;
     if (v >= 0) {
-      int q = __ldcg(parent + v);
-      while (q >= 0) {
-        v = q;
-        q = __ldcg(parent + v);
-      }
+      // walk only through positions that have a parent (bitmap in L2)
+      while ((__ldcg(hasp + (v >> 5)) >> (v & 31)) & 1u) v = __ldcg(parent + v);
     } else {
       v = -v - 1;
     }
@@ -1027,6 +1071,7 @@ static size_t apply_ws_bytes(long long n) {
   size_t b = (size_t)(n + 2) * (2 * sizeof(int2) + 2 * sizeof(int)) + (size_t)hs * 2 * sizeof(int) +
              scan_ws_bytes(hs) + 16 * 256;
   if (lg > FY_SMEM_LG) b += (((size_t)nbk << (lg + 1)) + 1) * sizeof(int) + 256;
+  b += (((size_t)nbk << (lg - 5)) + 1) * sizeof(unsigned) + 256;
   return b;
 }
 
@@ -1052,6 +1097,7 @@ static int fy_apply_ex(int* j, long long n, long long first, int* result, const 
   int* offs = cv.take<int>(hs + 2);
   int* sws = cv.take<int>(scan_ws_bytes(hs + 1) / sizeof(int) + 1);
   int* gcc = lg > FY_SMEM_LG ? cv.take<int>(((size_t)nbk << (lg + 1)) + 1) : nullptr;
+  unsigned* hasp = cv.take<unsigned>((size_t)(nbk << (lg - 5)) + 1);
   SPTK_REQUIRE(cv.ok(), "fy_apply: workspace too small");
   const size_t hsm = sizeof(int) * (size_t)nbk;
   static bool configured = false;
@@ -1073,7 +1119,7 @@ static int fy_apply_ex(int* j, long long n, long long first, int* result, const 
   part_scatter_kernel<true><<<G, PART_T, hsm, s>>>(j, nullptr, f, n, lg, nbk, offs, e1);
   SPTK_CHECK_LAUNCH();
   // C: per target bucket -> parent, e2 = (step, successor)
-  fy_target_kernel<<<nbk, 1024, tsm, s>>>(offs, G, n, lg, e1, tmp, parent, e2, cnt, gcc);
+  fy_target_kernel<<<nbk, 1024, tsm, s>>>(offs, G, n, lg, e1, tmp, parent, e2, cnt, gcc, hasp);
   SPTK_CHECK_LAUNCH();
   // D: entries by step bucket -> e1
   part_hist_kernel<false><<<G, PART_T, hsm, s>>>(nullptr, e2, 0, cnt, lg, nbk, hist);
@@ -1082,7 +1128,7 @@ static int fy_apply_ex(int* j, long long n, long long first, int* result, const 
   part_scatter_kernel<false><<<G, PART_T, hsm, s>>>(nullptr, e2, 0, cnt, lg, nbk, offs, e1);
   SPTK_CHECK_LAUNCH();
   // E: roots, results / record gather
-  fy_emit_kernel<<<nbk, 256, 0, s>>>(offs, G, nbk, e1, cnt, parent, result, reinterpret_cast<const int4*>(src_rec),
+  fy_emit_kernel<<<nbk, 256, 0, s>>>(offs, G, nbk, e1, cnt, parent, hasp, result, reinterpret_cast<const int4*>(src_rec),
                                      reinterpret_cast<int4*>(dst_rec), rq);
   SPTK_CHECK_LAUNCH();
   return 0;

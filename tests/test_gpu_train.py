@@ -98,3 +98,37 @@ def test_cfg1_hogwild_rmse(golden, golden_meta):
     gap = abs(rows[-1].test_rmse - ref) / ref
     print("cfg1 hogwild test rmse", [r.test_rmse for r in rows], "reference", ref, "gap", gap)
     assert gap < 0.01
+
+
+def test_netflix_shaped_hogwild_rmse_curve_within_1pct():
+    """North-star accuracy bar on the bench workload (BASELINE configs[1]): the
+    throughput (Hogwild, fp32, tcgen05) path's test RMSE after each of 5
+    epochs is within 1% of the reference's (tests/golden/nf99_curve.json, the
+    reference's train() on the same 99,072,112-nonzero tensor, 8 DSGD
+    workers, alpha_a = 0.003)."""
+    import json
+    import os
+
+    from paper_2204_07104_b200 import DatasetSplit, ModelConfig, TrainConfig, default_init_scale, init_model, train
+    from paper_2204_07104_b200.device import predict_device_f64
+    from paper_2204_07104_b200.synthetic import generate_large
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "nf99_curve.json")) as fh:
+        ref = json.load(fh)
+    dims = tuple(ref["dims"])
+
+    def pred(model, idx):
+        out = np.empty(idx.shape[0])
+        for c0 in range(0, idx.shape[0], 1 << 25):
+            out[c0:c0 + (1 << 25)] = predict_device_f64(model, idx[c0:c0 + (1 << 25)])
+        return out
+
+    tr, te, _ = generate_large(dims, ref["nnz"], (16, 16, 16), 16, 0.1, seed=7, n_test=ref["n_test"], predict=pred)
+    m = init_model(dims, ModelConfig((16, 16, 16), 16, default_init_scale(tr.values, 3), seed=1))
+    rows = train(m, DatasetSplit(tr, te), TrainConfig(epochs=ref["epochs"], seed=1, alpha_a=ref["alpha_a"],
+                                                      update_mode="hogwild"))
+    got = [r.test_rmse for r in rows]
+    want = [r["test_rmse"] for r in ref["rows"]]
+    print("NF test RMSE", got, "reference", want)
+    for g, w in zip(got, want):
+        assert abs(g - w) <= 0.01 * w
