@@ -218,7 +218,8 @@ def bench_ours(args, cfg):
     log(f"data ready ({gen_s:.1f} s)")
     scale = default_init_scale(tr.values, order)
     model = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
-    tcfg = TrainConfig(epochs=args.warmup + args.steps, seed=1, update_mode=args.mode,
+    # +3: every timed epoch also draws the next epoch's samples (steady state)
+    tcfg = TrainConfig(epochs=args.warmup + args.steps + 3, seed=1, update_mode=args.mode,
                        workers=world if world > 1 else 1, alpha_a=cfg.get("alpha_a", 0.009))
     if world > 1:
         from paper_2204_07104_b200 import dist
@@ -270,6 +271,12 @@ def bench_ours(args, cfg):
     algo_bytes = bytes_per_nnz(order, cfg["J"]) * nnz_local / launches_per_epoch
     peak, peak_src = measured_peak_gbs()
     achieved = algo_bytes / (f_ms / 1000.0) / 1e9
+    if os.environ.get("BENCH_TIMELINE") == "1":
+        runner.timeline = []
+        for t in range(args.warmup + args.steps, args.warmup + args.steps + 2):
+            runner.epoch(t, learning_rate(tcfg.alpha_a, tcfg.beta_a, t), learning_rate(tcfg.alpha_b, tcfg.beta_b, t))
+        for row in runner.timeline:
+            log(f"timeline {json.dumps(row)}")
     # accuracy after the run
     test_rmse = None
     if te is not None and rank == 0:

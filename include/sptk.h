@@ -86,9 +86,16 @@ int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, voi
  * sptk_permutation_ws_bytes(n). */
 int sptk_permute_records(const uint64_t h_state[4], long long n, const int32_t* d_rec_src, int rw,
                          int32_t* d_rec_out, int32_t* d_perm_out, void* d_ws, size_t ws_bytes, void* stream);
-/* test hook: the Fisher-Yates index sequence j_i (i = 1..n-1) of permutation(n). */
+/* The two halves of sptk_permutation, for pipelining across epochs:
+ * sptk_permutation_j writes the Fisher-Yates index sequence j_i (i = 1..n-1)
+ * of permutation(n) (workspace sptk_permutation_j_ws_bytes(n)); sptk_fy_apply
+ * applies such a sequence to the identity (d_j[0] is overwritten with 0;
+ * workspace sptk_fy_apply_ws_bytes(n)), d_out[n] = the permutation. */
+size_t sptk_permutation_j_ws_bytes(long long n);
 int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,
                        void* stream);
+size_t sptk_fy_apply_ws_bytes(long long n);
+int sptk_fy_apply(int32_t* d_j, long long n, int32_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
 size_t sptk_choice_ws_bytes(long long pop, long long k);
 /* d_out[k] = Generator.choice(pop, k, replace=False).  shuffle=0 returns the
  * same set without the final _shuffle_int (the core phase only needs the

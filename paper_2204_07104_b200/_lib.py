@@ -36,6 +36,9 @@ SIGNATURES = {
     "sptk_permutation_ws_bytes": (ctypes.c_size_t, [_i64]),
     "sptk_permutation": (ctypes.c_int, [_u64p, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
     "sptk_permute_records": (ctypes.c_int, [_u64p, _i64, _vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "sptk_permutation_j_ws_bytes": (ctypes.c_size_t, [_i64]),
+    "sptk_fy_apply_ws_bytes": (ctypes.c_size_t, [_i64]),
+    "sptk_fy_apply": (ctypes.c_int, [_vp, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
     "sptk_permutation_j": (ctypes.c_int, [_u64p, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
     "sptk_choice_ws_bytes": (ctypes.c_size_t, [_i64, _i64]),
     "sptk_choice": (ctypes.c_int, [_u64p, _i64, _i64, ctypes.c_int, _vp, _vp, ctypes.c_size_t,

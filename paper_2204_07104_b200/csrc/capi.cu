@@ -155,6 +155,12 @@ int sptk_permute_records(const uint64_t h_state[4], long long n, const int32_t* 
   return permute_records(h_state, n, d_rec_src, rw, d_rec_out, d_perm_out, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+size_t sptk_permutation_j_ws_bytes(long long n) { return jgen_ws_bytes(n); }
+size_t sptk_fy_apply_ws_bytes(long long n) { return fy_ws_bytes(n); }
+int sptk_fy_apply(int32_t* d_j, long long n, int32_t* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+  return fy_apply_public(d_j, n, d_out, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
 int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,
                        void* stream) {
   return permutation_j(h_state, n, d_j, d_ws, ws_bytes, (cudaStream_t)stream);

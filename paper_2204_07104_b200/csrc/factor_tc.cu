@@ -395,37 +395,40 @@ struct RecReg {
 // visit-list entry of this thread's sample in `tile` (-1 past the end)
 __device__ __forceinline__ long long load_vis(const int* __restrict__ visit, long long n_visit, long long tile,
                                               uint64_t pol) {
-  const long long k = tile * 128 + threadIdx.x;
-  if (k >= n_visit) return -1;
+  // unconditional (clamped) load; validity is recomputed from the tile index
+  long long k = tile * 128 + threadIdx.x;
+  k = k < n_visit ? k : n_visit - 1;
   return visit ? (long long)tc::ld_stream_s32(visit + k, pol) : k;
+}
+__device__ __forceinline__ bool tile_valid(long long n_visit, long long tile) {
+  return tile * 128 + threadIdx.x < n_visit;
 }
 
 template <int N, int RW>
-__device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict__ rec, long long v, long long base,
-                                         uint64_t pol) {
-  o.valid = v >= 0;
-  o.x = 0.f;
-#pragma unroll
-  for (int n = 0; n < N; ++n) o.idx[n] = 0;
-  if (o.valid) {
-    const int* rp = rec + (base + v) * RW;
-    int wv[8];
-    int4 w0 = tc::ld_stream_v4(rp, pol);
-    wv[0] = w0.x;
-    wv[1] = w0.y;
-    wv[2] = w0.z;
-    wv[3] = w0.w;
-    if (RW >= 8) {
-      int4 w1 = tc::ld_stream_v4(rp + 4, pol);
-      wv[4] = w1.x;
-      wv[5] = w1.y;
-      wv[6] = w1.z;
-      wv[7] = w1.w;
-    }
-#pragma unroll
-    for (int n = 0; n < N; ++n) o.idx[n] = wv[n];
-    o.x = __int_as_float(wv[N]);
+__device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict__ rec, long long v, bool valid,
+                                         long long base, uint64_t pol) {
+  // Unconditional load (past-the-end samples read the block's first record
+  // and are masked by `valid` at use): a predicated load merged with a
+  // default value would make the compiler wait for it right here, exposing
+  // the record-gather latency instead of hiding it behind two tiles of work.
+  o.valid = valid;
+  const int* rp = rec + (base + v) * RW;
+  int wv[8];
+  int4 w0 = tc::ld_stream_v4(rp, pol);
+  wv[0] = w0.x;
+  wv[1] = w0.y;
+  wv[2] = w0.z;
+  wv[3] = w0.w;
+  if (RW >= 8) {
+    int4 w1 = tc::ld_stream_v4(rp + 4, pol);
+    wv[4] = w1.x;
+    wv[5] = w1.y;
+    wv[6] = w1.z;
+    wv[7] = w1.w;
   }
+#pragma unroll
+  for (int n = 0; n < N; ++n) o.idx[n] = wv[n];
+  o.x = __int_as_float(wv[N]);
 }
 
 template <int N, int J, int R, int RW>
@@ -433,6 +436,14 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     factor_tc2_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
                       float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p,
                       unsigned* __restrict__ tile_ctr) {
+  // debug hook: per-phase clock64 stamps of block 0 / thread 0 for 16 tiles
+  long long* stamps = reinterpret_cast<long long*>(p.dbg);
+  int ntile = 0;
+#define TC2_STAMP(k)                                                              \
+  do {                                                                            \
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0 && ntile < 16) stamps[ntile * 16 + (k)] = clock64(); \
+  } while (0)
+
   using C = Tc2Cfg<N, J, R>;
   extern __shared__ __align__(16) float sm[];
   uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
@@ -506,8 +517,8 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
   RecReg<N, RW> cur, nxt;
   long long v2 = load_vis(visit, n_visit, t2, pol_stream);
-  load_rec<N, RW>(cur, rec, load_vis(visit, n_visit, tile, pol_stream), base, pol_stream);
-  load_rec<N, RW>(nxt, rec, load_vis(visit, n_visit, t1, pol_stream), base, pol_stream);
+  load_rec<N, RW>(cur, rec, load_vis(visit, n_visit, tile, pol_stream), tile_valid(n_visit, tile), base, pol_stream);
+  load_rec<N, RW>(nxt, rec, load_vis(visit, n_visit, t1, pol_stream), tile_valid(n_visit, t1), base, pol_stream);
   int pb = 0;
   // Prefetched modes (bit n of pfm) are gathered one tile ahead; the others
   // at the start of their own tile.  Default: prefetch only the modes written
@@ -522,6 +533,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   __syncthreads();
   long long t3 = 3 * G + s_claim;
   while (tile * 128 < n_visit) {
+    TC2_STAMP(0);
     unsigned claim = 0;
     if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
 #pragma unroll
@@ -529,12 +541,14 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       if (!(pfm >> n & 1u)) issue_mode(cur, n, pb);
     tc::cp_async_commit();
     RecReg<N, RW> nnxt;
-    load_rec<N, RW>(nnxt, rec, v2, base, pol_stream);
+    load_rec<N, RW>(nnxt, rec, v2, tile_valid(n_visit, t2), base, pol_stream);
     v2 = load_vis(visit, n_visit, t3, pol_stream);
+    TC2_STAMP(1);
     tc::cp_async_wait_all();
     tc::fence_async_smem();
     tc::fence_before_sync();
     __syncthreads();
+    TC2_STAMP(2);
     if (tid == 0) {
       tc::fence_after_sync();
 #pragma unroll
@@ -547,9 +561,11 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     }
     // the next tile's last-mode rows go to the other slot right away
     if (pfm >> (N - 1) & 1u) issue_mode(nxt, N - 1, pb ^ 1);
+    TC2_STAMP(3);
     tc::mbar_wait(&mbar, phase);
     phase ^= 1;
     tc::fence_after_sync();
+    TC2_STAMP(4);
     float c[N][R];
 #pragma unroll
     for (int n = 0; n < N; ++n)
@@ -574,7 +590,9 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       }
       tc::fence_async_smem();
       tc::fence_before_sync();
+      TC2_STAMP(5 + 3 * n);
       __syncthreads();
+      TC2_STAMP(6 + 3 * n);
       if (tid == 0) {
         tc::fence_after_sync();
         const uint32_t a = sbase + 4 * C::OFF_W;
@@ -588,6 +606,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       tc::mbar_wait(&mbar, phase);
       phase ^= 1;
       tc::fence_after_sync();
+      TC2_STAMP(7 + 3 * n);
       float g[J], h[R];
 #pragma unroll
       for (int q = 0; q < J / 16; ++q) tc::tmem_ld16(tlane + 16 * q, &g[16 * q]);
@@ -652,9 +671,12 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     t2 = t3;
     pb ^= 1;
     if (tid == 0) s_claim = claim;
+    TC2_STAMP(15);
     __syncthreads();
     t3 = 3 * G + s_claim;
+    ++ntile;
   }
+#undef TC2_STAMP
   tc::cp_async_wait_all();
   tc::fence_before_sync();
   __syncthreads();
@@ -674,7 +696,7 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
     p.gam[n] = gam[n];
     p.lam[n] = lam[n];
   }
-  p.dbg = nullptr;
+  p.dbg = g_tc_debug;  // tc2: per-phase clock stamps (long long[16][16]) when set
   p.atomic_mask = hot_mode_mask(md);
   {
     const char* e = getenv("SPTK_TC_PREFETCH");

@@ -363,7 +363,7 @@ __device__ __forceinline__ bool lemire_ok(uint32_t v, uint32_t rng, uint32_t* re
 }
 
 #define LEM_BITS 16
-#define LEM_B 1024
+#define LEM_B 256
 __global__ void __launch_bounds__(LEM_B) lemire_resolve_kernel(const uint32_t* __restrict__ v, long long vcap,
                                                                long long T, long long base, int dir,
                                                                uint32_t* __restrict__ out,
@@ -476,6 +476,88 @@ __global__ void __launch_bounds__(LEM_B) lemire_resolve_kernel(const uint32_t* _
   if (tid == 0) *q_end_out = T + delta;
 }
 
+// Lemire draw walker: one CTA, warp 0 walks the draws, warps 1..7 stage the
+// pre-generated stream v[] into a shared-memory ring ahead of it.  Each walker
+// round tests 32 consecutive draws against 32 consecutive stream positions
+// (one Lemire test per lane); the first rejecting lane ends the round and its
+// draw retries at the next position, so a round costs one test per lane and
+// the walk makes ~T/32 + (#rejections) rounds -- the work of the sequential
+// loop itself, with no speculative tests.
+#define LW_RING_LOG 13
+#define LW_RING (1 << LW_RING_LOG)
+#define LW_BLK 256
+#define LW_NB (LW_RING / LW_BLK)
+__global__ void __launch_bounds__(256) lemire_walk_kernel(const uint32_t* __restrict__ v, long long vcap, long long T,
+                                                          long long base, int dir, uint32_t* __restrict__ out,
+                                                          long long* __restrict__ q_end_out, int* __restrict__ err) {
+  __shared__ uint32_t ring[LW_RING];
+  __shared__ long long ready[LW_NB];
+  __shared__ long long cons;
+  __shared__ int done;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int b = tid; b < LW_NB; b += blockDim.x) ready[b] = -1;
+  if (tid == 0) {
+    cons = 0;
+    done = 0;
+  }
+  __syncthreads();
+  volatile long long* vready = ready;
+  volatile long long* vcons = &cons;
+  volatile int* vdone = &done;
+  const long long nblk = (vcap + LW_BLK - 1) / LW_BLK;
+  if (warp > 0) {
+    // producers: warp w stages blocks w-1, w-1+7, ...
+    const int np = (blockDim.x >> 5) - 1;
+    for (long long b = warp - 1; b < nblk; b += np) {
+      // block b overwrites block b - LW_NB: wait until the walker is past it
+      while ((*vcons) < (b - LW_NB + 1) * LW_BLK && !(*vdone)) __nanosleep(200);
+      if (*vdone) break;
+      const long long p0 = b * LW_BLK;
+      uint32_t x[LW_BLK / 32];
+#pragma unroll
+      for (int k = 0; k < LW_BLK / 32; ++k) {
+        const long long pos = p0 + k * 32 + lane;
+        x[k] = pos < vcap ? __ldcs(v + pos) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < LW_BLK / 32; ++k) ring[((b % LW_NB) * LW_BLK) + k * 32 + lane] = x[k];
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) vready[b % LW_NB] = b;
+    }
+    return;
+  }
+  // walker (warp 0)
+  long long q = 0, t = 0;
+  int bad = 0;
+  while (t < T) {
+    if (q + 32 > vcap) {
+      bad = 1;
+      break;
+    }
+    const long long b0 = q / LW_BLK, b1 = (q + 31) / LW_BLK;
+    while (vready[b0 % LW_NB] != b0 || vready[b1 % LW_NB] != b1) __nanosleep(32);
+    __syncwarp();
+    const uint32_t x = ring[(q + lane) & (LW_RING - 1)];
+    const long long tt = t + lane;
+    const bool valid = tt < T;
+    uint32_t r = 0;
+    const bool ok = !valid || lemire_ok(x, (uint32_t)(base + (long long)dir * tt), &r);
+    const unsigned bal = __ballot_sync(FULLMASK, !ok);
+    int nacc = bal ? __ffs(bal) - 1 : 32;
+    if (nacc > T - t) nacc = (int)(T - t);  // lanes past the last draw consume nothing
+    if (lane < nacc && valid) out[tt] = r;
+    t += nacc;
+    q += nacc + (bal ? 1 : 0);
+    if (lane == 0) *vcons = q;
+  }
+  if (lane == 0) {
+    *vdone = 1;
+    if (bad) *err = 3;
+    *q_end_out = q;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // (3) apply a Fisher-Yates swap sequence
 // ---------------------------------------------------------------------------
@@ -550,7 +632,7 @@ __global__ void fy_result_kernel(const int* __restrict__ start, const int* __res
 // ---------------------------------------------------------------------------
 // exclusive scan of int32 (n+1 outputs: out[n] = total); 3-phase
 // ---------------------------------------------------------------------------
-#define SCAN_B 1024
+#define SCAN_B 256
 #define SCAN_ITEMS 8
 __device__ __forceinline__ int block_excl_scan(int x, int* sh, int* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -780,6 +862,21 @@ static const int PERM_E = 64;
 
 static size_t apply_ws_bytes(long long n);
 
+// workspace of the j-sequence generation alone (segment chunk summaries)
+size_t jgen_ws_bytes(long long n) {
+  size_t chunks = 0;
+  if (n >= 2) {
+    int kmax = 64 - __builtin_clzll((unsigned long long)(n - 1));
+    for (int k = kmax; k > K_SMALL; --k) {
+      SegPlan sp = plan_segment(n, k);
+      if ((size_t)sp.C > chunks) chunks = sp.C;
+    }
+  }
+  return 66 * sizeof(long long) + 66 * sizeof(int) + 2 * 256 + (chunks + 1) * (4 * sizeof(int) + PERM_E * sizeof(int2)) +
+         6 * 256;
+}
+size_t fy_ws_bytes(long long n) { return apply_ws_bytes(n) + 256; }
+
 size_t perm_ws_bytes(long long n) {
   // j-generation chunk buffers
   size_t chunks = 0;
@@ -877,89 +974,178 @@ int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* 
 // Random DRAM traffic is one parent read per chain hop (~1 per step on
 // average) plus, for the record gather, one record read per step.
 // ---------------------------------------------------------------------------
-#define PART_G 148
-#define PART_T 1024
-#define PART_U 8
 
 static inline int fy_bucket_log(long long n) {
   int bits = 1;
   while ((1LL << bits) < n) ++bits;
-  int lg = bits - 13;
-  return lg < 14 ? 14 : lg;
+  int lg = bits - 14;
+  return lg < 13 ? 13 : lg;
+}
+
+// ---- two-pass MSD partition with coalesced writes ---------------------------
+// Items (step, target) from j (FROM_J) or int2 entries e (key = e.x) are
+// grouped by fine bucket f = key >> lg (nbk <= 2^13 buckets).  A single pass
+// would scatter into nbk x CTAs write fronts whose partially written sectors
+// get evicted (ECC read-modify-write); instead:
+//   count:  per-CTA shared histograms of f, summed into fine_cnt (global)
+//   pass 1: tiles of MSD_TILE items are counting-sorted in shared memory by
+//           the coarse bucket f >> 6 and written as contiguous runs at space
+//           reserved with one atomicAdd per (tile, coarse bucket)
+//   pass 2: tiles inside each coarse segment are sorted by f & 63 the same
+//           way and written to their final fine-bucket ranges.
+// Each pass streams 8 bytes in and out per item with run-length ~TILE/64.
+#define MSD_T 256
+#define FY_TT 256
+#define MSD_TILE 2048
+#define MSD_CB 7
+
+template <bool FROM_J>
+__device__ __forceinline__ int2 msd_item(const int* __restrict__ j, const int2* __restrict__ e, long long lo,
+                                         long long i) {
+  if (FROM_J) return make_int2((int)(lo + i), __ldcs(j + lo + i));
+  return __ldcs(e + i);
+}
+template <bool FROM_J>
+__device__ __forceinline__ int msd_key(int2 v) {
+  return FROM_J ? v.y : v.x;
 }
 
 template <bool FROM_J>
-__device__ __forceinline__ int part_key(const int* __restrict__ j, const int2* __restrict__ e, long long i) {
-  return FROM_J ? __ldcs(j + i) : __ldcs(e + i).x;
-}
-
-// in: FROM_J: j[f..n) (key = target, payload (i, j[i])); else e[0..cnt) (key = e.x)
-template <bool FROM_J>
-__global__ void __launch_bounds__(PART_T) part_hist_kernel(const int* __restrict__ j, const int2* __restrict__ e,
-                                                           long long lo, long long hi, int lg, int nbk,
-                                                           int* __restrict__ hist) {
+__global__ void __launch_bounds__(MSD_T) msd_count_kernel(const int* __restrict__ j, const int2* __restrict__ e,
+                                                          long long lo, long long n, int lg, int nbk,
+                                                          int* __restrict__ fine_cnt) {
   extern __shared__ int hsm[];
-  for (int b = threadIdx.x; b < nbk; b += PART_T) hsm[b] = 0;
+  for (int b = threadIdx.x; b < nbk; b += MSD_T) hsm[b] = 0;
   __syncthreads();
-  const long long len = hi - lo, per = (len + gridDim.x - 1) / gridDim.x;
-  const long long a = lo + per * blockIdx.x, z = min(hi, a + per);
-  for (long long i0 = a + threadIdx.x; i0 < z; i0 += (long long)PART_T * PART_U) {
-    int key[PART_U];
+  const long long per = (n + gridDim.x - 1) / gridDim.x;
+  const long long a = per * blockIdx.x, z = min(n, a + per);
+  for (long long i0 = a + threadIdx.x; i0 < z; i0 += (long long)MSD_T * 8) {
+    int key[8];
 #pragma unroll
-    for (int u = 0; u < PART_U; ++u) {
-      const long long i = i0 + (long long)u * PART_T;
-      key[u] = i < z ? part_key<FROM_J>(j, e, i) : -1;
+    for (int u = 0; u < 8; ++u) {
+      const long long i = i0 + (long long)u * MSD_T;
+      key[u] = i < z ? msd_key<FROM_J>(msd_item<FROM_J>(j, e, lo, i)) : -1;
     }
 #pragma unroll
-    for (int u = 0; u < PART_U; ++u)
+    for (int u = 0; u < 8; ++u)
       if (key[u] >= 0) atomicAdd(&hsm[key[u] >> lg], 1);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < nbk; b += PART_T) hist[(size_t)b * gridDim.x + blockIdx.x] = hsm[b];
+  for (int b = threadIdx.x; b < nbk; b += MSD_T)
+    if (hsm[b]) atomicAdd(&fine_cnt[b], hsm[b]);
+}
+
+// coarse cursors and per-coarse-segment tile prefix (one thread; ncb <= 128)
+__global__ void msd_setup_kernel(const int* __restrict__ boff, int nbk, int* __restrict__ ccur,
+                                 int* __restrict__ tile_start) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int ncb = (nbk + (1 << MSD_CB) - 1) >> MSD_CB;
+  int acc = 0;
+  for (int c = 0; c < ncb; ++c) {
+    const int a = boff[c << MSD_CB], z = boff[min(nbk, (c + 1) << MSD_CB)];
+    ccur[c] = a;
+    tile_start[c] = acc;
+    acc += (z - a + MSD_TILE - 1) / MSD_TILE;
+  }
+  tile_start[ncb] = acc;
+}
+
+// Sort one tile (items v[0..cnt) held MSD_TILE/MSD_T per thread) by bucket
+// b(item) in [0, nb) and write runs to out at cursor-reserved positions.
+template <int NBMAX, typename BucketFn>
+__device__ __forceinline__ void msd_tile_scatter(int2 (&v)[MSD_TILE / MSD_T], const bool (&ok)[MSD_TILE / MSD_T],
+                                                 int nb, BucketFn bucket, int* __restrict__ cursor,
+                                                 int2* __restrict__ out, int2* sbuf, int* cnt, int* toff,
+                                                 int* gbase, int* sh) {
+  constexpr int U = MSD_TILE / MSD_T;
+  const int tid = threadIdx.x;
+  for (int b = tid; b < nb; b += MSD_T) cnt[b] = 0;
+  __syncthreads();
+  int rank[U], bk[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    bk[u] = ok[u] ? bucket(v[u]) : -1;
+    if (bk[u] >= 0) rank[u] = atomicAdd(&cnt[bk[u]], 1);
+  }
+  __syncthreads();
+  // exclusive scan of cnt[0..nb) (nb <= NBMAX <= MSD_T) and cursor reservation
+  const int x = tid < nb ? cnt[tid] : 0;
+  int tot;
+  const int ex = block_excl_scan(x, sh, &tot);
+  if (tid < nb) {
+    toff[tid] = ex;
+    gbase[tid] = x ? atomicAdd(&cursor[tid], x) : 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (bk[u] >= 0) sbuf[toff[bk[u]] + rank[u]] = v[u];
+  __syncthreads();
+  for (int i = tid; i < tot; i += MSD_T) {
+    const int2 w = sbuf[i];
+    const int b = bucket(w);
+    out[gbase[b] + (i - toff[b])] = w;
+  }
+  __syncthreads();
 }
 
 template <bool FROM_J>
-__global__ void __launch_bounds__(PART_T) part_scatter_kernel(const int* __restrict__ j, const int2* __restrict__ e,
-                                                              long long lo, long long hi, int lg, int nbk,
-                                                              const int* __restrict__ offs, int2* __restrict__ out) {
-  extern __shared__ int csm[];
-  for (int b = threadIdx.x; b < nbk; b += PART_T) csm[b] = offs[(size_t)b * gridDim.x + blockIdx.x];
-  __syncthreads();
-  const long long len = hi - lo, per = (len + gridDim.x - 1) / gridDim.x;
-  const long long a = lo + per * blockIdx.x, z = min(hi, a + per);
-  // PART_U independent elements per thread per step: loads, then shared
-  // cursor atomics, then stores, so each thread keeps PART_U misses in flight
-  constexpr int U = PART_U;
-  for (long long i0 = a + threadIdx.x; i0 < z; i0 += (long long)PART_T * U) {
+__global__ void __launch_bounds__(MSD_T) msd_pass1_kernel(const int* __restrict__ j, const int2* __restrict__ e,
+                                                          long long lo, long long n, int lg, int nbk,
+                                                          int* __restrict__ ccur, int2* __restrict__ out) {
+  __shared__ int2 sbuf[MSD_TILE];
+  __shared__ int cnt[256], toff[256], gbase[256], sh[33];
+  constexpr int U = MSD_TILE / MSD_T;
+  const int ncb = (nbk + (1 << MSD_CB) - 1) >> MSD_CB;
+  const int sh_b = lg + MSD_CB;
+  const long long ntiles = (n + MSD_TILE - 1) / MSD_TILE;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int2 v[U];
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const long long i = i0 + (long long)u * PART_T;
-      ok[u] = i < z;
-      if (ok[u]) {
-        if (FROM_J) {
-          v[u].x = (int)i;
-          v[u].y = __ldcs(j + i);
-        } else {
-          v[u] = __ldcs(e + i);
-        }
-      }
+      const long long i = t * MSD_TILE + u * MSD_T + threadIdx.x;
+      ok[u] = i < n;
+      v[u] = ok[u] ? msd_item<FROM_J>(j, e, lo, i) : make_int2(0, 0);
     }
-    int slot[U];
+    msd_tile_scatter<128>(v, ok, ncb, [&](int2 w) { return msd_key<FROM_J>(w) >> sh_b; }, ccur, out, sbuf, cnt,
+                          toff, gbase, sh);
+  }
+}
+
+template <bool FROM_J>
+__global__ void __launch_bounds__(MSD_T) msd_pass2_kernel(const int2* __restrict__ in, const int* __restrict__ boff,
+                                                          int lg, int nbk, const int* __restrict__ tile_start,
+                                                          int* __restrict__ fcur, int2* __restrict__ out) {
+  __shared__ int2 sbuf[MSD_TILE];
+  __shared__ int cnt[1 << MSD_CB], toff[1 << MSD_CB], gbase[1 << MSD_CB], sh[33], ts[129];
+  constexpr int U = MSD_TILE / MSD_T;
+  const int ncb = (nbk + (1 << MSD_CB) - 1) >> MSD_CB;
+  for (int c = threadIdx.x; c <= ncb; c += MSD_T) ts[c] = tile_start[c];
+  __syncthreads();
+  const int ntiles = ts[ncb];
+  for (int g = blockIdx.x; g < ntiles; g += gridDim.x) {
+    int c = 0;
+    while (ts[c + 1] <= g) ++c;
+    const int f0 = c << MSD_CB, f1 = min(nbk, (c + 1) << MSD_CB);
+    const long long a = boff[f0] + (long long)(g - ts[c]) * MSD_TILE, z = boff[f1];
+    int2 v[U];
+    bool ok[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (ok[u]) slot[u] = atomicAdd(&csm[(FROM_J ? v[u].y : v[u].x) >> lg], 1);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (ok[u]) __stcg(out + slot[u], v[u]);
+    for (int u = 0; u < U; ++u) {
+      const long long i = a + u * MSD_T + threadIdx.x;
+      ok[u] = i < z;
+      v[u] = ok[u] ? __ldcs(in + i) : make_int2(0, 0);
+    }
+    msd_tile_scatter<(1 << MSD_CB)>(v, ok, f1 - f0, [&](int2 w) { return (msd_key<FROM_J>(w) >> lg) - f0; },
+                                    fcur + f0, out, sbuf, cnt, toff, gbase, sh);
   }
 }
 
 // C: per target bucket.  Dynamic smem: cnt[B] + cur[B] ints.
 // (cnt/cur live in shared memory for buckets of <= 2^14 positions, else in
 // the per-bucket slice of gcc[2 * 2^lg * nbk].)
-__global__ void __launch_bounds__(1024) fy_target_kernel(const int* __restrict__ offs, int G, long long n, int lg,
+__global__ void __launch_bounds__(FY_TT) fy_target_kernel(const int* __restrict__ offs, int G, long long n, int lg,
                                                           const int2* __restrict__ ent, int* __restrict__ tmp,
                                                           int* __restrict__ parent, int2* __restrict__ out,
                                                           long long cnt_total, int* __restrict__ gcc,
@@ -1063,13 +1249,12 @@ __global__ void __launch_bounds__(256) fy_emit_kernel(const int* __restrict__ of
   }
 }
 
-#define FY_SMEM_LG 14
+#define FY_SMEM_LG 13
 static size_t apply_ws_bytes(long long n) {
   const int lg = fy_bucket_log(n > 1 ? n : 2);
   const long long nbk = (n + (1LL << lg) - 1) >> lg;
-  const long long hs = nbk * PART_G + 2;
-  size_t b = (size_t)(n + 2) * (2 * sizeof(int2) + 2 * sizeof(int)) + (size_t)hs * 2 * sizeof(int) +
-             scan_ws_bytes(hs) + 16 * 256;
+  size_t b = (size_t)(n + 2) * (3 * sizeof(int2) + 2 * sizeof(int)) + (size_t)(nbk + 2) * 3 * sizeof(int) +
+             (size_t)(130 * 2) * sizeof(int) + scan_ws_bytes(nbk + 1) + 24 * 256;
   if (lg > FY_SMEM_LG) b += (((size_t)nbk << (lg + 1)) + 1) * sizeof(int) + 256;
   b += (((size_t)nbk << (lg - 5)) + 1) * sizeof(unsigned) + 256;
   return b;
@@ -1087,49 +1272,66 @@ static int fy_apply_ex(int* j, long long n, long long first, int* result, const 
   const long long cnt = n - f;
   const int lg = fy_bucket_log(n > 1 ? n : 2);
   const int nbk = (int)((n + (1LL << lg) - 1) >> lg);
-  const int G = PART_G;
-  const long long hs = (long long)nbk * G;
+  const int ncb = (nbk + (1 << MSD_CB) - 1) >> MSD_CB;
   int2* e1 = cv.take<int2>(cnt + 1);
   int2* e2 = cv.take<int2>(cnt + 1);
+  int2* e3 = cv.take<int2>(cnt + 1);  // pass-1 scratch of both partitions
   int* tmp = cv.take<int>(cnt + 1);
   int* parent = cv.take<int>(n + 1);
-  int* hist = cv.take<int>(hs + 2);
-  int* offs = cv.take<int>(hs + 2);
-  int* sws = cv.take<int>(scan_ws_bytes(hs + 1) / sizeof(int) + 1);
+  int* fcnt = cv.take<int>(nbk + 2);
+  int* boff = cv.take<int>(nbk + 2);
+  int* fcur = cv.take<int>(nbk + 2);
+  int* ccur = cv.take<int>(ncb + 2);
+  int* tstart = cv.take<int>(ncb + 2);
+  int* sws = cv.take<int>(scan_ws_bytes(nbk + 1) / sizeof(int) + 1);
   int* gcc = lg > FY_SMEM_LG ? cv.take<int>(((size_t)nbk << (lg + 1)) + 1) : nullptr;
   unsigned* hasp = cv.take<unsigned>((size_t)(nbk << (lg - 5)) + 1);
   SPTK_REQUIRE(cv.ok(), "fy_apply: workspace too small");
+  SPTK_REQUIRE(ncb <= 128 && (1 << MSD_CB) <= MSD_T, "fy_apply: n=%lld too large", n);
   const size_t hsm = sizeof(int) * (size_t)nbk;
   static bool configured = false;
   if (!configured) {
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(part_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(part_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(part_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
-    SPTK_CUDA_TRY(
-        cudaFuncSetAttribute(part_scatter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(msd_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(msd_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     SPTK_CUDA_TRY(cudaFuncSetAttribute(fy_target_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 << FY_SMEM_LG));
     configured = true;
   }
-  SPTK_REQUIRE(hsm <= (96u << 10), "fy_apply: n=%lld too large", n);
+  SPTK_REQUIRE(hsm <= (64u << 10), "fy_apply: n=%lld too large", n);
   const size_t tsm = gcc ? 0 : (size_t)8 << lg;
+  const unsigned G = 2 * 148;
+  auto partition = [&](bool from_j, const int2* src, int2* dst) -> int {
+    SPTK_CUDA_TRY(cudaMemsetAsync(fcnt, 0, sizeof(int) * (nbk + 1), s));
+    if (from_j)
+      msd_count_kernel<true><<<G, MSD_T, hsm, s>>>(j, nullptr, f, cnt, lg, nbk, fcnt);
+    else
+      msd_count_kernel<false><<<G, MSD_T, hsm, s>>>(nullptr, src, 0, cnt, lg, nbk, fcnt);
+    SPTK_CHECK_LAUNCH();
+    if (exclusive_scan(fcnt, nbk, boff, sws, s)) return 1;
+    SPTK_CUDA_TRY(cudaMemcpyAsync(fcur, boff, sizeof(int) * nbk, cudaMemcpyDeviceToDevice, s));
+    msd_setup_kernel<<<1, 32, 0, s>>>(boff, nbk, ccur, tstart);
+    SPTK_CHECK_LAUNCH();
+    if (from_j)
+      msd_pass1_kernel<true><<<G, MSD_T, 0, s>>>(j, nullptr, f, cnt, lg, nbk, ccur, e3);
+    else
+      msd_pass1_kernel<false><<<G, MSD_T, 0, s>>>(nullptr, src, 0, cnt, lg, nbk, ccur, e3);
+    SPTK_CHECK_LAUNCH();
+    if (from_j)
+      msd_pass2_kernel<true><<<G, MSD_T, 0, s>>>(e3, boff, lg, nbk, tstart, fcur, dst);
+    else
+      msd_pass2_kernel<false><<<G, MSD_T, 0, s>>>(e3, boff, lg, nbk, tstart, fcur, dst);
+    SPTK_CHECK_LAUNCH();
+    return 0;
+  };
   // B: steps by target bucket -> e1
-  part_hist_kernel<true><<<G, PART_T, hsm, s>>>(j, nullptr, f, n, lg, nbk, hist);
-  SPTK_CHECK_LAUNCH();
-  if (exclusive_scan(hist, hs, offs, sws, s)) return 1;
-  part_scatter_kernel<true><<<G, PART_T, hsm, s>>>(j, nullptr, f, n, lg, nbk, offs, e1);
-  SPTK_CHECK_LAUNCH();
+  if (partition(true, nullptr, e1)) return 1;
   // C: per target bucket -> parent, e2 = (step, successor)
-  fy_target_kernel<<<nbk, 1024, tsm, s>>>(offs, G, n, lg, e1, tmp, parent, e2, cnt, gcc, hasp);
+  fy_target_kernel<<<nbk, FY_TT, tsm, s>>>(boff, 1, n, lg, e1, tmp, parent, e2, cnt, gcc, hasp);
   SPTK_CHECK_LAUNCH();
   // D: entries by step bucket -> e1
-  part_hist_kernel<false><<<G, PART_T, hsm, s>>>(nullptr, e2, 0, cnt, lg, nbk, hist);
-  SPTK_CHECK_LAUNCH();
-  if (exclusive_scan(hist, hs, offs, sws, s)) return 1;
-  part_scatter_kernel<false><<<G, PART_T, hsm, s>>>(nullptr, e2, 0, cnt, lg, nbk, offs, e1);
-  SPTK_CHECK_LAUNCH();
+  if (partition(false, e2, e1)) return 1;
   // E: roots, results / record gather
-  fy_emit_kernel<<<nbk, 256, 0, s>>>(offs, G, nbk, e1, cnt, parent, hasp, result, reinterpret_cast<const int4*>(src_rec),
-                                     reinterpret_cast<int4*>(dst_rec), rq);
+  fy_emit_kernel<<<nbk, 256, 0, s>>>(boff, 1, nbk, e1, cnt, parent, hasp, result,
+                                     reinterpret_cast<const int4*>(src_rec), reinterpret_cast<int4*>(dst_rec), rq);
   SPTK_CHECK_LAUNCH();
   return 0;
 }
@@ -1182,13 +1384,28 @@ int permute_records(const uint64_t st[4], long long n, const int* rec_src, int r
 // j-sequence only (tests): j_out[i] for i in [1, n)
 int permutation_j(const uint64_t st[4], long long n, int* j_out, void* ws, size_t ws_bytes, cudaStream_t s) {
   SPTK_REQUIRE(n >= 0 && n < (1LL << 30), "permutation_j: n out of range");
-  SPTK_REQUIRE(ws_bytes >= perm_ws_bytes(n), "permutation_j: workspace too small");
+  SPTK_REQUIRE(ws_bytes >= jgen_ws_bytes(n), "permutation_j: workspace too small");
   if (n < 2) return 0;
   Carve cv{(char*)ws, ws_bytes};
   long long* d_P = cv.take<long long>(66);
   int* d_meta = cv.take<int>(66);
   Pcg64 g = make_pcg(st);
   return perm_jgen(g, n, j_out, cv, d_P, d_meta, s);
+}
+
+// result[i] (i in [0, n)) of applying the Fisher-Yates steps j[1..n-1] (j[0] is
+// overwritten with 0): the second half of permutation(), for pipelining the
+// j-sequence of one epoch with the apply of the previous one.
+int fy_apply_public(int* j, long long n, int* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+  SPTK_REQUIRE(n >= 0 && n < (1LL << 30), "fy_apply: n=%lld out of range [0, 2^30)", n);
+  SPTK_REQUIRE(ws_bytes >= fy_ws_bytes(n), "fy_apply: workspace too small (%zu < %zu)", ws_bytes, fy_ws_bytes(n));
+  if (n == 0) return 0;
+  if (n == 1) {
+    SPTK_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(int), s));
+    return 0;
+  }
+  Carve cv{(char*)ws, ws_bytes};
+  return fy_apply(j, n, 1, out, cv, s);
 }
 
 // --- choice ---------------------------------------------------------------
@@ -1235,7 +1452,7 @@ static int shuffle_int_jgen(Pcg64 g, long long q0, long long n, long long first,
   SPTK_REQUIRE(cv.ok(), "sampler workspace too small");
   u32_stream_kernel<<<grid_for(vcap, 256), 256, 0, s>>>(g, (unsigned long long)q0, vcap, v);
   SPTK_CHECK_LAUNCH();
-  lemire_resolve_kernel<<<1, LEM_B, 0, s>>>(v, vcap, T, n - 1, -1, tmp, d_qend, d_err);
+  lemire_walk_kernel<<<1, 256, 0, s>>>(v, vcap, T, n - 1, -1, tmp, d_qend, d_err);
   SPTK_CHECK_LAUNCH();
   reverse_into_kernel<<<grid_for(T, 256), 256, 0, s>>>(tmp, T, n, j);
   SPTK_CHECK_LAUNCH();
@@ -1281,7 +1498,7 @@ int choice(const uint64_t st[4], long long pop, long long k, int shuffle, int* o
   if (T > 0) {
     u32_stream_kernel<<<grid_for(vcap, 256), 256, 0, s>>>(g, 0ULL, vcap, v);
     SPTK_CHECK_LAUNCH();
-    lemire_resolve_kernel<<<1, LEM_B, 0, s>>>(v, vcap, T, base + t_begin, +1, vals + t_begin, d_q, d_err);
+    lemire_walk_kernel<<<1, 256, 0, s>>>(v, vcap, T, base + t_begin, +1, vals + t_begin, d_q, d_err);
     SPTK_CHECK_LAUNCH();
   } else {
     SPTK_CUDA_TRY(cudaMemsetAsync(d_q, 0, sizeof(long long), s));

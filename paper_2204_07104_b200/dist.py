@@ -230,7 +230,7 @@ class DistRunner(EpochRunner):
         if self.k == self.nnz:
             ids = self.torch.arange(lo, hi, dtype=self.torch.int32, device=self.dm.fac.device)
         else:
-            ids = self.psi[slot][lo:hi]
+            ids = self.psi[self.psi_slot][lo:hi]
         return ids, hi - lo, (1 if self.mode == 1 else 0)
 
     def reduce_core_acc(self):

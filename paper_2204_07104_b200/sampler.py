@@ -72,16 +72,32 @@ def permute_records(n: int, src, rw: int, out, ws: Workspace | None = None, stat
     return out
 
 
-def permutation_j(entropy, n: int):
-    """The Fisher-Yates index sequence j_i (i = 1..n-1) of permutation(n)."""
+def permutation_j(entropy, n: int, out=None, ws: Workspace | None = None, state=None, stream=None):
+    """The Fisher-Yates index sequence j_i (i = 1..n-1) of permutation(n)
+    (the first half of ``permutation``; ``fy_apply`` is the second)."""
     import torch
 
     _lib.require_cuda()
     L = _lib.load()
-    stc, sp = u64arr(pcg64_state(entropy))
-    out = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
-    w = Workspace().get(int(L.sptk_permutation_ws_bytes(n)))
-    check(L.sptk_permutation_j(sp, n, ptr(out), ptr(w), w.numel(), stream_ptr()), "sptk_permutation_j")
+    stc, sp = u64arr(state if state is not None else pcg64_state(entropy))
+    if out is None:
+        out = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+    w = (ws or Workspace()).get(int(L.sptk_permutation_j_ws_bytes(n)))
+    check(L.sptk_permutation_j(sp, n, ptr(out), ptr(w), w.numel(), stream_ptr(stream)), "sptk_permutation_j")
+    return out[:n]
+
+
+def fy_apply(j, n: int, out=None, ws: Workspace | None = None, stream=None):
+    """Apply the Fisher-Yates sequence j (from ``permutation_j``; j[0] is
+    overwritten) to the identity: the permutation itself."""
+    import torch
+
+    _lib.require_cuda()
+    L = _lib.load()
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    w = (ws or Workspace()).get(int(L.sptk_fy_apply_ws_bytes(n)))
+    check(L.sptk_fy_apply(ptr(j), n, ptr(out), ptr(w), w.numel(), stream_ptr(stream)), "sptk_fy_apply")
     return out[:n]
 
 

@@ -43,7 +43,7 @@ import numpy as np
 from . import _lib
 from ._lib import check, f64arr, ptr, stream_ptr
 from .device import DeviceCoo, DeviceModel, rmse_mae_device
-from .sampler import Workspace, choice, pcg64_state, permutation, permute_records
+from .sampler import Workspace, choice, fy_apply, pcg64_state, permutation_j
 from .schedule import DevicePartition, round_schedule
 from .tensor import DatasetSplit, SparseTensorCoo
 from .tucker import TuckerModel
@@ -218,35 +218,24 @@ class EpochRunner:
                     self.nnz_local += cnt
             self.rounds.append(items)
         dev = self.dm.fac.device
-        # Visit orders of every block of an epoch (double-buffered), laid out
-        # like the partitioned records.  With gather_records the sampler also
-        # applies them to the records (sptk_permute_records), so the factor
-        # pass streams visit-ordered records with no indirection; otherwise the
-        # factor pass gathers rec[visit[k]] itself.  Both cost one random
-        # record read per sample; which is cheaper depends on whether the
-        # factor kernel or the sampler has DRAM headroom (SPTK_GATHER=1).
-        import os
-
-        self.gather_records = os.environ.get("SPTK_GATHER", "0") == "1"
-        if self.gather_records:
-            self.prec = [torch.empty_like(self.part.rec) for _ in range(2)]
-        else:
-            self.perm = [torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
+        # Sampler state (K2), double-buffered by epoch parity: Fisher-Yates
+        # j-sequences (jbuf), visit orders (perm, laid out like the
+        # partitioned records) and core batches (psi).
+        self.jbuf = [torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.perm = [torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
         self.k = min(self.nnz, int(config.core_batch_cap))
-        self.psi = [torch.empty(max(self.k, 1), dtype=torch.int32, device=dev) for _ in range(2)]
-        # one preallocated sampler workspace per stream (never regrown while a
-        # kernel on the other stream may still be using it)
+        # core batches run two epochs ahead (the Floyd/Lemire draw is a serial
+        # single-CTA walk): three slots
+        self.psi = [torch.empty(max(self.k, 1), dtype=torch.int32, device=dev) for _ in range(3)]
+        # one preallocated workspace per sampler stage (never regrown while a
+        # kernel on another stream may still be using it)
         Lb = _lib.load()
         max_block = max((c for items in self.rounds for (_, _, c) in items), default=1)
-        need = int(Lb.sptk_permutation_ws_bytes(max_block))
+        self.ws_j, self.ws_fy, self.ws_psi = Workspace(dev), Workspace(dev), Workspace(dev)
+        self.ws_j.get(int(Lb.sptk_permutation_j_ws_bytes(max_block)))
+        self.ws_fy.get(int(Lb.sptk_fy_apply_ws_bytes(max_block)))
         if config.update_core and self.k < self.nnz:
-            need = max(need, int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
-        # [main, side (visit orders), side2 (core batch)]
-        self.ws = [Workspace(dev), Workspace(dev), Workspace(dev)]
-        for w in self.ws[:2]:
-            w.get(need)
-        if config.update_core and self.k < self.nnz:
-            self.ws[2].get(int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
+            self.ws_psi.get(int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
         self.acc = torch.zeros(max(self.dm.cor_size, 1), dtype=torch.float64, device=dev)
         L = _lib.load()
         chunks = self.m if self.mode == 1 else 0
@@ -259,65 +248,131 @@ class EpochRunner:
         self.map = self.part.pos_of_id if self.m > 1 else None
         self.L = L
         self.factor_events = None  # optional list: (start, end) CUDA events per factor launch
+        # Pipelined sampling: while the main stream trains epoch t,
+        #   side_j draws the j-sequences of epoch t+2,
+        #   side   applies those of epoch t+1 (visit orders),
+        #   side2  draws the core batch of epoch t+1.
+        # The j-generation is latency-bound (serial segment resolvers) and the
+        # apply is bandwidth-bound, so splitting them across epochs lets both
+        # run underneath the factor pass instead of back to back.
         self.prefetch = prefetch
-        self.side = torch.cuda.Stream(device=dev) if prefetch else None
-        self.side2 = torch.cuda.Stream(device=dev) if prefetch else None
-        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
-        self.ready2 = [torch.cuda.Event(), torch.cuda.Event()]
-        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        mk = (lambda: torch.cuda.Stream(device=dev)) if prefetch else (lambda: None)
+        self.side_j, self.side, self.side2 = mk(), mk(), mk()
+        ev2 = lambda: [torch.cuda.Event(), torch.cuda.Event()]  # noqa: E731
+        self.j_ready, self.j_free, self.perm_ready, self.done = ev2(), ev2(), ev2(), ev2()
+        self.psi_ready = [torch.cuda.Event() for _ in range(3)]
+        self.j_epoch = [None, None]
         self.sampled_epoch = [None, None]
+        self.psi_epoch = [None, None, None]
+        self.psi_slot = 0
+        self.timeline = None  # set to [] to record per-epoch stream timelines (synchronises)
+        self._marks = []
 
     # -- samplers (K2) -----------------------------------------------------
-    def draw_core_batch(self, t: int, slot: int, stream, ws) -> None:
-        """Core batch Psi of epoch t (trainer.py:316-324)."""
+    def draw_core_batch(self, t: int, stream) -> None:
+        """Core batch Psi of epoch t (trainer.py:212-220) into psi[t % 3]."""
         cfg = self.cfg
         if cfg.update_core and self.k < self.nnz:
-            choice(None, self.nnz, self.k, shuffle=(self.mode == 1), out=self.psi[slot], ws=ws,
+            choice(None, self.nnz, self.k, shuffle=(self.mode == 1), out=self.psi[t % 3], ws=self.ws_psi,
                    state=pcg64_state([cfg.seed, 2, t]), stream=stream)
+        self.psi_epoch[t % 3] = t
 
-    def draw_visit_orders(self, t: int, slot: int, stream, ws) -> None:
-        """Visit orders of every block of epoch t (trainer.py:294-303), applied
-        to the block's records: prec[slot] holds each block's records in the
-        exact order the reference visits them."""
+    def draw_jseq(self, t: int, slot: int, stream) -> None:
+        """Fisher-Yates j-sequences of every (own) block of epoch t:
+        default_rng([seed,1,t,*block]).permutation(len(ids)), first half
+        (trainer.py:196-199)."""
         cfg = self.cfg
-        rw = self.part.rw
         for items in self.rounds:
             for block, off, cnt in items:
-                st = pcg64_state([cfg.seed, 1, t, *block])
-                if self.gather_records:
-                    permute_records(cnt, self.part.rec[off * rw:(off + cnt) * rw], rw,
-                                    self.prec[slot][off * rw:(off + cnt) * rw], ws=ws, state=st, stream=stream)
-                else:
-                    permutation(None, cnt, out=self.perm[slot][off:off + cnt], ws=ws, state=st, stream=stream)
+                permutation_j(None, cnt, out=self.jbuf[slot][off:off + cnt], ws=self.ws_j,
+                              state=pcg64_state([cfg.seed, 1, t, *block]), stream=stream)
+        self.j_epoch[slot] = t
 
-    def draw_samples(self, t: int, slot: int, stream, ws) -> None:
-        """Visit orders of every block and the core batch of epoch t."""
-        self.draw_core_batch(t, slot, stream, self.ws[2])
-        self.draw_visit_orders(t, slot, stream, ws)
+    def apply_jseq(self, t: int, slot: int, stream) -> None:
+        """The visit orders of epoch t from its j-sequences (second half)."""
+        for items in self.rounds:
+            for block, off, cnt in items:
+                fy_apply(self.jbuf[slot][off:off + cnt], cnt, out=self.perm[slot][off:off + cnt], ws=self.ws_fy,
+                         stream=stream)
         self.sampled_epoch[slot] = t
+
+    def draw_samples(self, t: int, slot: int, stream) -> None:
+        """Visit orders of every block and the core batch of epoch t, in order on one stream."""
+        if self.psi_epoch[t % 3] != t:
+            self.draw_core_batch(t, stream)
+        self.draw_jseq(t, slot, stream)
+        self.apply_jseq(t, slot, stream)
 
     def _ensure_samples(self, t: int) -> int:
         torch = self.torch
-        slot = t % 2
+        slot, o = t % 2, 1 - t % 2
         main = torch.cuda.current_stream()
+        E = self.cfg.epochs
+        self.psi_slot = t % 3
         if self.sampled_epoch[slot] != t:
-            self.draw_samples(t, slot, main, self.ws[0])
+            if self.psi_epoch[t % 3] == t:
+                main.wait_event(self.psi_ready[t % 3])
+            self.draw_samples(t, slot, main)
+            self.j_free[slot].record(main)
+            if self.prefetch:  # the side stages reuse the same workspaces
+                ev = torch.cuda.Event()
+                ev.record(main)
+                for st in (self.side_j, self.side, self.side2):
+                    st.wait_event(ev)
         else:
-            main.wait_event(self.ready[slot])
-            main.wait_event(self.ready2[slot])
-        if self.prefetch and t + 1 < self.cfg.epochs and self.sampled_epoch[1 - slot] != t + 1:
-            # The other slot was last read by epoch t-1, which `done` marks.  The
-            # core batch (a latency-bound single-CTA resolver) goes first on its
-            # own stream so it runs beside this epoch's factor pass.
-            o = 1 - slot
-            self.side2.wait_event(self.done[o])
-            self.draw_core_batch(t + 1, o, self.side2, self.ws[2])
-            self.ready2[o].record(self.side2)
+            main.wait_event(self.perm_ready[slot])
+            main.wait_event(self.psi_ready[t % 3])
+        if not self.prefetch:
+            return slot
+        for e in (t + 1, t + 2):
+            if e < E and self.psi_epoch[e % 3] != e:
+                # psi[e % 3] was last read by epoch e - 3 (its `done` parity slot
+                # still holds that epoch's event)
+                self.side2.wait_event(self.done[(e - 3) % 2])
+                self._mark(f"psi{e - t}_start", self.side2)
+                self.draw_core_batch(e, self.side2)
+                self._mark(f"psi{e - t}_end", self.side2)
+                self.psi_ready[e % 3].record(self.side2)
+        if t + 1 < E and self.sampled_epoch[o] != t + 1:
+            if self.j_epoch[o] != t + 1:
+                self.side_j.wait_event(self.j_free[o])
+                self._mark("jseq_start", self.side_j)
+                self.draw_jseq(t + 1, o, self.side_j)
+                self._mark("jseq_end", self.side_j)
+                self.j_ready[o].record(self.side_j)
+            # perm[o] was last read by epoch t-1 (`done`)
             self.side.wait_event(self.done[o])
-            self.draw_visit_orders(t + 1, o, self.side, self.ws[1])
-            self.ready[o].record(self.side)
-            self.sampled_epoch[o] = t + 1
+            self.side.wait_event(self.j_ready[o])
+            self._mark("perm_start", self.side)
+            self.apply_jseq(t + 1, o, self.side)
+            self._mark("perm_end", self.side)
+            self.j_free[o].record(self.side)
+            self.perm_ready[o].record(self.side)
+        if t + 2 < E and self.j_epoch[slot] != t + 2:
+            # jbuf[slot] is free once epoch t's apply has read it
+            self.side_j.wait_event(self.j_free[slot])
+            self._mark("jseq2_start", self.side_j)
+            self.draw_jseq(t + 2, slot, self.side_j)
+            self._mark("jseq2_end", self.side_j)
+            self.j_ready[slot].record(self.side_j)
         return slot
+
+    # -- optional per-epoch stream timeline (timeline = [] to enable) --------
+    def _mark(self, name, stream=None):
+        if self.timeline is None:
+            return
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(stream if stream is not None else self.torch.cuda.current_stream())
+        self._marks.append((name, ev))
+
+    def _flush_timeline(self, t):
+        if self.timeline is None or not self._marks:
+            return
+        self._marks[-1][1].synchronize()
+        self.torch.cuda.synchronize()
+        t0 = self._marks[0][1]
+        self.timeline.append({"epoch": t, **{n: round(t0.elapsed_time(e), 3) for n, e in self._marks}})
+        self._marks = []
 
     # -- K3 / K4 / K5 ------------------------------------------------------
     def factor_phase(self, t: int, gamma_a: float, slot: int) -> int:
@@ -331,10 +386,7 @@ class EpochRunner:
                 if self.factor_events is not None:
                     e0 = self.torch.cuda.Event(enable_timing=True)
                     e0.record()
-                if self.gather_records:
-                    rec, visit = self.prec[slot], None
-                else:
-                    rec, visit = self.part.rec, self.perm[slot][off:off + cnt]
+                rec, visit = self.part.rec, self.perm[slot][off:off + cnt]
                 check(fn(ptr(rec), self.part.rw, ptr(visit), cnt, off, ptr(dm.fac), dm.p_foff, ptr(dm.cor),
                          dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam, self.mode, s),
                       "sptk_factor_pass")
@@ -357,7 +409,7 @@ class EpochRunner:
     def core_slice(self, slot: int):
         """(visit ids or None, count, exact chunk count) of this process's share of Psi."""
         k = self.k
-        return (None if k == self.nnz else self.psi[slot][:k]), k, (self.m if self.mode == 1 else 0)
+        return (None if k == self.nnz else self.psi[self.psi_slot][:k]), k, (self.m if self.mode == 1 else 0)
 
     def reduce_core_acc(self) -> None:
         """Sum the core-gradient accumulators over processes (allreduce)."""
@@ -380,13 +432,18 @@ class EpochRunner:
               "sptk_core_apply")
 
     def epoch(self, t: int, gamma_a: float, gamma_b: float) -> None:
+        self._mark("epoch_start")
         slot = self._ensure_samples(t)
+        self._mark("factor_start")
         processed = self.factor_phase(t, gamma_a, slot)
         if processed != self.nnz_local:
             raise RuntimeError("partition did not cover every training entry")
+        self._mark("factor_end")
         if self.cfg.update_core:
             self.core_phase(t, gamma_b, slot)
+        self._mark("epoch_end")
         self.done[slot].record(self.torch.cuda.current_stream())
+        self._flush_timeline(t)
 
 
 def train(model: TuckerModel, split: DatasetSplit, config: TrainConfig) -> list[MetricsRow]:
