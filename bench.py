@@ -56,6 +56,18 @@ def bytes_per_nnz(order, J):
     return 4 * (order + 1) + 8 * order * J
 
 
+def factor_traffic(workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum per factor-kernel launch from
+    the committed ncu --set full capture of this workload (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "factor_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d["bytes_per_launch"] if d.get("workload") == workload else None
+    except Exception:
+        return None
+
+
 def measured_peak_gbs():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -320,7 +332,9 @@ def bench_ours(args, cfg):
                              "model is L2-resident by design"},
             "test_rmse": test_rmse,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "factor_tps_kernel",
+                         "frac": achieved / peak, "traffic": factor_traffic(cfg["workload"]),
+                         "kernel": "factor_tc2_kernel" if cfg["J"] == cfg["R"] and cfg["J"] in (16, 32)
+                         else "factor_tps_kernel",
                          "kernel_ms": f_ms, "kernel_share": f_ms * launches_per_epoch / ms_per_step,
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
                          "frac_of_8TBs": achieved / 8000.0},
@@ -342,7 +356,7 @@ def main():
     ap.add_argument("--config", default="nf", choices=sorted(CONFIGS))
     ap.add_argument("--rank", type=int, default=None, help="J = R override (rank sweep)")
     ap.add_argument("--mode", default="hogwild", choices=["hogwild", "exact", "auto"])
-    ap.add_argument("--e2e-epochs", type=int, default=3)
+    ap.add_argument("--e2e-epochs", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

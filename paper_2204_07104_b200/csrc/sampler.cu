@@ -24,14 +24,17 @@
 //      out of range are walked exactly (slow path), so the result is exact
 //      for every input, not just with high probability.
 //  (2) Lemire draw sequences (Floyd values, _shuffle_int j's): rejections are
-//      rare (< 1%), so one CTA resolves 1024 draws per batch from 16
-//      speculative acceptance bits per draw and a ballot walk over the rare
-//      rejection events.
+//      rare (< 1%); one warp walks 32 draws per round against 32 stream
+//      positions staged in shared memory by the CTA's other warps, a round
+//      ending at the first rejection (one test per draw, no speculation).
+//      The training loop draws the core batch two epochs ahead, so this
+//      single-SM walk runs underneath the other work.
 //  (3) applying a Fisher-Yates swap sequence: with L_p the ascending list of
 //      steps targeting p, result[l_k] = val(l_{k+1}), result[l_last] = p,
 //      where val(s) (the value at position s just before step s) is the root
-//      of the forest parent(s) = first step > s targeting s.  Built with a
-//      counting sort by target, short per-bucket sorts and chain walks.
+//      of the forest parent(s) = first step > s targeting s.  Built with two
+//      bucket partitions (by target, then by step) around per-bucket counting
+//      sorts, and chain walks guarded by an L2-resident has-parent bitmap.
 #include <math.h>
 #include <stdio.h>
 
@@ -346,7 +349,7 @@ __global__ void perm_small_kernel(Pcg64 g, const long long* __restrict__ P, int 
 }
 
 // ---------------------------------------------------------------------------
-// (2) Lemire draw sequences (one CTA)
+// (2) Lemire draw sequences (one CTA, one walking warp)
 // ---------------------------------------------------------------------------
 // Draw t (t in [0,T)) asks for a value in [0, rng_t], rng_t = base + dir*t,
 // via buffered_bounded_lemire_uint32; stream values v[] start at position Q0
@@ -360,120 +363,6 @@ __device__ __forceinline__ bool lemire_ok(uint32_t v, uint32_t rng, uint32_t* re
   if (left >= rng_excl) return true;
   uint32_t thr = (0xffffffffu - rng) % rng_excl;
   return left >= thr;
-}
-
-#define LEM_BITS 16
-#define LEM_B 256
-__global__ void __launch_bounds__(LEM_B) lemire_resolve_kernel(const uint32_t* __restrict__ v, long long vcap,
-                                                               long long T, long long base, int dir,
-                                                               uint32_t* __restrict__ out,
-                                                               long long* __restrict__ q_end_out,
-                                                               int* __restrict__ err) {
-  __shared__ uint32_t masks[LEM_B];
-  __shared__ int eoff[LEM_B];  // resolved offset e* of each draw
-  __shared__ int s_stop, s_elast;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  long long delta = 0;  // rejections before draw t0
-  long long t0 = 0;
-  while (t0 < T) {
-    long long t = t0 + tid;
-    uint32_t rng = (uint32_t)(base + (long long)dir * t);
-    uint32_t mk = 0;
-    if (t < T) {
-      for (int e = 0; e < LEM_BITS; ++e) {
-        long long pos = t + delta + e;
-        uint32_t r;
-        bool ok = pos < vcap ? lemire_ok(v[pos], rng, &r) : false;
-        mk |= (ok ? 1u : 0u) << e;
-      }
-    } else {
-      mk = 0xffffu;
-    }
-    masks[tid] = mk;
-    __syncthreads();
-    if (tid < 32) {
-      // warp 0 walks the batch in 32-draw sub-batches
-      int e = 0;
-      int stop = LEM_B;
-      for (int sb = 0; sb < LEM_B / 32; ++sb) {
-        uint32_t m = masks[sb * 32 + lane];
-        int my_e = e;  // offset before this draw (updated below)
-        int start = 0;
-        while (true) {
-          bool zero = lane >= start && !((m >> e) & 1u);
-          unsigned z = __ballot_sync(FULLMASK, zero);
-          if (z == 0) {
-            if (lane >= start) my_e = e;
-            break;
-          }
-          int l1 = __ffs(z) - 1;
-          if (lane >= start && lane <= l1) my_e = e;
-          // draw l1 rejects until the next accepted bit
-          uint32_t m1 = __shfl_sync(FULLMASK, m, l1);
-          uint32_t rest = e + 1 < 32 ? (m1 >> (e + 1)) : 0u;
-          int ne = rest ? e + 1 + (__ffs(rest) - 1) : LEM_BITS;
-          if (ne >= LEM_BITS) {
-            stop = sb * 32 + l1;  // cannot resolve draw l1 within the window
-            break;
-          }
-          if (lane == l1) my_e = ne;  // l1 accepts at ne
-          e = ne;
-          start = l1 + 1;
-          if (start >= 32) break;
-        }
-        eoff[sb * 32 + lane] = my_e;
-        if (stop != LEM_B) break;
-      }
-      if (lane == 0) {
-        s_stop = stop;
-        s_elast = e;
-      }
-    }
-    __syncthreads();
-    const int stop = s_stop;
-    if (stop == 0) {
-      // the very first draw of the batch needs > LEM_BITS tries: walk it alone
-      if (tid == 0) {
-        long long pos = t0 + delta;
-        uint32_t rng0 = (uint32_t)(base + (long long)dir * t0);
-        uint32_t r;
-        while (pos < vcap && !lemire_ok(v[pos], rng0, &r)) ++pos;
-        if (pos >= vcap) {
-          *err = 1;
-        } else {
-          out[t0] = r;
-        }
-        s_elast = (int)(pos - (t0 + delta));
-      }
-      __syncthreads();
-      if (*err) return;
-      delta += s_elast;
-      t0 += 1;
-      __syncthreads();
-      continue;
-    }
-    if (tid < stop && t < T) {
-      long long pos = t + delta + eoff[tid];
-      uint32_t r = 0;
-      if (pos < vcap) lemire_ok(v[pos], rng, &r);
-      else *err = 2;
-      out[t] = r;
-    }
-    long long nres = stop;
-    if (t0 + nres > T) nres = T - t0;
-    // delta after the resolved prefix: e offset carried at the stop point
-    int ecarry;
-    if (stop == LEM_B) {
-      ecarry = s_elast;
-    } else {
-      ecarry = eoff[stop - 1];  // draw stop-1 accepted at its eoff; next starts there
-    }
-    __syncthreads();
-    delta += ecarry;
-    t0 += nres;
-  }
-  if (tid == 0) *q_end_out = T + delta;
 }
 
 // Lemire draw walker: one CTA, warp 0 walks the draws, warps 1..7 stage the
@@ -555,77 +444,6 @@ __global__ void __launch_bounds__(256) lemire_walk_kernel(const uint32_t* __rest
     *vdone = 1;
     if (bad) *err = 3;
     *q_end_out = q;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// (3) apply a Fisher-Yates swap sequence
-// ---------------------------------------------------------------------------
-__global__ void fy_hist_kernel(const int* __restrict__ j, long long first, long long n, int* __restrict__ cnt) {
-  long long i = first + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) atomicAdd(&cnt[j[i]], 1);
-}
-
-__global__ void fy_scatter_kernel(const int* __restrict__ j, long long first, long long n,
-                                  const int* __restrict__ start, int* __restrict__ fill,
-                                  int* __restrict__ list) {
-  long long i = first + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) {
-    int p = j[i];
-    int pos = start[p] + atomicAdd(&fill[p], 1);
-    list[pos] = (int)i;
-  }
-}
-
-// sort each bucket ascending; parent[p] = first step > p targeting p (or -1)
-__global__ void fy_bucket_kernel(const int* __restrict__ start, int* __restrict__ list, long long n,
-                                 int* __restrict__ parent) {
-  long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  for (; p < n; p += stride) {
-    int b = start[p], e = start[p + 1];
-    for (int x = b + 1; x < e; ++x) {
-      int key = list[x];
-      int y = x - 1;
-      while (y >= b && list[y] > key) {
-        list[y + 1] = list[y];
-        --y;
-      }
-      list[y + 1] = key;
-    }
-    int par = -1;
-    if (e > b) {
-      int l1 = list[b];
-      if (l1 > p) par = l1;
-      else if (e - b >= 2) par = list[b + 1];
-    }
-    parent[p] = par;
-  }
-}
-
-__global__ void fy_val_kernel(const int* __restrict__ parent, long long n, int* __restrict__ val) {
-  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  for (; s < n; s += stride) {
-    int v = (int)s;
-    int p = parent[v];
-    while (p >= 0) {
-      v = p;
-      p = parent[v];
-    }
-    val[s] = v;
-  }
-}
-
-__global__ void fy_result_kernel(const int* __restrict__ start, const int* __restrict__ list,
-                                 const int* __restrict__ val, long long n, int* __restrict__ result) {
-  long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  for (; p < n; p += stride) {
-    int b = start[p], e = start[p + 1];
-    for (int x = b; x < e; ++x) result[list[x]] = (x + 1 < e) ? val[list[x + 1]] : (int)p;
   }
 }
 
@@ -958,9 +776,8 @@ int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* 
 // (3) applying the swap sequence: two bucket partitions around a per-bucket
 // sort, so that every pass is either sequential or L2-local.
 //
-//   B  partition the steps by target bucket (2^lg positions per bucket):
-//      per-CTA shared-memory histograms -> scan -> scatter with shared-memory
-//      cursors (write fronts merge in L2), payload (step, target).
+//   B  partition the steps by target bucket (2^lg positions per bucket),
+//      payload (step, target): the two-pass MSD partition below.
 //   C  one CTA per target bucket: counting sort by target in an L2-resident
 //      scratch, insertion sort of each (short, O(log n)) step list, then
 //      parent[p] = first step > p targeting p, and each entry rewritten as
@@ -1143,7 +960,7 @@ __global__ void __launch_bounds__(MSD_T) msd_pass2_kernel(const int2* __restrict
 }
 
 // C: per target bucket.  Dynamic smem: cnt[B] + cur[B] ints.
-// (cnt/cur live in shared memory for buckets of <= 2^14 positions, else in
+// (cnt/cur live in shared memory for buckets of <= 2^13 positions, else in
 // the per-bucket slice of gcc[2 * 2^lg * nbk].)
 __global__ void __launch_bounds__(FY_TT) fy_target_kernel(const int* __restrict__ offs, int G, long long n, int lg,
                                                           const int2* __restrict__ ent, int* __restrict__ tmp,
@@ -1411,7 +1228,7 @@ int fy_apply_public(int* j, long long n, int* out, void* ws, size_t ws_bytes, cu
 // --- choice ---------------------------------------------------------------
 static long long lemire_vcap(long long T, double p_rej_max) {
   double mean = T * p_rej_max / (1.0 - p_rej_max);
-  return T + (long long)(mean + 12.0 * sqrt(mean + 1.0) + 64.0) + LEM_BITS + 64;
+  return T + (long long)(mean + 12.0 * sqrt(mean + 1.0) + 64.0) + 16 + 64;
 }
 
 size_t choice_ws_bytes(long long pop, long long k) {
