@@ -393,26 +393,33 @@ struct RecReg {
 };
 
 // visit-list entry of this thread's sample in `tile` (-1 past the end)
-__device__ __forceinline__ long long load_vis(const int* __restrict__ visit, long long n_visit, long long tile,
-                                              uint64_t pol) {
+// Returns the raw 32-bit entry: widening it here would make the compiler
+// consume the load immediately (a sign extension right after the LDG), which
+// exposed the full visit-gather latency at the start of every tile.
+// (HV: a visit list is given; without one the k-th sample is record k.  A
+// template flag, so no predicated select ever writes the loaded register.)
+template <bool HV>
+__device__ __forceinline__ int load_vis(const int* __restrict__ visit, long long n_visit, long long tile,
+                                        uint64_t pol) {
   // unconditional (clamped) load; validity is recomputed from the tile index
   long long k = tile * 128 + threadIdx.x;
   k = k < n_visit ? k : n_visit - 1;
-  return visit ? (long long)tc::ld_stream_s32(visit + k, pol) : k;
+  if (HV) return tc::ld_stream_s32(visit + k, pol);
+  return (int)k;
 }
 __device__ __forceinline__ bool tile_valid(long long n_visit, long long tile) {
   return tile * 128 + threadIdx.x < n_visit;
 }
 
 template <int N, int RW>
-__device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict__ rec, long long v, bool valid,
+__device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict__ rec, int v, bool valid,
                                          long long base, uint64_t pol) {
   // Unconditional load (past-the-end samples read the block's first record
   // and are masked by `valid` at use): a predicated load merged with a
   // default value would make the compiler wait for it right here, exposing
   // the record-gather latency instead of hiding it behind two tiles of work.
   o.valid = valid;
-  const int* rp = rec + (base + v) * RW;
+  const int* rp = rec + (base + (long long)v) * RW;
   int wv[8];
   int4 w0 = tc::ld_stream_v4(rp, pol);
   wv[0] = w0.x;
@@ -431,7 +438,7 @@ __device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict
   o.x = __int_as_float(wv[N]);
 }
 
-template <int N, int J, int R, int RW>
+template <int N, int J, int R, bool HV>
 __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 128 ? 3 : 2)))
     factor_tc2_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
                       float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p,
@@ -444,6 +451,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     if (stamps && blockIdx.x == 0 && threadIdx.x == 0 && ntile < 16) stamps[ntile * 16 + (k)] = clock64(); \
   } while (0)
 
+  constexpr int RW = N <= 3 ? 4 : (N <= 7 ? 8 : 16);
   using C = Tc2Cfg<N, J, R>;
   extern __shared__ __align__(16) float sm[];
   uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
@@ -516,9 +524,10 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
   if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
   RecReg<N, RW> cur, nxt;
-  long long v2 = load_vis(visit, n_visit, t2, pol_stream);
-  load_rec<N, RW>(cur, rec, load_vis(visit, n_visit, tile, pol_stream), tile_valid(n_visit, tile), base, pol_stream);
-  load_rec<N, RW>(nxt, rec, load_vis(visit, n_visit, t1, pol_stream), tile_valid(n_visit, t1), base, pol_stream);
+  int v2 = load_vis<HV>(visit, n_visit, t2, pol_stream);
+  load_rec<N, RW>(cur, rec, load_vis<HV>(visit, n_visit, tile, pol_stream), tile_valid(n_visit, tile), base,
+                  pol_stream);
+  load_rec<N, RW>(nxt, rec, load_vis<HV>(visit, n_visit, t1, pol_stream), tile_valid(n_visit, t1), base, pol_stream);
   int pb = 0;
   // Prefetched modes (bit n of pfm) are gathered one tile ahead; the others
   // at the start of their own tile.  Default: prefetch only the modes written
@@ -526,9 +535,14 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   // read fresh, which keeps their Hogwild staleness to one tile (measured on
   // the NF bench tensor: prefetching the hot modes costs ~1.5% test RMSE).
   const unsigned pfm = p.prefetch == 0 ? 0u : p.prefetch == 2 ? ~0u : ~p.atomic_mask;
+  // late-prefetched modes (prefetch == 3: the hot modes): gathered for the
+  // next tile once this tile reaches its last mode, i.e. a fraction of a
+  // tile early instead of a whole tile
+  const unsigned lpm = p.prefetch == 3 ? p.atomic_mask : 0u;
+  const unsigned fresh = ~(pfm | lpm);
 #pragma unroll
   for (int n = 0; n < N; ++n)
-    if (pfm >> n & 1u) issue_mode(cur, n, pb);
+    if ((pfm | lpm) >> n & 1u) issue_mode(cur, n, pb);
   tc::cp_async_commit();
   __syncthreads();
   long long t3 = 3 * G + s_claim;
@@ -538,11 +552,11 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
 #pragma unroll
     for (int n = 0; n < N; ++n)
-      if (!(pfm >> n & 1u)) issue_mode(cur, n, pb);
+      if (fresh >> n & 1u) issue_mode(cur, n, pb);
     tc::cp_async_commit();
     RecReg<N, RW> nnxt;
     load_rec<N, RW>(nnxt, rec, v2, tile_valid(n_visit, t2), base, pol_stream);
-    v2 = load_vis(visit, n_visit, t3, pol_stream);
+    v2 = load_vis<HV>(visit, n_visit, t3, pol_stream);
     TC2_STAMP(1);
     tc::cp_async_wait_all();
     tc::fence_async_smem();
@@ -603,6 +617,13 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       // every thread is past its mode n-1 update: that slot is free for the
       // next tile's rows
       if (n >= 1 && n - 1 < N - 1 && (pfm >> (n - 1) & 1u)) issue_mode(nxt, n - 1, 0);
+      if (n == N - 1 && lpm) {
+        // every thread is past modes 0..N-2 of this tile: their slots and the
+        // spare last-mode slot are free
+#pragma unroll
+        for (int m = 0; m < N; ++m)
+          if (lpm >> m & 1u) issue_mode(nxt, m, m == N - 1 ? (pb ^ 1) : 0);
+      }
       tc::mbar_wait(&mbar, phase);
       phase ^= 1;
       tc::fence_after_sync();
@@ -702,18 +723,15 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
     const char* e = getenv("SPTK_TC_PREFETCH");
     p.prefetch = e ? atoi(e) : 1;
   }
-  auto kfn = rw == 4 ? factor_tc2_kernel<N, J, R, 4> : factor_tc2_kernel<N, J, R, 8>;
+  (void)rw;  // == rec_words(N), checked by try_factor_tc
+  auto kfn = visit ? factor_tc2_kernel<N, J, R, true> : factor_tc2_kernel<N, J, R, false>;
   static int configured = 0;
   static int per_sm = 1;
   if (!configured) {
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc2_kernel<N, J, R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)C::SMEM));
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc2_kernel<N, J, R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)C::SMEM));
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc2_kernel<N, J, R, 4>,
-                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(factor_tc2_kernel<N, J, R, 8>,
-                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    for (auto f : {factor_tc2_kernel<N, J, R, true>, factor_tc2_kernel<N, J, R, false>}) {
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
     per_sm = resident_ctas((const void*)kfn, C::SMEM, C::TCOLS);
     configured = 1;
   }

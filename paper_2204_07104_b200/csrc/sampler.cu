@@ -795,8 +795,8 @@ int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* 
 static inline int fy_bucket_log(long long n) {
   int bits = 1;
   while ((1LL << bits) < n) ++bits;
-  int lg = bits - 14;
-  return lg < 13 ? 13 : lg;
+  int lg = bits - 15;
+  return lg < 12 ? 12 : lg;
 }
 
 // ---- two-pass MSD partition with coalesced writes ---------------------------
@@ -813,8 +813,9 @@ static inline int fy_bucket_log(long long n) {
 // Each pass streams 8 bytes in and out per item with run-length ~TILE/64.
 #define MSD_T 256
 #define FY_TT 256
+#define FY_LCAP 8192
 #define MSD_TILE 2048
-#define MSD_CB 7
+#define MSD_CB 8
 
 template <bool FROM_J>
 __device__ __forceinline__ int2 msd_item(const int* __restrict__ j, const int2* __restrict__ e, long long lo,
@@ -831,8 +832,12 @@ template <bool FROM_J>
 __global__ void __launch_bounds__(MSD_T) msd_count_kernel(const int* __restrict__ j, const int2* __restrict__ e,
                                                           long long lo, long long n, int lg, int nbk,
                                                           int* __restrict__ fine_cnt) {
-  extern __shared__ int hsm[];
-  for (int b = threadIdx.x; b < nbk; b += MSD_T) hsm[b] = 0;
+  // packed 16-bit counters (two per word; the grid is sized so no CTA sees
+  // more than 65535 items): half the shared memory, so the kernel fits beside
+  // the factor grid
+  extern __shared__ unsigned hsm2[];
+  const int nw = (nbk + 1) >> 1;
+  for (int b = threadIdx.x; b < nw; b += MSD_T) hsm2[b] = 0u;
   __syncthreads();
   const long long per = (n + gridDim.x - 1) / gridDim.x;
   const long long a = per * blockIdx.x, z = min(n, a + per);
@@ -845,11 +850,17 @@ __global__ void __launch_bounds__(MSD_T) msd_count_kernel(const int* __restrict_
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (key[u] >= 0) atomicAdd(&hsm[key[u] >> lg], 1);
+      if (key[u] >= 0) {
+        const int b = key[u] >> lg;
+        atomicAdd(&hsm2[b >> 1], (b & 1) ? 65536u : 1u);
+      }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < nbk; b += MSD_T)
-    if (hsm[b]) atomicAdd(&fine_cnt[b], hsm[b]);
+  for (int w = threadIdx.x; w < nw; w += MSD_T) {
+    const unsigned x = hsm2[w];
+    if (x & 0xffffu) atomicAdd(&fine_cnt[2 * w], (int)(x & 0xffffu));
+    if ((x >> 16) && 2 * w + 1 < nbk) atomicAdd(&fine_cnt[2 * w + 1], (int)(x >> 16));
+  }
 }
 
 // coarse cursors and per-coarse-segment tile prefix (one thread; ncb <= 128)
@@ -959,8 +970,41 @@ __global__ void __launch_bounds__(MSD_T) msd_pass2_kernel(const int2* __restrict
   }
 }
 
+// Per target p of a bucket: insertion-sort its step list L (short), emit
+// parent[p], the has-parent bit and (step, successor) entries.  Called with a
+// shared-memory or a global list buffer (separate instantiations, so the
+// shared case compiles to LDS/STS rather than generic loads).
+__device__ __forceinline__ void fy_target_lists(int* lists, const int* cnt, const int* cur, long long base,
+                                                long long n, int B, long long e0, int* __restrict__ parent,
+                                                int2* __restrict__ out, unsigned* __restrict__ hasp) {
+  for (int t = threadIdx.x; t < B; t += blockDim.x) {
+    const long long p = base + t;
+    if (p >= n) break;
+    const int m = cnt[t];
+    const int rel = cur[t] - m;
+    int* L = lists + rel;
+    for (int x = 1; x < m; ++x) {
+      const int v = L[x];
+      int c = x - 1;
+      while (c >= 0 && L[c] > v) {
+        L[c + 1] = L[c];
+        --c;
+      }
+      L[c + 1] = v;
+    }
+    int par = -1;
+    if (m > 0) par = L[0] > (int)p ? L[0] : (m > 1 ? L[1] : -1);
+    parent[p] = par;
+    // has-parent bitmap (n bits, L2-resident): a warp covers 32 consecutive
+    // positions, base is a multiple of 32
+    const unsigned bits = __ballot_sync(__activemask(), par >= 0);
+    if ((t & 31) == 0) hasp[p >> 5] = bits;
+    for (int k = 0; k < m; ++k) out[e0 + rel + k] = make_int2(L[k], k + 1 < m ? L[k + 1] : -(int)(p + 1));
+  }
+}
+
 // C: per target bucket.  Dynamic smem: cnt[B] + cur[B] ints.
-// (cnt/cur live in shared memory for buckets of <= 2^13 positions, else in
+// (cnt/cur live in shared memory for buckets of <= 2^12 positions, else in
 // the per-bucket slice of gcc[2 * 2^lg * nbk].)
 __global__ void __launch_bounds__(FY_TT) fy_target_kernel(const int* __restrict__ offs, int G, long long n, int lg,
                                                           const int2* __restrict__ ent, int* __restrict__ tmp,
@@ -976,6 +1020,9 @@ __global__ void __launch_bounds__(FY_TT) fy_target_kernel(const int* __restrict_
   const long long base = (long long)b << lg;
   const long long e0 = offs[(size_t)b * G];
   const long long e1 = (size_t)(b + 1) * G < (size_t)gridDim.x * G ? offs[(size_t)(b + 1) * G] : cnt_total;
+  // target-sorted step lists: in shared memory when the bucket fits (the
+  // common case), else in the bucket's slice of the global scratch
+  int* lists = (!gcc && e1 - e0 <= FY_LCAP) ? tsm + 2 * B : tmp + e0;
   for (int t = tid; t < B; t += T) cnt[t] = 0;
   __syncthreads();
   for (long long e = e0 + tid; e < e1; e += (long long)T * 4) {
@@ -1008,34 +1055,14 @@ __global__ void __launch_bounds__(FY_TT) fy_target_kernel(const int* __restrict_
       if (v[u].y >= 0) slot[u] = atomicAdd(&cur[v[u].y - (int)base], 1);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (v[u].y >= 0) tmp[e0 + slot[u]] = v[u].x;
+      if (v[u].y >= 0) lists[slot[u]] = v[u].x;
   }
   __syncthreads();
   // cur[t] = end of target t's segment (relative to e0), cnt[t] its length
-  for (int t = tid; t < B; t += T) {
-    const long long p = base + t;
-    if (p >= n) break;
-    const int m = cnt[t];
-    const long long st = e0 + cur[t] - m;
-    int* L = tmp + st;
-    for (int x = 1; x < m; ++x) {
-      const int v = L[x];
-      int c = x - 1;
-      while (c >= 0 && L[c] > v) {
-        L[c + 1] = L[c];
-        --c;
-      }
-      L[c + 1] = v;
-    }
-    int par = -1;
-    if (m > 0) par = L[0] > (int)p ? L[0] : (m > 1 ? L[1] : -1);
-    parent[p] = par;
-    // has-parent bitmap (n bits, L2-resident): a warp covers 32 consecutive
-    // positions, base is a multiple of 32
-    const unsigned bits = __ballot_sync(__activemask(), par >= 0);
-    if ((t & 31) == 0) hasp[p >> 5] = bits;
-    for (int k = 0; k < m; ++k) out[st + k] = make_int2(L[k], k + 1 < m ? L[k + 1] : -(int)(p + 1));
-  }
+  if (lists != tmp + e0)
+    fy_target_lists(tsm + 2 * B, cnt, cur, base, n, B, e0, parent, out, hasp);
+  else
+    fy_target_lists(tmp + e0, cnt, cur, base, n, B, e0, parent, out, hasp);
 }
 
 // E: per step bucket; entries e[lo..hi) are the bucket's steps in any order.
@@ -1048,25 +1075,52 @@ __global__ void __launch_bounds__(256) fy_emit_kernel(const int* __restrict__ of
   const int b = blockIdx.x;
   const long long e0 = offs[(size_t)b * G];
   const long long e1 = b + 1 < nbk ? offs[(size_t)(b + 1) * G] : cnt_total;
-  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const int2 v2 = ent[e];
-    int v = v2.y;
-    if (v >= 0) {
-      // walk only through positions that have a parent (bitmap in L2)
-      while ((__ldcg(hasp + (v >> 5)) >> (v & 31)) & 1u) v = __ldcg(parent + v);
-    } else {
-      v = -v - 1;
+  // EU independent chains per thread, walked in lock step (memory-level
+  // parallelism for the random parent reads); a chain only continues through
+  // positions whose has-parent bit is set (bitmap in L2)
+  constexpr int EU = 4;
+  for (long long e0u = e0 + threadIdx.x; e0u < e1; e0u += (long long)blockDim.x * EU) {
+    int st[EU], v[EU];
+    bool live[EU];
+#pragma unroll
+    for (int u = 0; u < EU; ++u) {
+      const long long e = e0u + (long long)u * blockDim.x;
+      const bool ok = e < e1;
+      const int2 v2 = ok ? ent[e] : make_int2(-1, -1);
+      st[u] = v2.x;
+      v[u] = v2.y >= 0 ? v2.y : -v2.y - 1;
+      live[u] = ok && v2.y >= 0;
     }
-    if (result) result[v2.x] = v;
-    if (dst) {
-      const int4* sp = src + (long long)v * rq;
-      int4* dp = dst + (long long)v2.x * rq;
-      for (int k = 0; k < rq; ++k) dp[k] = __ldcs(sp + k);
+    bool any = true;
+    while (any) {
+      unsigned w[EU];
+#pragma unroll
+      for (int u = 0; u < EU; ++u) w[u] = live[u] ? __ldcg(hasp + (v[u] >> 5)) : 0u;
+      any = false;
+#pragma unroll
+      for (int u = 0; u < EU; ++u) {
+        live[u] = live[u] && ((w[u] >> (v[u] & 31)) & 1u);
+        any |= live[u];
+      }
+      if (!any) break;
+#pragma unroll
+      for (int u = 0; u < EU; ++u)
+        if (live[u]) v[u] = __ldcg(parent + v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < EU; ++u) {
+      if (st[u] < 0) continue;
+      if (result) result[st[u]] = v[u];
+      if (dst) {
+        const int4* sp = src + (long long)v[u] * rq;
+        int4* dp = dst + (long long)st[u] * rq;
+        for (int k = 0; k < rq; ++k) dp[k] = __ldcs(sp + k);
+      }
     }
   }
 }
 
-#define FY_SMEM_LG 13
+#define FY_SMEM_LG 12
 static size_t apply_ws_bytes(long long n) {
   const int lg = fy_bucket_log(n > 1 ? n : 2);
   const long long nbk = (n + (1LL << lg) - 1) >> lg;
@@ -1105,23 +1159,26 @@ static int fy_apply_ex(int* j, long long n, long long first, int* result, const 
   unsigned* hasp = cv.take<unsigned>((size_t)(nbk << (lg - 5)) + 1);
   SPTK_REQUIRE(cv.ok(), "fy_apply: workspace too small");
   SPTK_REQUIRE(ncb <= 128 && (1 << MSD_CB) <= MSD_T, "fy_apply: n=%lld too large", n);
-  const size_t hsm = sizeof(int) * (size_t)nbk;
+  const size_t hsm = sizeof(unsigned) * (size_t)((nbk + 1) / 2);
+  const long long gcount_ll = (cnt + 65534) / 65535;
+  const unsigned Gc = (unsigned)(gcount_ll > 4 * 148 ? gcount_ll : 4 * 148);
   static bool configured = false;
   if (!configured) {
     SPTK_CUDA_TRY(cudaFuncSetAttribute(msd_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     SPTK_CUDA_TRY(cudaFuncSetAttribute(msd_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(fy_target_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 << FY_SMEM_LG));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(fy_target_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (8 << FY_SMEM_LG) + (int)sizeof(int) * FY_LCAP));
     configured = true;
   }
   SPTK_REQUIRE(hsm <= (64u << 10), "fy_apply: n=%lld too large", n);
-  const size_t tsm = gcc ? 0 : (size_t)8 << lg;
-  const unsigned G = 2 * 148;
+  const size_t tsm = gcc ? 0 : ((size_t)8 << lg) + sizeof(int) * FY_LCAP;
+  const unsigned G = 4 * 148;
   auto partition = [&](bool from_j, const int2* src, int2* dst) -> int {
     SPTK_CUDA_TRY(cudaMemsetAsync(fcnt, 0, sizeof(int) * (nbk + 1), s));
     if (from_j)
-      msd_count_kernel<true><<<G, MSD_T, hsm, s>>>(j, nullptr, f, cnt, lg, nbk, fcnt);
+      msd_count_kernel<true><<<Gc, MSD_T, hsm, s>>>(j, nullptr, f, cnt, lg, nbk, fcnt);
     else
-      msd_count_kernel<false><<<G, MSD_T, hsm, s>>>(nullptr, src, 0, cnt, lg, nbk, fcnt);
+      msd_count_kernel<false><<<Gc, MSD_T, hsm, s>>>(nullptr, src, 0, cnt, lg, nbk, fcnt);
     SPTK_CHECK_LAUNCH();
     if (exclusive_scan(fcnt, nbk, boff, sws, s)) return 1;
     SPTK_CUDA_TRY(cudaMemcpyAsync(fcur, boff, sizeof(int) * nbk, cudaMemcpyDeviceToDevice, s));
