@@ -611,7 +611,8 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
         tc::fence_after_sync();
         const uint32_t a = sbase + 4 * C::OFF_W;
         issue_gemm<J, R, false>(tbase, a, 0, sbase + 4 * (C::OFF_BN + n * J * R), 0, id_g);
-        issue_gemm<R, R, false>(tbase + J, a, 0, sbase + 4 * (C::OFF_G + n * R * R), 0, id_h);
+        // the refreshed c of the last mode is never read again: no h for it
+        if (n < N - 1) issue_gemm<R, R, false>(tbase + J, a, 0, sbase + 4 * (C::OFF_G + n * R * R), 0, id_h);
         tc::mma_commit(&mbar);
       }
       // every thread is past its mode n-1 update: that slot is free for the
@@ -631,8 +632,10 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       float g[J], h[R];
 #pragma unroll
       for (int q = 0; q < J / 16; ++q) tc::tmem_ld16(tlane + 16 * q, &g[16 * q]);
+      if (n < N - 1) {
 #pragma unroll
-      for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + J + 16 * q, &h[16 * q]);
+        for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + J + 16 * q, &h[16 * q]);
+      }
       float* at = sm + a_off(n, pb);
       float a[J], a0[J];
 #pragma unroll
@@ -680,9 +683,11 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
             tc::st_v4_hint(dst, v, pol_keep);
         }
       }
-      const float keep = 1.f - gm * lm, step = gm * (cur.x - inter);
+      if (n < N - 1) {
+        const float keep = 1.f - gm * lm, step = gm * (cur.x - inter);
 #pragma unroll
-      for (int r = 0; r < R; ++r) c[n][r] = fmaf(step, h[r], keep * c[n][r]);
+        for (int r = 0; r < R; ++r) c[n][r] = fmaf(step, h[r], keep * c[n][r]);
+      }
     }
     tc::cp_async_commit();
     cur = nxt;
@@ -705,6 +710,304 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     tc::fence_after_sync();
     tc::tmem_dealloc(tbase, C::TCOLS);
   }
+}
+
+// ----------------------------------------------------------------------------
+// v3: the v2 update with two threads per sample.  256 threads own one
+// 128-sample tile: warp w reads TMEM lane quadrant w % 4 (samples
+// 32(w%4)..+31) and owns column half h = w / 4 of every J- or R-vector, so
+// each thread's elementwise chain (products, update, refresh, write-back) is
+// half as long and twice as many warps cover a tile.  The only cross-thread
+// quantity, inter = a . gs, equals sum_r W_n[r] c_n[r] (the current
+// prediction), so each thread adds its half of that sum and exchanges it
+// through shared memory across the barrier that already precedes the MMA.
+// ----------------------------------------------------------------------------
+template <int N, int J, int R>
+struct Tc3Cfg {
+  static constexpr int M = 128;
+  static constexpr int OFF_BT = 0;
+  static constexpr int OFF_BN = OFF_BT + N * R * J;
+  static constexpr int OFF_G = OFF_BN + N * J * R;
+  static constexpr int OFF_A = OFF_G + N * R * R;        // N + 1 slots of 128 x J
+  static constexpr int OFF_W = OFF_A + (N + 1) * M * J;  // 128 x R
+  static constexpr int OFF_X = OFF_W + M * R;            // 2 x 128 partial predictions
+  static constexpr int FLOATS = OFF_X + 2 * M;
+  static constexpr int NEED = (N * R > J + R) ? N * R : J + R;
+  static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
+};
+
+template <int N, int J, int R, bool HV>
+__global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
+    factor_tc3_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
+                      float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p,
+                      unsigned* __restrict__ tile_ctr) {
+  static_assert(J == R && J % 16 == 0, "v3 needs J == R, a multiple of 16");
+  constexpr int RW = N <= 3 ? 4 : (N <= 7 ? 8 : 16);
+  constexpr int H = J / 2;  // columns per thread
+  using C = Tc3Cfg<N, J, R>;
+  extern __shared__ __align__(16) float sm[];
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qd = warp & 3, hf = warp >> 2, s = 32 * qd + lane;  // quadrant, column half, sample
+  const int c0 = hf * H;                                         // first owned column
+
+  for (int e = tid; e < N * J * R; e += 256) {
+    const int n = e / (J * R), rem = e - n * (J * R), j = rem / R, r = rem - j * R;
+    const float b = __ldg(cor + e);
+    sm[C::OFF_BT + n * R * J + canon<R>(r, j)] = b;
+    sm[C::OFF_BN + n * J * R + canon<J>(j, r)] = b;
+  }
+  for (int e = tid; e < N * R * R; e += 256) {
+    const int n = e / (R * R), rem = e - n * (R * R), r = rem / R, r2 = rem - r * R;
+    float g = 0.f;
+    for (int j = 0; j < J; ++j) g = fmaf(__ldg(cor + n * J * R + j * R + r), __ldg(cor + n * J * R + j * R + r2), g);
+    sm[C::OFF_G + n * R * R + canon<R>(r, r2)] = g;
+  }
+  if (tid == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tslot, C::TCOLS);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = tslot;
+  const uint32_t tlane = tbase + ((uint32_t)(qd * 32) << 16);
+  const uint32_t sbase = tc::smem_u32(sm);
+  const uint32_t id_c = tc::idesc_tf32(128, R), id_g = tc::idesc_tf32(128, J), id_h = tc::idesc_tf32(128, R);
+  const uint64_t pol_keep = tc::policy_evict_last(), pol_stream = tc::policy_evict_first();
+  uint32_t phase = 0;
+
+  auto a_off = [&](int n, int pb) { return C::OFF_A + (n < N - 1 ? n : N - 1 + pb) * 128 * J; };
+  // this warp's half-rows of its 32 samples: 2 lanes per row chunk pair
+  // (H/4 chunks per half-row; H = 8 -> 2 chunks, 16 rows per instruction)
+  constexpr int HCH = H / 4, RPI = 32 / HCH;
+  const int cq = lane % HCH, crow = lane / HCH;
+  auto issue_mode = [&](const RecReg<N, RW>& rr, int n, int pb) {
+    const uint32_t dst = sbase + 4 * a_off(n, pb);
+#pragma unroll
+    for (int k = 0; k < HCH; ++k) {
+      const int sl = k * RPI + crow;
+      const int row = __shfl_sync(0xffffffffu, rr.idx[n], sl);
+      const int ok = __shfl_sync(0xffffffffu, rr.valid ? 1 : 0, sl);
+      const float* src = fac + p.foff[n] + (long long)row * J + c0 + 4 * cq;
+      tc::cp_async16_nohint(dst + 4 * canon<128>(32 * qd + sl, c0 + 4 * cq), src, ok ? 16u : 0u);
+    }
+  };
+
+  const long long G = gridDim.x;
+  uint32_t& s_claim = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 3);
+  long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
+  if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
+  RecReg<N, RW> cur, nxt;
+  // visit entries / records are indexed by sample s (both halves load them)
+  auto vis = [&](long long t) -> int {
+    long long k = t * 128 + s;
+    k = k < n_visit ? k : n_visit - 1;
+    if (HV) return tc::ld_stream_s32(visit + k, pol_stream);
+    return (int)k;
+  };
+  auto valid_of = [&](long long t) { return t * 128 + s < n_visit; };
+  int v2 = vis(t2);
+  load_rec<N, RW>(cur, rec, vis(tile), valid_of(tile), base, pol_stream);
+  load_rec<N, RW>(nxt, rec, vis(t1), valid_of(t1), base, pol_stream);
+  int pb = 0;
+  const unsigned pfm = p.prefetch == 0 ? 0u : p.prefetch == 2 ? ~0u : ~p.atomic_mask;
+#pragma unroll
+  for (int n = 0; n < N; ++n)
+    if (pfm >> n & 1u) issue_mode(cur, n, pb);
+  tc::cp_async_commit();
+  __syncthreads();
+  long long t3 = 3 * G + s_claim;
+  float* px = sm + C::OFF_X;
+  while (tile * 128 < n_visit) {
+    unsigned claim = 0;
+    if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+      if (!(pfm >> n & 1u)) issue_mode(cur, n, pb);
+    tc::cp_async_commit();
+    RecReg<N, RW> nnxt;
+    load_rec<N, RW>(nnxt, rec, v2, valid_of(t2), base, pol_stream);
+    v2 = vis(t3);
+    tc::cp_async_wait_all();
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        issue_gemm<R, J, false>(tbase + n * R, sbase + 4 * a_off(n, pb), 0, sbase + 4 * (C::OFF_BT + n * R * J), 0,
+                                id_c);
+      tc::mma_commit(&mbar);
+    }
+    if (pfm >> (N - 1) & 1u) issue_mode(nxt, N - 1, pb ^ 1);
+    tc::mbar_wait(&mbar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+    float c[N][H];
+#pragma unroll
+    for (int n = 0; n < N; ++n) tc::tmem_ldh<H>(tlane + n * R + c0, c[n]);
+
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      // W_n (my half), my half of inter = sum_r W_n[r] c_n[r]
+      float* wt = sm + C::OFF_W;
+      float part = 0.f;
+#pragma unroll
+      for (int q = 0; q < H / 4; ++q) {
+        float w4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float w = 1.f;
+#pragma unroll
+          for (int n0 = 0; n0 < N; ++n0)
+            if (n0 != n) w *= c[n0][4 * q + u];
+          w4[u] = w;
+          part = fmaf(w, c[n][4 * q + u], part);
+        }
+        *reinterpret_cast<float4*>(wt + canon<128>(s, c0 + 4 * q)) = make_float4(w4[0], w4[1], w4[2], w4[3]);
+      }
+      px[hf * 128 + s] = part;
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t a = sbase + 4 * C::OFF_W;
+        issue_gemm<J, R, false>(tbase, a, 0, sbase + 4 * (C::OFF_BN + n * J * R), 0, id_g);
+        if (n < N - 1) issue_gemm<R, R, false>(tbase + J, a, 0, sbase + 4 * (C::OFF_G + n * R * R), 0, id_h);
+        tc::mma_commit(&mbar);
+      }
+      if (n >= 1 && n - 1 < N - 1 && (pfm >> (n - 1) & 1u)) issue_mode(nxt, n - 1, 0);
+      const float inter = part + px[(hf ^ 1) * 128 + s];
+      tc::mbar_wait(&mbar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      float g[H], hv[H];
+      tc::tmem_ldh<H>(tlane + c0, g);
+      if (n < N - 1) tc::tmem_ldh<H>(tlane + J + c0, hv);
+      float* at = sm + a_off(n, pb);
+      float a[H], a0[H];
+#pragma unroll
+      for (int q = 0; q < H / 4; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(at + canon<128>(s, c0 + 4 * q));
+        a[4 * q] = v.x;
+        a[4 * q + 1] = v.y;
+        a[4 * q + 2] = v.z;
+        a[4 * q + 3] = v.w;
+      }
+      const float gm = p.gam[n], lm = p.lam[n];
+#pragma unroll
+      for (int j = 0; j < H; ++j) {
+        a0[j] = a[j];
+        const float gr = -cur.x * g[j] + lm * a[j] + inter * g[j];
+        a[j] -= gm * gr;
+      }
+      const bool red = p.atomic_mask >> n & 1u;
+#pragma unroll
+      for (int q = 0; q < H / 4; ++q) {
+        const float4 v = red ? make_float4(a[4 * q] - a0[4 * q], a[4 * q + 1] - a0[4 * q + 1],
+                                           a[4 * q + 2] - a0[4 * q + 2], a[4 * q + 3] - a0[4 * q + 3])
+                             : make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+        *reinterpret_cast<float4*>(at + canon<128>(s, c0 + 4 * q)) = v;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < HCH; ++k) {
+        const int sl = k * RPI + crow;
+        const int row = __shfl_sync(0xffffffffu, cur.idx[n], sl);
+        const int ok = __shfl_sync(0xffffffffu, cur.valid ? 1 : 0, sl);
+        const float4 v = *reinterpret_cast<const float4*>(at + canon<128>(32 * qd + sl, c0 + 4 * cq));
+        float* dst = fac + p.foff[n] + (long long)row * J + c0 + 4 * cq;
+        if (ok) {
+          if (red)
+            tc::red_add_v4(dst, v);
+          else
+            tc::st_v4_hint(dst, v, pol_keep);
+        }
+      }
+      if (n < N - 1) {
+        const float keep = 1.f - gm * lm, step = gm * (cur.x - inter);
+#pragma unroll
+        for (int r = 0; r < H; ++r) c[n][r] = fmaf(step, hv[r], keep * c[n][r]);
+      }
+    }
+    tc::cp_async_commit();
+    cur = nxt;
+    nxt = nnxt;
+    tile = t1;
+    t1 = t2;
+    t2 = t3;
+    pb ^= 1;
+    if (tid == 0) s_claim = claim;
+    __syncthreads();
+    t3 = 3 * G + s_claim;
+  }
+  tc::cp_async_wait_all();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tbase, C::TCOLS);
+  }
+}
+
+template <int N, int J, int R>
+static int launch_tc3(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                      const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+  using C = Tc3Cfg<N, J, R>;
+  TcParams<N> p;
+  for (int n = 0; n < N; ++n) {
+    p.foff[n] = md.foff[n];
+    p.gam[n] = gam[n];
+    p.lam[n] = lam[n];
+  }
+  p.dbg = nullptr;
+  p.atomic_mask = hot_mode_mask(md);
+  {
+    const char* e = getenv("SPTK_TC_PREFETCH");
+    p.prefetch = e ? atoi(e) : 1;
+  }
+  (void)rw;
+  auto kfn = visit ? factor_tc3_kernel<N, J, R, true> : factor_tc3_kernel<N, J, R, false>;
+  static int configured = 0;
+  static int per_sm = 1;
+  if (!configured) {
+    for (auto f : {factor_tc3_kernel<N, J, R, true>, factor_tc3_kernel<N, J, R, false>}) {
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    cudaFuncAttributes fa;
+    SPTK_CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)kfn));
+    const int regs = fa.numRegs < 1 ? 1 : fa.numRegs;
+    int by_regs = 65536 / (((regs * 32 + 255) / 256) * 256 * 8);
+    int by_smem = (int)((228 * 1024) / (C::SMEM + fa.sharedSizeBytes + 1024));
+    int by_tmem = 512 / C::TCOLS;
+    int n = by_regs < by_smem ? by_regs : by_smem;
+    n = n < by_tmem ? n : by_tmem;
+    int cap = n >= 3 ? n - 1 : n;  // leave room for the side-stream samplers (see resident_ctas)
+    if (const char* e = getenv("SPTK_TC_CTAS")) cap = atoi(e);
+    if (cap >= 1 && cap < n) n = cap;
+    per_sm = n < 1 ? 1 : n;
+    if (getenv("SPTK_DEBUG")) fprintf(stderr, "[sptk] tc3 regs=%d smem=%zu -> %d CTAs/SM\n", regs, C::SMEM, per_sm);
+    configured = 1;
+  }
+  long long tiles = (n_visit + 127) / 128;
+  long long blocks = 148LL * per_sm;
+  if (blocks > tiles) blocks = tiles;
+  static unsigned slot = 0;
+  unsigned* ctr = nullptr;
+  SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tile_ctr));
+  ctr += (slot++ & 63u);
+  SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+  kfn<<<(unsigned)blocks, 256, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
+  SPTK_CHECK_LAUNCH();
+  return 0;
 }
 
 template <int N, int J, int R>
@@ -750,7 +1053,8 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   return 0;
 }
 
-// 0 off (CUDA-core FMA kernel), 1 TF32 v2 (default), 2 TF32 v1, 3 3xTF32 v1
+// 0 off (CUDA-core FMA kernel), 1 TF32 v2 (default), 2 TF32 v1, 3 3xTF32 v1,
+// 4 TF32 v3 (two threads per sample)
 static int g_tc_mode = -1;
 
 static int tc_mode_env() {
@@ -762,7 +1066,7 @@ static int tc_mode_env() {
 }
 
 int set_tc_mode(int mode) {
-  if (mode < 0 || mode > 3) return 2;
+  if (mode < 0 || mode > 4) return 2;
   g_tc_mode = mode;
   return 0;
 }
@@ -815,7 +1119,8 @@ int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, l
   if (J != R || rw != rec_words(N)) return 0;
 #define SPTK_TC_CASE(NN, JJ)                                                                                 \
   if (N == NN && J == JJ) {                                                                                  \
-    *rc = mode == 1   ? launch_tc2<NN, JJ, JJ>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s)        \
+    *rc = mode == 4   ? launch_tc3<NN, JJ, JJ>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s)        \
+          : mode == 1 ? launch_tc2<NN, JJ, JJ>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s)        \
           : mode == 2 ? launch_tc<NN, JJ, JJ, false>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s) \
                       : launch_tc<NN, JJ, JJ, true>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);  \
     return 1;                                                                                                \

@@ -94,6 +94,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+// H consecutive columns (H a multiple of 8)
+template <int H>
+__device__ __forceinline__ void tmem_ldh(uint32_t taddr, float* v) {
+  if (H % 16 == 0) {
+#pragma unroll
+    for (int q = 0; q < H / 16; ++q) tmem_ld16(taddr + 16 * q, v + 16 * q);
+  } else {
+#pragma unroll
+    for (int q = 0; q < H / 8; ++q) tmem_ld8(taddr + 8 * q, v + 8 * q);
+  }
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 }  // namespace tc
