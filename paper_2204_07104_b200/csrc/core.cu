@@ -427,7 +427,7 @@ int core_pass(const int* rec, int rw, const int* visit, const int* map, long lon
   SPTK_REQUIRE(ws_bytes >= (size_t)blocks * md.cor_size * sizeof(double), "core_pass: workspace too small");
   double* partial = (double*)ws;
   auto kfn = core_pass_kernel<T, false>;
-  if (smem > 48 * 1024) SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, rw, rec_val_off(md.n_modes, f64), visit, map, n_visit, fac, cor, md, S,
                                            partial, nullptr);
   SPTK_CHECK_LAUNCH();
@@ -465,7 +465,7 @@ int core_pass_exact(const int* rec, int rw, const int* visit, const int* map, lo
   long long* d_lo = (long long*)((char*)ws + (((size_t)nb * md.cor_size * sizeof(double) + 255) & ~(size_t)255));
   SPTK_CUDA_TRY(cudaMemcpyAsync(d_lo, h_lo, sizeof(long long) * (nb + 1), cudaMemcpyHostToDevice, s));
   auto kfn = core_pass_kernel<T, true>;
-  if (smem > 48 * 1024) SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kfn<<<(unsigned)nb, 256, smem, s>>>(rec, rw, rec_val_off(md.n_modes, f64), visit, map, n_visit, fac, cor, md, S,
                                        partial, d_lo);
   SPTK_CHECK_LAUNCH();

@@ -100,7 +100,7 @@ int eval(const int* rec, int rw, long long m, const T* fac, const T* cor, const 
 #define SPTK_EVAL_CASE(RV)                                                                        \
   case RV: {                                                                                      \
     auto kfn = eval_kernel<T, RV>;                                                                \
-    if (smem > 48 * 1024) SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
     kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, rw, m, fac, cor, md, pred_out, sums);             \
     break;                                                                                        \
   }
@@ -112,10 +112,12 @@ int eval(const int* rec, int rw, long long m, const T* fac, const T* cor, const 
     SPTK_EVAL_CASE(16)
     SPTK_EVAL_CASE(32)
     default: {
+      // generic rank: up to 255 registers per thread (fp64), so 128-thread
+      // blocks (256 would need more than the SM's 64K registers)
       auto kfn = eval_kernel<T, 0>;
-      if (smem > 48 * 1024)
-        SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, rw, m, fac, cor, md, pred_out, sums);
+      // (always: the 1.5 KB of static shared memory counts against the default 48 KB)
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kfn<<<(unsigned)(4 * blocks), 64, smem, s>>>(rec, rw, m, fac, cor, md, pred_out, sums);
     }
   }
 #undef SPTK_EVAL_CASE

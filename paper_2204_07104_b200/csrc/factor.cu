@@ -38,34 +38,52 @@ struct TpsParams {
   float lam[N];
 };
 
+// Software pipeline over the grid-stride samples: the visit entry two
+// samples ahead and the record one sample ahead are in flight while the
+// current sample computes (a thread's chain visit -> record -> rows would
+// otherwise expose three memory latencies per sample).
+template <int RW>
+__device__ __forceinline__ void tps_load_rec(const int* __restrict__ rec, long long ri, int4& w0, int4& w1) {
+  const int4* rp = reinterpret_cast<const int4*>(rec + ri * RW);
+  w0 = __ldg(rp);
+  if (RW >= 8) w1 = __ldg(rp + 1);
+}
+
 template <int N, int J, int R, int RW>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, (J <= 4 ? 6 : (N * J <= 24 ? 5 : (J <= 8 ? 4 : 3))))
     factor_tps_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit,
                       long long base, float* __restrict__ fac, TpsParams<N> p) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n_visit; k += stride) {
-    const long long ri = base + (visit ? (long long)__ldg(visit + k) : k);
-    const int* rp = rec + ri * RW;
+  const long long k0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  auto vis = [&](long long k) -> long long {
+    const long long kc = k < n_visit ? k : n_visit - 1;
+    return base + (visit ? (long long)__ldg(visit + kc) : kc);
+  };
+  long long v_next = vis(k0 + stride);
+  int4 c0w = make_int4(0, 0, 0, 0), c1w = make_int4(0, 0, 0, 0);
+  tps_load_rec<RW>(rec, vis(k0), c0w, c1w);
+  for (long long k = k0; k < n_visit; k += stride) {
     int idx[N];
     float x;
     {
-      int4 w0 = __ldg(reinterpret_cast<const int4*>(rp));
       int wv[RW];
-      wv[0] = w0.x;
-      wv[1] = w0.y;
-      wv[2] = w0.z;
-      wv[3] = w0.w;
+      wv[0] = c0w.x;
+      wv[1] = c0w.y;
+      wv[2] = c0w.z;
+      wv[3] = c0w.w;
       if (RW >= 8) {
-        int4 w1 = __ldg(reinterpret_cast<const int4*>(rp) + 1);
-        wv[4 % RW] = w1.x;
-        wv[5 % RW] = w1.y;
-        wv[6 % RW] = w1.z;
-        wv[7 % RW] = w1.w;
+        wv[4 % RW] = c1w.x;
+        wv[5 % RW] = c1w.y;
+        wv[6 % RW] = c1w.z;
+        wv[7 % RW] = c1w.w;
       }
 #pragma unroll
       for (int n = 0; n < N; ++n) idx[n] = wv[n];
       x = __int_as_float(wv[N]);
     }
+    // next sample's record and the visit entry after it
+    tps_load_rec<RW>(rec, v_next, c0w, c1w);
+    v_next = vis(k + 2 * stride);
     float a[N][J];
 #pragma unroll
     for (int n = 0; n < N; ++n) {
@@ -416,8 +434,7 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
     size_t smem = sizeof(T) * ((size_t)((md.cor_size + 1) & ~1) + (size_t)per_thread * 32);
     SPTK_REQUIRE(smem <= 200 * 1024, "factor_pass(sequential): model ranks too large for shared memory");
     auto kfn = factor_seq_kernel<T>;
-    if (smem > 48 * 1024)
-      SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kfn<<<1, 32, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl, cand, per_thread);
     SPTK_CHECK_LAUNCH();
     return 0;
@@ -443,8 +460,7 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
   }
   SPTK_REQUIRE(smem <= 200 * 1024, "factor_pass: model ranks too large for shared memory");
   auto kfn = factor_wps_kernel<T>;
-  if (smem > 48 * 1024)
-    SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   long long blocks = (n_visit + warps - 1) / warps;
   if (blocks > 148 * 8) blocks = 148 * 8;
   kfn<<<(unsigned)blocks, 32 * warps, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl, per_warp);
