@@ -434,7 +434,7 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
     size_t smem = sizeof(T) * ((size_t)((md.cor_size + 1) & ~1) + (size_t)per_thread * 32);
     SPTK_REQUIRE(smem <= 200 * 1024, "factor_pass(sequential): model ranks too large for shared memory");
     auto kfn = factor_seq_kernel<T>;
-          SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kfn<<<1, 32, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl, cand, per_thread);
     SPTK_CHECK_LAUNCH();
     return 0;

@@ -582,9 +582,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     TC2_STAMP(4);
     float c[N][R];
 #pragma unroll
-    for (int n = 0; n < N; ++n)
-#pragma unroll
-      for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + n * R + 16 * q, &c[n][16 * q]);
+    for (int n = 0; n < N; ++n) tc::tmem_ldh<R>(tlane + n * R, c[n]);
 
 #pragma unroll
     for (int n = 0; n < N; ++n) {
@@ -630,12 +628,8 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       tc::fence_after_sync();
       TC2_STAMP(7 + 3 * n);
       float g[J], h[R];
-#pragma unroll
-      for (int q = 0; q < J / 16; ++q) tc::tmem_ld16(tlane + 16 * q, &g[16 * q]);
-      if (n < N - 1) {
-#pragma unroll
-        for (int q = 0; q < R / 16; ++q) tc::tmem_ld16(tlane + J + 16 * q, &h[16 * q]);
-      }
+      tc::tmem_ldh<J>(tlane, g);
+      if (n < N - 1) tc::tmem_ldh<R>(tlane + J, h);
       float* at = sm + a_off(n, pb);
       float a[J], a0[J];
 #pragma unroll
@@ -1128,6 +1122,16 @@ int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, l
   SPTK_TC_CASE(3, 16)
   SPTK_TC_CASE(4, 16)
   SPTK_TC_CASE(3, 32)
+  if (mode == 1) {  // v2 only: 8-column tiles (MMA N = 8, K = 8)
+    if (N == 3 && J == 8) {
+      *rc = launch_tc2<3, 8, 8>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);
+      return 1;
+    }
+    if (N == 6 && J == 8) {
+      *rc = launch_tc2<6, 8, 8>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);
+      return 1;
+    }
+  }
 #undef SPTK_TC_CASE
   return 0;
 }
