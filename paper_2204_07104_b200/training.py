@@ -256,6 +256,9 @@ class EpochRunner:
         # apply is bandwidth-bound, so splitting them across epochs lets both
         # run underneath the factor pass instead of back to back.
         self.prefetch = prefetch
+        import os
+
+        self.fy_on_main = os.environ.get("SPTK_FY_MAIN", "0") == "1"
         mk = (lambda: torch.cuda.Stream(device=dev)) if prefetch else (lambda: None)
         self.side_j, self.side, self.side2 = mk(), mk(), mk()
         ev2 = lambda: [torch.cuda.Event(), torch.cuda.Event()]  # noqa: E731
@@ -340,14 +343,17 @@ class EpochRunner:
                 self.draw_jseq(t + 1, o, self.side_j)
                 self._mark("jseq_end", self.side_j)
                 self.j_ready[o].record(self.side_j)
-            # perm[o] was last read by epoch t-1 (`done`)
-            self.side.wait_event(self.done[o])
-            self.side.wait_event(self.j_ready[o])
-            self._mark("perm_start", self.side)
-            self.apply_jseq(t + 1, o, self.side)
-            self._mark("perm_end", self.side)
-            self.j_free[o].record(self.side)
-            self.perm_ready[o].record(self.side)
+            # perm[o] was last read by epoch t-1 (`done`).  The apply runs on
+            # the main stream ahead of this epoch's factor pass (fy_on_main) or
+            # beside it on its own stream.
+            st = main if self.fy_on_main else self.side
+            st.wait_event(self.done[o])
+            st.wait_event(self.j_ready[o])
+            self._mark("perm_start", st)
+            self.apply_jseq(t + 1, o, st)
+            self._mark("perm_end", st)
+            self.j_free[o].record(st)
+            self.perm_ready[o].record(st)
         if t + 2 < E and self.j_epoch[slot] != t + 2:
             # jbuf[slot] is free once epoch t's apply has read it
             self.side_j.wait_event(self.j_free[slot])
