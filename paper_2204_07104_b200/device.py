@@ -27,7 +27,12 @@ class DeviceModel:
     (trainer.py:135-141, _loops.py:8-10), fp32 (throughput) or fp64
     (verification)."""
 
-    def __init__(self, model, f64: bool = False, device=None):
+    def __init__(self, model, f64: bool = False, device=None, pad_rank: int | None = None):
+        """pad_rank = P zero-pads every J_n and R up to P on the device.  The
+        padded model is exactly equivalent (padded rows/columns of A and B are
+        zero and every gradient on them is zero), so ranks below the smallest
+        tensor-core tile (J = R = 4 -> 8) run on the tcgen05 kernels;
+        ``download_into`` strips the padding."""
         torch = _torch()
         _lib.require_cuda()
         self.device = torch.device(device or "cuda")
@@ -35,15 +40,27 @@ class DeviceModel:
         self.dtype = torch.float64 if f64 else torch.float32
         self.order = model.order
         self.dims = tuple(model.dims)
-        self.rcore = int(model.r_core)
-        self.jr = np.asarray(model.j_ranks, dtype=np.int64)
-        sizes_a = [d * j for d, j in zip(model.dims, model.j_ranks)]
-        sizes_b = [j * model.r_core for j in model.j_ranks]
+        self.true_jr = [int(j) for j in model.j_ranks]
+        self.true_r = int(model.r_core)
+        P = int(pad_rank) if pad_rank else 0
+        self.rcore = max(self.true_r, P)
+        self.jr = np.asarray([max(j, P) for j in self.true_jr], dtype=np.int64)
+        sizes_a = [d * j for d, j in zip(model.dims, self.jr)]
+        sizes_b = [int(j) * self.rcore for j in self.jr]
         self.foff = np.concatenate([[0], np.cumsum(sizes_a)]).astype(np.int64)
         self.coff = np.concatenate([[0], np.cumsum(sizes_b)]).astype(np.int64)
         npdt = np.float64 if f64 else np.float32
-        fac = np.concatenate([np.asarray(a, dtype=np.float64).ravel() for a in model.factors]).astype(npdt)
-        cor = np.concatenate([np.asarray(b, dtype=np.float64).ravel() for b in model.core_factors]).astype(npdt)
+
+        def padded(m, rows, cols):
+            m = np.asarray(m, dtype=np.float64)
+            if m.shape == (rows, cols):
+                return m.ravel()
+            out = np.zeros((rows, cols))
+            out[: m.shape[0], : m.shape[1]] = m
+            return out.ravel()
+
+        fac = np.concatenate([padded(a, a.shape[0], int(j)) for a, j in zip(model.factors, self.jr)]).astype(npdt)
+        cor = np.concatenate([padded(b, int(j), self.rcore) for b, j in zip(model.core_factors, self.jr)]).astype(npdt)
         self.fac = torch.from_numpy(fac).to(self.device)
         self.cor = torch.from_numpy(cor).to(self.device)
         self.cor_size = int(self.coff[-1])
@@ -56,9 +73,11 @@ class DeviceModel:
         fac = self.fac.double().cpu().numpy()
         cor = self.cor.double().cpu().numpy()
         for n, a in enumerate(model.factors):
-            np.copyto(a, fac[self.foff[n]: self.foff[n + 1]].reshape(a.shape))
+            full = fac[self.foff[n]: self.foff[n + 1]].reshape(a.shape[0], int(self.jr[n]))
+            np.copyto(a, full[:, : a.shape[1]])
         for n, b in enumerate(model.core_factors):
-            np.copyto(b, cor[self.coff[n]: self.coff[n + 1]].reshape(b.shape))
+            full = cor[self.coff[n]: self.coff[n + 1]].reshape(int(self.jr[n]), self.rcore)
+            np.copyto(b, full[: b.shape[0], : b.shape[1]])
 
 
 class DeviceCoo:

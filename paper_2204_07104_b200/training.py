@@ -200,7 +200,11 @@ class EpochRunner:
         self.owner_rank = owner_rank
         self.order = model.order
         self.nnz = train_set.nnz
-        self.dm = DeviceModel(model, f64=self.f64)
+        # J = R = 4 in throughput mode: run on a zero-padded rank-8 model (the
+        # smallest tcgen05 tile; exactly equivalent, see DeviceModel)
+        pad = 8 if (not self.f64 and self.mode == 0 and model.r_core == 4
+                    and all(int(j) == 4 for j in model.j_ranks)) else None
+        self.dm = DeviceModel(model, f64=self.f64, pad_rank=pad)
         self.part = DevicePartition(train_set.indices, train_set.values, model.dims, self.m, f64=self.f64,
                                     want_ids=False)
         self.schedule = round_schedule(model.order, self.m)

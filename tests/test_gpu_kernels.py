@@ -239,3 +239,44 @@ def test_core_throughput_uniform_ranks(dims, J, nnz, sub):
     want = np.zeros(int(coff[-1]))
     O.core_pass(idx, vals, visit.astype(np.int64), fac, foff, cor, coff, jr, J, want, coff)
     np.testing.assert_allclose(acc.cpu().numpy(), want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
+
+
+def test_rank4_zero_padding_is_exact():
+    """J = R = 4 runs on a zero-padded rank-8 device model (tcgen05 tile):
+    predictions, the factor pass on conflict-free samples and the core
+    gradient equal the rank-4 reference, and the padding stays zero."""
+    from paper_2204_07104_b200 import TuckerModel, _lib
+    from paper_2204_07104_b200.device import DeviceModel, eval_sums
+
+    dims, J = (4000, 4000, 4000), 4
+    idx, vals, fs, bs = _model_and_data(dims, (J,) * 3, J, 2500, 3, distinct=True)
+    model = TuckerModel(dims, (J,) * 3, J, [a.copy() for a in fs], [b.copy() for b in bs])
+    dm = DeviceModel(model, pad_rank=8)
+    assert list(dm.jr) == [8, 8, 8] and dm.rcore == 8
+    recs = _records(idx, vals, False)
+    L = _lib.load()
+    # eval
+    s_pad = eval_sums(dm, recs).cpu().numpy()
+    s_ref = eval_sums(DeviceModel(model), recs).cpu().numpy()
+    np.testing.assert_allclose(s_pad, s_ref, rtol=1e-5)
+    # factor pass (Hogwild kernel, distinct rows -> sequential semantics)
+    g, pg = _lib.f64arr([0.003] * 3)
+    lam, pl = _lib.f64arr([0.01] * 3)
+    _lib.check(L.sptk_set_tc_mode(1), "tc")
+    visit = _dev(np.arange(len(vals)), np.int32)
+    _lib.check(L.sptk_factor_pass(recs.rec.data_ptr(), recs.rw, visit.data_ptr(), len(vals), 0, dm.fac.data_ptr(),
+                                  dm.p_foff, dm.cor.data_ptr(), dm.p_coff, dm.p_jr, 3, 8, pg, pl, 0,
+                                  _lib.stream_ptr()), "factor")
+    fac, foff = O.pack(fs)
+    cor, coff = O.pack(bs)
+    jr = np.array([J] * 3)
+    O.factor_pass(idx, vals, np.arange(len(vals), dtype=np.int64), fac, foff, cor, coff, jr, J, np.full(3, 0.003),
+                  np.full(3, 0.01))
+    out = TuckerModel(dims, (J,) * 3, J, [np.zeros_like(a) for a in fs], [np.zeros_like(b) for b in bs])
+    dm.download_into(out)
+    got, _ = O.pack(out.factors)
+    np.testing.assert_allclose(got, fac, rtol=5e-3, atol=5e-4 * np.abs(fac).max())
+    padded = dm.fac.cpu().numpy()
+    for n, d in enumerate(dims):
+        rows = padded[dm.foff[n]: dm.foff[n + 1]].reshape(d, 8)
+        assert not rows[:, J:].any()
