@@ -1121,6 +1121,12 @@ int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, l
   }
   SPTK_TC_CASE(3, 16)
   SPTK_TC_CASE(4, 16)
+  if (mode == 1 && N == 3 && J == 32) {
+    // at J = R = 32 the one-thread-per-sample kernel needs ~250 registers (one
+    // CTA per SM); two threads per sample is faster (NF: 37 vs 46 ms)
+    *rc = launch_tc3<3, 32, 32>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);
+    return 1;
+  }
   SPTK_TC_CASE(3, 32)
   if (mode == 1) {  // v2 only: 8-column tiles (MMA N = 8, K = 8)
     if (N == 3 && J == 8) {
