@@ -301,7 +301,7 @@ def bench_ours(args, cfg):
     e2e = None
     if not args.no_e2e and world == 1:
         m2 = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
-        k2 = args.e2e_epochs
+        k2 = args.e2e_epochs or args.steps
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         train(m2, DatasetSplit(tr, te), TrainConfig(epochs=k2, seed=1, update_mode=args.mode,
@@ -360,7 +360,7 @@ def main():
     ap.add_argument("--config", default="nf", choices=sorted(CONFIGS))
     ap.add_argument("--rank", type=int, default=None, help="J = R override (rank sweep)")
     ap.add_argument("--mode", default="hogwild", choices=["hogwild", "exact", "auto"])
-    ap.add_argument("--e2e-epochs", type=int, default=5)
+    ap.add_argument("--e2e-epochs", type=int, default=None, help="default: --steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
