@@ -222,7 +222,10 @@ def bench_ours(args, cfg):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    # BENCH_FORCE_DIST=1: the multi-GPU code path (NCCL, DistRunner) even at
+    # world size 1 (exercises it on a one-GPU box)
+    distributed = world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1"
+    if distributed:
         import torch.distributed as td
 
         td.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -237,7 +240,7 @@ def bench_ours(args, cfg):
     # +3: every timed epoch also draws the next epoch's samples (steady state)
     tcfg = TrainConfig(epochs=args.warmup + args.steps + 3, seed=1, update_mode=args.mode,
                        workers=world if world > 1 else 1, alpha_a=cfg.get("alpha_a", 0.009))
-    if world > 1:
+    if distributed:
         from paper_2204_07104_b200 import dist
 
         runner = dist.DistRunner(model, tr, tcfg)
@@ -347,7 +350,7 @@ def bench_ours(args, cfg):
             "setup_seconds": {"data_generation": gen_s},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         torch.distributed.destroy_process_group()
 
 
