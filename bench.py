@@ -240,10 +240,18 @@ def bench_ours(args, cfg):
     # +3: every timed epoch also draws the next epoch's samples (steady state)
     tcfg = TrainConfig(epochs=args.warmup + args.steps + 3, seed=1, update_mode=args.mode,
                        workers=world if world > 1 else 1, alpha_a=cfg.get("alpha_a", 0.009))
+    sim = int(os.environ.get("BENCH_DSGD_SIM", "0"))
     if distributed:
         from paper_2204_07104_b200 import dist
 
         runner = dist.DistRunner(model, tr, tcfg)
+    elif sim > 1:
+        # one rank's share of an M-GPU DSGD epoch (its blocks, their samplers,
+        # the core phase) without the exchanges: a per-rank compute estimate
+        from dataclasses import replace
+
+        tcfg = replace(tcfg, workers=sim)
+        runner = EpochRunner(model, tr, tcfg, owner_rank=0)
     else:
         runner = EpochRunner(model, tr, tcfg)
     # warm-up epochs (not timed)

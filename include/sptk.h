@@ -94,6 +94,12 @@ int sptk_permute_records(const uint64_t h_state[4], long long n, const int32_t* 
 size_t sptk_permutation_j_ws_bytes(long long n);
 int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,
                        void* stream);
+/* Several blocks' j-sequences end to end (block b at [off[b], off[b+1]),
+ * block-local values, off relative to d_j) -> one sequence for a single
+ * sptk_fy_apply over the concatenation, whose result is every block's
+ * permutation shifted by its offset (blocks touch disjoint positions).  One
+ * apply per epoch instead of one per DSGD block. */
+int sptk_fy_globalize(int32_t* d_j, const int32_t* d_block_off, int n_blocks, void* stream);
 size_t sptk_fy_apply_ws_bytes(long long n);
 int sptk_fy_apply(int32_t* d_j, long long n, int32_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
 size_t sptk_choice_ws_bytes(long long pop, long long k);

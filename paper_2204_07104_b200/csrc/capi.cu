@@ -161,6 +161,10 @@ int sptk_fy_apply(int32_t* d_j, long long n, int32_t* d_out, void* d_ws, size_t 
   return fy_apply_public(d_j, n, d_out, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int sptk_fy_globalize(int32_t* d_j, const int32_t* d_block_off, int n_blocks, void* stream) {
+  return fy_globalize(d_j, d_block_off, n_blocks, (cudaStream_t)stream);
+}
+
 int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,
                        void* stream) {
   return permutation_j(h_state, n, d_j, d_ws, ws_bytes, (cudaStream_t)stream);

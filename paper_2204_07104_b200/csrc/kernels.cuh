@@ -13,6 +13,7 @@ size_t perm_ws_bytes(long long n);
 size_t jgen_ws_bytes(long long n);
 size_t fy_ws_bytes(long long n);
 int fy_apply_public(int* j, long long n, int* out, void* ws, size_t ws_bytes, cudaStream_t s);
+int fy_globalize(int* j, const int* off, int nb, cudaStream_t s);
 int permutation(const uint64_t st[4], long long n, int* out, void* ws, size_t ws_bytes, cudaStream_t s);
 int permute_records(const uint64_t st[4], long long n, const int* rec_src, int rw, int* rec_out, int* perm_out,
                     void* ws, size_t ws_bytes, cudaStream_t s);

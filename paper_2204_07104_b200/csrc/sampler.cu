@@ -1282,6 +1282,24 @@ int fy_apply_public(int* j, long long n, int* out, void* ws, size_t ws_bytes, cu
   return fy_apply(j, n, 1, out, cv, s);
 }
 
+// Several blocks' j-sequences laid end to end (block b at [off[b], off[b+1]),
+// block-local values) become one sequence over the concatenation: targets
+// shifted by off[b] and each block's virtual step 0 a self-step.  Blocks
+// touch disjoint position ranges, so one apply of the combined sequence
+// equals the per-block permutations (each shifted by its offset).
+__global__ void fy_globalize_kernel(int* __restrict__ j, const int* __restrict__ off) {
+  const int b = blockIdx.x;
+  const int lo = off[b], hi = off[b + 1];
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) j[i] = (i == lo) ? lo : j[i] + lo;
+}
+
+int fy_globalize(int* j, const int* off, int nb, cudaStream_t s) {
+  if (nb <= 0) return 0;
+  fy_globalize_kernel<<<nb, 256, 0, s>>>(j, off);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
 // --- choice ---------------------------------------------------------------
 static long long lemire_vcap(long long T, double p_rej_max) {
   double mean = T * p_rej_max / (1.0 - p_rej_max);

@@ -235,9 +235,29 @@ class EpochRunner:
         # kernel on another stream may still be using it)
         Lb = _lib.load()
         max_block = max((c for items in self.rounds for (_, _, c) in items), default=1)
+        # This process's blocks lie end to end in the partitioned records
+        # (block key order, mode 0 most significant), so their visit orders are
+        # applied in ONE Fisher-Yates pass over the concatenation
+        # (sptk_fy_globalize): the visit entries are then relative to lo.
+        own = sorted((off, cnt) for items in self.rounds for (_, off, cnt) in items)
+        self.lo = own[0][0] if own else 0
+        self.hi = own[-1][0] + own[-1][1] if own else 0
+        contiguous = all(a[0] + a[1] == b[0] for a, b in zip(own, own[1:]))
+        import os
+
+        # (measured per-rank DSGD epochs, NF: batching pays from 16 blocks up)
+        min_fy = int(os.environ.get("SPTK_BATCHED_FY_MIN_BLOCKS", "16"))
+        self.batched_fy = contiguous and len(own) > 1 and len(own) >= min_fy
+        if self.batched_fy:
+            offs = np.array([o - self.lo for o, _ in own] + [self.hi - self.lo], dtype=np.int32)
+            self.fy_off = torch.from_numpy(offs).to(dev)
+        self.jstreams = None
+        import os
+
+        self.jstream_min_blocks = int(os.environ.get("SPTK_JSTREAM_MIN_BLOCKS", "32"))
         self.ws_j, self.ws_fy, self.ws_psi = Workspace(dev), Workspace(dev), Workspace(dev)
         self.ws_j.get(int(Lb.sptk_permutation_j_ws_bytes(max_block)))
-        self.ws_fy.get(int(Lb.sptk_fy_apply_ws_bytes(max_block)))
+        self.ws_fy.get(int(Lb.sptk_fy_apply_ws_bytes(self.hi - self.lo if self.batched_fy else max_block)))
         if config.update_core and self.k < self.nnz:
             self.ws_psi.get(int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
         self.acc = torch.zeros(max(self.dm.cor_size, 1), dtype=torch.float64, device=dev)
@@ -287,20 +307,50 @@ class EpochRunner:
     def draw_jseq(self, t: int, slot: int, stream) -> None:
         """Fisher-Yates j-sequences of every (own) block of epoch t:
         default_rng([seed,1,t,*block]).permutation(len(ids)), first half
-        (trainer.py:196-199)."""
+        (trainer.py:196-199).  With several blocks (DSGD) they are spread over
+        a few streams: each block's segment resolvers are serial single-warp
+        kernels, independent across blocks."""
         cfg = self.cfg
-        for items in self.rounds:
-            for block, off, cnt in items:
-                permutation_j(None, cnt, out=self.jbuf[slot][off:off + cnt], ws=self.ws_j,
-                              state=pcg64_state([cfg.seed, 1, t, *block]), stream=stream)
+        items = [it for rnd in self.rounds for it in rnd]
+        torch = self.torch
+        multi = len(items) >= self.jstream_min_blocks
+        if multi and self.jstreams is None:
+            k = min(8, len(items))
+            self.jstreams = [torch.cuda.Stream(device=self.dm.fac.device) for _ in range(k)]
+            self.ws_js = [self.ws_j] + [Workspace(self.dm.fac.device) for _ in range(k - 1)]
+            for w in self.ws_js[1:]:
+                w.get(self.ws_j.buf.numel())
+        if not multi:
+            streams, wss = [stream], [self.ws_j]
+        else:
+            start = torch.cuda.Event()
+            start.record(stream)
+            streams, wss = self.jstreams, self.ws_js
+            for st in streams:
+                st.wait_event(start)
+        for i, (block, off, cnt) in enumerate(items):
+            permutation_j(None, cnt, out=self.jbuf[slot][off:off + cnt], ws=wss[i % len(streams)],
+                          state=pcg64_state([cfg.seed, 1, t, *block]), stream=streams[i % len(streams)])
+        if multi:
+            for st in streams:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                stream.wait_event(ev)
         self.j_epoch[slot] = t
 
     def apply_jseq(self, t: int, slot: int, stream) -> None:
         """The visit orders of epoch t from its j-sequences (second half)."""
-        for items in self.rounds:
-            for block, off, cnt in items:
-                fy_apply(self.jbuf[slot][off:off + cnt], cnt, out=self.perm[slot][off:off + cnt], ws=self.ws_fy,
-                         stream=stream)
+        if self.batched_fy:
+            lo, hi = self.lo, self.hi
+            j = self.jbuf[slot][lo:hi]
+            check(self.L.sptk_fy_globalize(ptr(j), ptr(self.fy_off), self.fy_off.numel() - 1, stream_ptr(stream)),
+                  "sptk_fy_globalize")
+            fy_apply(j, hi - lo, out=self.perm[slot][lo:hi], ws=self.ws_fy, stream=stream)
+        else:
+            for items in self.rounds:
+                for block, off, cnt in items:
+                    fy_apply(self.jbuf[slot][off:off + cnt], cnt, out=self.perm[slot][off:off + cnt], ws=self.ws_fy,
+                             stream=stream)
         self.sampled_epoch[slot] = t
 
     def draw_samples(self, t: int, slot: int, stream) -> None:
@@ -397,7 +447,8 @@ class EpochRunner:
                     e0 = self.torch.cuda.Event(enable_timing=True)
                     e0.record()
                 rec, visit = self.part.rec, self.perm[slot][off:off + cnt]
-                check(fn(ptr(rec), self.part.rw, ptr(visit), cnt, off, ptr(dm.fac), dm.p_foff, ptr(dm.cor),
+                vbase = self.lo if self.batched_fy else off  # visit entries are relative to vbase
+                check(fn(ptr(rec), self.part.rw, ptr(visit), cnt, vbase, ptr(dm.fac), dm.p_foff, ptr(dm.cor),
                          dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam, self.mode, s),
                       "sptk_factor_pass")
                 if self.factor_events is not None:
