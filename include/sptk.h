@@ -100,6 +100,13 @@ int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, voi
  * permutation shifted by its offset (blocks touch disjoint positions).  One
  * apply per epoch instead of one per DSGD block. */
 int sptk_fy_globalize(int32_t* d_j, const int32_t* d_block_off, int n_blocks, void* stream);
+/* Batched first half: the j-sequences of n_blocks permutations (generator
+ * states h_states[4b..4b+3], sizes h_n[b]) into d_j + h_offsets[b], all
+ * blocks advancing segment level by segment level together (one launch per
+ * phase for the batch instead of per block: the DSGD blocks of a rank). */
+size_t sptk_permutation_j_batch_ws_bytes(const long long* h_n, int n_blocks);
+int sptk_permutation_j_batch(const uint64_t* h_states, const long long* h_n, const long long* h_offsets,
+                             int n_blocks, int32_t* d_j, void* d_ws, size_t ws_bytes, void* stream);
 size_t sptk_fy_apply_ws_bytes(long long n);
 int sptk_fy_apply(int32_t* d_j, long long n, int32_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
 size_t sptk_choice_ws_bytes(long long pop, long long k);

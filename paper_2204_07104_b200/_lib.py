@@ -38,6 +38,8 @@ SIGNATURES = {
     "sptk_permute_records": (ctypes.c_int, [_u64p, _i64, _vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "sptk_permutation_j_ws_bytes": (ctypes.c_size_t, [_i64]),
     "sptk_fy_apply_ws_bytes": (ctypes.c_size_t, [_i64]),
+    "sptk_permutation_j_batch_ws_bytes": (ctypes.c_size_t, [_i64p, ctypes.c_int]),
+    "sptk_permutation_j_batch": (ctypes.c_int, [_u64p, _i64p, _i64p, ctypes.c_int, _vp, _vp, ctypes.c_size_t, _vp]),
     "sptk_fy_globalize": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp]),
     "sptk_fy_apply": (ctypes.c_int, [_vp, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
     "sptk_permutation_j": (ctypes.c_int, [_u64p, _i64, _vp, _vp, ctypes.c_size_t, _vp]),

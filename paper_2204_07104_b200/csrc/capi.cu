@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <stdlib.h>
+
 namespace sptk {
 
 static thread_local char g_err[1024] = "";
@@ -163,6 +165,20 @@ int sptk_fy_apply(int32_t* d_j, long long n, int32_t* d_out, void* d_ws, size_t 
 
 int sptk_fy_globalize(int32_t* d_j, const int32_t* d_block_off, int n_blocks, void* stream) {
   return fy_globalize(d_j, d_block_off, n_blocks, (cudaStream_t)stream);
+}
+
+size_t sptk_permutation_j_batch_ws_bytes(const long long* h_n, int n_blocks) {
+  return jgen_batch_ws_bytes(h_n, n_blocks);
+}
+int sptk_permutation_j_batch(const uint64_t* h_states, const long long* h_n, const long long* h_offsets,
+                             int n_blocks, int32_t* d_j, void* d_ws, size_t ws_bytes, void* stream) {
+  if (n_blocks <= 0) return 0;
+  int** outs = (int**)malloc(sizeof(int*) * n_blocks);
+  if (!outs) return 2;
+  for (int b = 0; b < n_blocks; ++b) outs[b] = d_j + h_offsets[b];
+  int rc = permutation_j_batch(h_states, h_n, outs, n_blocks, d_ws, ws_bytes, (cudaStream_t)stream);
+  free(outs);
+  return rc;
 }
 
 int sptk_permutation_j(const uint64_t h_state[4], long long n, int32_t* d_j, void* d_ws, size_t ws_bytes,

@@ -11,6 +11,9 @@ namespace sptk {
 // sampler.cu
 size_t perm_ws_bytes(long long n);
 size_t jgen_ws_bytes(long long n);
+size_t jgen_batch_ws_bytes(const long long* n, int B);
+int permutation_j_batch(const uint64_t* st, const long long* n, int* const* j_out, int B, void* ws, size_t ws_bytes,
+                        cudaStream_t s);
 size_t fy_ws_bytes(long long n);
 int fy_apply_public(int* j, long long n, int* out, void* ws, size_t ws_bytes, cudaStream_t s);
 int fy_globalize(int* j, const int* off, int nb, cudaStream_t s);

@@ -38,6 +38,9 @@
 #include <math.h>
 #include <stdio.h>
 
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "pcg64.cuh"
@@ -170,12 +173,11 @@ __device__ __forceinline__ int guess_count(const Seg& sg, long long p) {
   return (int)r;
 }
 
-// Phase A: reference trajectory per chunk (one warp per chunk).
-__global__ void perm_phaseA_kernel(Pcg64 g, const long long* __restrict__ P, Seg sg, int L, int C,
-                                   int Delta, ChunkBuf cb) {
+// Phase A: reference trajectory per chunk (one warp per chunk c).
+__device__ void perm_phaseA_body(const Pcg64& g, const long long* __restrict__ P, const Seg& sg, int L, int C,
+                                 int Delta, const ChunkBuf& cb, int c) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= C) return;
   u128 A32, C32;
   pcg_jump_coeffs(g.inc, 32, &A32, &C32);
@@ -219,9 +221,9 @@ __global__ void perm_phaseA_kernel(Pcg64 g, const long long* __restrict__ P, Seg
 
 // Resolver: one warp propagates the exact count through the chunks.
 // meta[0] = index of the chunk holding the segment end; P[1] = next start.
-__global__ void perm_resolve_kernel(Pcg64 g, long long* __restrict__ P, Seg sg, int L, int C,
-                                    int Delta, ChunkBuf cb, int* __restrict__ meta) {
-  __shared__ int2 ent_s[32][PERM_E_DEV];
+__device__ void perm_resolve_body(const Pcg64& g, long long* __restrict__ P, const Seg& sg, int L, int C,
+                                  int Delta, const ChunkBuf& cb, int* __restrict__ meta,
+                                  int2 (*ent_s)[PERM_E_DEV]) {
   const int lane = threadIdx.x & 31;
   u128 A32, C32;
   pcg_jump_coeffs(g.inc, 32, &A32, &C32);
@@ -316,9 +318,8 @@ __global__ void perm_resolve_kernel(Pcg64 g, long long* __restrict__ P, Seg sg, 
 }
 
 // Phase B: regenerate each chunk from its exact count and write j.
-__global__ void perm_phaseB_kernel(Pcg64 g, const long long* __restrict__ P, Seg sg, int L, int C,
-                                   ChunkBuf cb, const int* __restrict__ meta, int* __restrict__ j_out) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ void perm_phaseB_body(const Pcg64& g, const long long* __restrict__ P, const Seg& sg, int L, int C,
+                                 const ChunkBuf& cb, const int* __restrict__ meta, int* __restrict__ j_out, int c) {
   const int c_end = meta[0];
   if (c >= C || c_end < 0 || c > c_end || P[0] < 0) return;
   u128 A32, C32;
@@ -328,8 +329,8 @@ __global__ void perm_phaseB_kernel(Pcg64 g, const long long* __restrict__ P, Seg
 }
 
 // Small segments k = kmax_small..1 walked by one warp.
-__global__ void perm_small_kernel(Pcg64 g, const long long* __restrict__ P, int kstart, long long n,
-                                  int* __restrict__ j_out, long long* __restrict__ q_final) {
+__device__ void perm_small_body(const Pcg64& g, const long long* __restrict__ P, int kstart, long long n,
+                                int* __restrict__ j_out, long long* __restrict__ q_final) {
   u128 A32, C32;
   pcg_jump_coeffs(g.inc, 32, &A32, &C32);
   long long q = P[0];
@@ -347,6 +348,64 @@ __global__ void perm_small_kernel(Pcg64 g, const long long* __restrict__ P, int 
   }
   if ((threadIdx.x & 31) == 0 && q_final) *q_final = q;
 }
+
+// ---- batched j-generation: several permutations (e.g. a rank's DSGD blocks)
+// advance segment level by segment level together, one launch per phase for
+// all of them (a single permutation is a batch of one).
+struct PermJob {
+  Pcg64 g;
+  long long* P;  // this block's start slot for the level
+  int* meta;
+  int* j_out;
+  Seg sg;
+  int L, C, Delta;
+  int chunk0;  // first chunk of this job in the level's chunk space
+  ChunkBuf cb;
+};
+struct SmallJob {
+  Pcg64 g;
+  long long* P;
+  int kstart;
+  long long n;
+  int* j_out;
+  long long* q_final;
+};
+
+__device__ __forceinline__ int find_job(const PermJob* __restrict__ jobs, int nj, int w) {
+  int lo = 0, hi = nj - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].chunk0 <= w) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void perm_phaseA_batched(const PermJob* __restrict__ jobs, int nj, int total) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= total) return;
+  const PermJob& jb = jobs[find_job(jobs, nj, w)];
+  perm_phaseA_body(jb.g, jb.P, jb.sg, jb.L, jb.C, jb.Delta, jb.cb, w - jb.chunk0);
+}
+
+__global__ void perm_resolve_batched(const PermJob* __restrict__ jobs) {
+  __shared__ int2 ent_s[32][PERM_E_DEV];
+  const PermJob& jb = jobs[blockIdx.x];
+  perm_resolve_body(jb.g, jb.P, jb.sg, jb.L, jb.C, jb.Delta, jb.cb, jb.meta, ent_s);
+}
+
+__global__ void perm_phaseB_batched(const PermJob* __restrict__ jobs, int nj, int total) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= total) return;
+  const PermJob& jb = jobs[find_job(jobs, nj, w)];
+  perm_phaseB_body(jb.g, jb.P, jb.sg, jb.L, jb.C, jb.cb, jb.meta, jb.j_out, w - jb.chunk0);
+}
+
+__global__ void perm_small_batched(const SmallJob* __restrict__ jobs) {
+  const SmallJob& jb = jobs[blockIdx.x];
+  perm_small_body(jb.g, jb.P, jb.kstart, jb.n, jb.j_out, jb.q_final);
+}
+
 
 // ---------------------------------------------------------------------------
 // (2) Lemire draw sequences (one CTA, one walking warp)
@@ -680,37 +739,16 @@ static const int PERM_E = 64;
 
 static size_t apply_ws_bytes(long long n);
 
+size_t jgen_batch_ws_bytes(const long long* n, int B);
+
 // workspace of the j-sequence generation alone (segment chunk summaries)
-size_t jgen_ws_bytes(long long n) {
-  size_t chunks = 0;
-  if (n >= 2) {
-    int kmax = 64 - __builtin_clzll((unsigned long long)(n - 1));
-    for (int k = kmax; k > K_SMALL; --k) {
-      SegPlan sp = plan_segment(n, k);
-      if ((size_t)sp.C > chunks) chunks = sp.C;
-    }
-  }
-  return 66 * sizeof(long long) + 66 * sizeof(int) + 2 * 256 + (chunks + 1) * (4 * sizeof(int) + PERM_E * sizeof(int2)) +
-         6 * 256;
-}
+size_t jgen_ws_bytes(long long n) { return jgen_batch_ws_bytes(&n, 1); }
 size_t fy_ws_bytes(long long n) { return apply_ws_bytes(n) + 256; }
 
 size_t perm_ws_bytes(long long n) {
-  // j-generation chunk buffers
-  size_t chunks = 0;
-  if (n >= 2) {
-    int kmax = 64 - __builtin_clzll((unsigned long long)(n - 1));
-    for (int k = kmax; k > K_SMALL; --k) {
-      SegPlan sp = plan_segment(n, k);
-      if ((size_t)sp.C > chunks) chunks = sp.C;
-    }
-  }
-  size_t b = 0;
-  b += 64 * sizeof(long long) + 64;            // P + meta
-  b += chunks * (4 * sizeof(int) + PERM_E * sizeof(int2)) + 256;
-  // j (n+1) + apply (values, ping-pong keys/values, parent, radix workspace)
-  b += (size_t)(n + 2) * sizeof(int) + apply_ws_bytes(n) + 16 * 256;
-  return b;
+  // P + meta of the caller, j (n+1), the j-generation and the apply
+  return 66 * sizeof(long long) + 66 * sizeof(int) + 2 * 256 + (size_t)(n + 2) * sizeof(int) + 256 +
+         jgen_ws_bytes(n) + apply_ws_bytes(n) + 16 * 256;
 }
 
 struct Carve {
@@ -732,15 +770,48 @@ struct Carve {
   bool ok() const { return !overflow; }
 };
 
-// j-sequence of Generator.permutation(n) into j_out[1..n-1]; j_out[0] = 0.
-int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* d_meta,
-              cudaStream_t s) {
-  if (n < 2) return 0;
-  int kmax = 64 - __builtin_clzll((unsigned long long)(n - 1));
+// j-sequences of B permutations: block b (n[b], generator st[4b..4b+3]) into
+// j_out[b][1..n[b]-1].  Segment levels run in lock step across blocks.
+static size_t jgen_batch_plan(const long long* n, int B, size_t* max_chunks, int* kmax_all) {
   size_t chunks = 0;
-  for (int k = kmax; k > K_SMALL; --k) {
-    SegPlan sp = plan_segment(n, k);
-    if ((size_t)sp.C > chunks) chunks = sp.C;
+  int km = 0;
+  for (int b = 0; b < B; ++b)
+    if (n[b] >= 2) km = std::max(km, 64 - __builtin_clzll((unsigned long long)(n[b] - 1)));
+  size_t njobs = 0;
+  for (int k = km; k > K_SMALL; --k) {
+    size_t lvl = 0;
+    for (int b = 0; b < B; ++b) {
+      if (n[b] < 2) continue;
+      const int kb = 64 - __builtin_clzll((unsigned long long)(n[b] - 1));
+      if (kb < k) continue;
+      lvl += plan_segment(n[b], k).C;
+      ++njobs;
+    }
+    chunks = std::max(chunks, lvl);
+  }
+  *max_chunks = chunks;
+  *kmax_all = km;
+  return njobs;
+}
+
+size_t jgen_batch_ws_bytes(const long long* n, int B) {
+  size_t chunks;
+  int km;
+  const size_t njobs = jgen_batch_plan(n, B, &chunks, &km);
+  return (size_t)B * (66 * sizeof(long long) + 66 * sizeof(int) + 2 * 256) +
+         (chunks + 1) * (4 * sizeof(int) + PERM_E * sizeof(int2)) + 6 * 256 + (njobs + 1) * sizeof(PermJob) +
+         (size_t)(B + 1) * sizeof(SmallJob) + 4 * 256;
+}
+
+int perm_jgen_batch(const Pcg64* g, const long long* n, int* const* j_out, int B, Carve& cv, cudaStream_t s) {
+  size_t chunks;
+  int km;
+  const size_t njobs = jgen_batch_plan(n, B, &chunks, &km);
+  std::vector<long long*> P(B);
+  std::vector<int*> meta(B);
+  for (int b = 0; b < B; ++b) {
+    P[b] = cv.take<long long>(66);
+    meta[b] = cv.take<int>(66);
   }
   ChunkBuf cb;
   cb.E = PERM_E;
@@ -749,27 +820,98 @@ int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* 
   cb.cnt = cv.take<int>(chunks + 1);
   cb.a_in = cv.take<int>(chunks + 1);
   cb.ent = cv.take<int2>((chunks + 1) * PERM_E);
+  PermJob* d_jobs = cv.take<PermJob>(njobs + 1);
+  SmallJob* d_small = cv.take<SmallJob>(B + 1);
   SPTK_REQUIRE(cv.ok(), "permutation: workspace too small");
-  SPTK_CUDA_TRY(cudaMemsetAsync(d_P, 0, sizeof(long long) * 66, s));
-  int k = kmax;
-  int slot = 0;  // d_P[slot] = start of segment k
-  for (; k > K_SMALL; --k, ++slot) {
-    SegPlan sp = plan_segment(n, k);
-    const int warps_per_block = 8;
-    unsigned blocks = (unsigned)((sp.C + warps_per_block - 1) / warps_per_block);
-    perm_phaseA_kernel<<<blocks, 32 * warps_per_block, 0, s>>>(g, d_P + slot, sp.sg, sp.L, sp.C,
-                                                               sp.Delta, cb);
+  std::vector<PermJob> jobs;
+  std::vector<int> lvl_begin, lvl_total;
+  jobs.reserve(njobs);
+  for (int k = km; k > K_SMALL; --k) {
+    lvl_begin.push_back((int)jobs.size());
+    int c0 = 0;
+    for (int b = 0; b < B; ++b) {
+      if (n[b] < 2) continue;
+      const int kb = 64 - __builtin_clzll((unsigned long long)(n[b] - 1));
+      if (kb < k) continue;
+      const SegPlan sp = plan_segment(n[b], k);
+      PermJob jb;
+      jb.g = g[b];
+      jb.P = P[b] + (kb - k);
+      jb.meta = meta[b] + (kb - k);
+      jb.j_out = j_out[b];
+      jb.sg = sp.sg;
+      jb.L = sp.L;
+      jb.C = sp.C;
+      jb.Delta = sp.Delta;
+      jb.chunk0 = c0;
+      jb.cb = cb;
+      jb.cb.a0 += c0;
+      jb.cb.D += c0;
+      jb.cb.cnt += c0;
+      jb.cb.a_in += c0;
+      jb.cb.ent += (long long)c0 * PERM_E;
+      c0 += sp.C;
+      jobs.push_back(jb);
+    }
+    lvl_total.push_back(c0);
+  }
+  lvl_begin.push_back((int)jobs.size());
+  std::vector<SmallJob> small;
+  for (int b = 0; b < B; ++b) {
+    if (n[b] < 2) continue;
+    const int kb = 64 - __builtin_clzll((unsigned long long)(n[b] - 1));
+    const int kst = kb > K_SMALL ? K_SMALL : kb;
+    SmallJob sj;
+    sj.g = g[b];
+    sj.P = P[b] + (kb - kst);
+    sj.kstart = kst;
+    sj.n = n[b];
+    sj.j_out = j_out[b];
+    sj.q_final = P[b] + 65;
+    small.push_back(sj);
+  }
+  for (int b = 0; b < B; ++b) SPTK_CUDA_TRY(cudaMemsetAsync(P[b], 0, sizeof(long long) * 66, s));
+  if (!jobs.empty())
+    SPTK_CUDA_TRY(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(PermJob) * jobs.size(), cudaMemcpyHostToDevice, s));
+  if (!small.empty())
+    SPTK_CUDA_TRY(cudaMemcpyAsync(d_small, small.data(), sizeof(SmallJob) * small.size(), cudaMemcpyHostToDevice, s));
+  const int warps_per_block = 8;
+  for (size_t l = 0; l + 1 < lvl_begin.size(); ++l) {
+    const int j0 = lvl_begin[l], nj = lvl_begin[l + 1] - j0, total = lvl_total[l];
+    if (nj == 0) continue;
+    const unsigned blocks = (unsigned)((total + warps_per_block - 1) / warps_per_block);
+    perm_phaseA_batched<<<blocks, 32 * warps_per_block, 0, s>>>(d_jobs + j0, nj, total);
     SPTK_CHECK_LAUNCH();
-    perm_resolve_kernel<<<1, 32, 0, s>>>(g, d_P + slot, sp.sg, sp.L, sp.C, sp.Delta, cb,
-                                         d_meta + slot);
+    perm_resolve_batched<<<nj, 32, 0, s>>>(d_jobs + j0);
     SPTK_CHECK_LAUNCH();
-    perm_phaseB_kernel<<<blocks, 32 * warps_per_block, 0, s>>>(g, d_P + slot, sp.sg, sp.L, sp.C,
-                                                               cb, d_meta + slot, j_out);
+    perm_phaseB_batched<<<blocks, 32 * warps_per_block, 0, s>>>(d_jobs + j0, nj, total);
     SPTK_CHECK_LAUNCH();
   }
-  perm_small_kernel<<<1, 32, 0, s>>>(g, d_P + slot, k, n, j_out, d_P + 65);
-  SPTK_CHECK_LAUNCH();
+  if (!small.empty()) {
+    perm_small_batched<<<(unsigned)small.size(), 32, 0, s>>>(d_small);
+    SPTK_CHECK_LAUNCH();
+  }
   return 0;
+}
+
+// j-sequence of Generator.permutation(n) into j_out[1..n-1]: a batch of one.
+int perm_jgen(Pcg64 g, long long n, int* j_out, Carve& cv, long long* d_P, int* d_meta, cudaStream_t s) {
+  (void)d_P;
+  (void)d_meta;
+  if (n < 2) return 0;
+  int* outs[1] = {j_out};
+  return perm_jgen_batch(&g, &n, outs, 1, cv, s);
+}
+
+int permutation_j_batch(const uint64_t* st, const long long* n, int* const* j_out, int B, void* ws, size_t ws_bytes,
+                        cudaStream_t s) {
+  SPTK_REQUIRE(B >= 0, "permutation_j_batch: bad batch");
+  for (int b = 0; b < B; ++b) SPTK_REQUIRE(n[b] >= 0 && n[b] < (1LL << 30), "permutation_j_batch: n out of range");
+  SPTK_REQUIRE(ws_bytes >= jgen_batch_ws_bytes(n, B), "permutation_j_batch: workspace too small");
+  std::vector<Pcg64> g(B);
+  for (int b = 0; b < B; ++b) g[b] = make_pcg(st + 4 * b);
+  Carve cv{(char*)ws, ws_bytes};
+  return perm_jgen_batch(g.data(), n, j_out, B, cv, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -87,6 +87,21 @@ def permutation_j(entropy, n: int, out=None, ws: Workspace | None = None, state=
     return out[:n]
 
 
+def permutation_j_batch(states, ns, offsets, out, ws: Workspace | None = None, stream=None):
+    """j-sequences of several permutations at once: block b (PCG64 state
+    states[b], size ns[b]) into out[offsets[b] : offsets[b] + ns[b]] (the
+    DSGD blocks of one process, one launch per segment phase for all)."""
+    _lib.require_cuda()
+    L = _lib.load()
+    st, sp = u64arr(np.asarray(states, dtype=np.uint64).reshape(-1))
+    nn, pn = _lib.i64arr(ns)
+    oo, po = _lib.i64arr(offsets)
+    w = (ws or Workspace()).get(int(L.sptk_permutation_j_batch_ws_bytes(pn, len(nn))))
+    check(L.sptk_permutation_j_batch(sp, pn, po, len(nn), ptr(out), ptr(w), w.numel(), stream_ptr(stream)),
+          "sptk_permutation_j_batch")
+    return out
+
+
 def fy_apply(j, n: int, out=None, ws: Workspace | None = None, stream=None):
     """Apply the Fisher-Yates sequence j (from ``permutation_j``; j[0] is
     overwritten) to the identity: the permutation itself."""

@@ -41,9 +41,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import check, f64arr, ptr, stream_ptr
+from ._lib import check, f64arr, i64arr, ptr, stream_ptr
 from .device import DeviceCoo, DeviceModel, rmse_mae_device
-from .sampler import Workspace, choice, fy_apply, pcg64_state, permutation_j
+from .sampler import Workspace, choice, fy_apply, pcg64_state, permutation_j, permutation_j_batch
 from .schedule import DevicePartition, round_schedule
 from .tensor import DatasetSplit, SparseTensorCoo
 from .tucker import TuckerModel
@@ -251,12 +251,12 @@ class EpochRunner:
         if self.batched_fy:
             offs = np.array([o - self.lo for o, _ in own] + [self.hi - self.lo], dtype=np.int32)
             self.fy_off = torch.from_numpy(offs).to(dev)
-        self.jstreams = None
-        import os
-
-        self.jstream_min_blocks = int(os.environ.get("SPTK_JSTREAM_MIN_BLOCKS", "32"))
         self.ws_j, self.ws_fy, self.ws_psi = Workspace(dev), Workspace(dev), Workspace(dev)
-        self.ws_j.get(int(Lb.sptk_permutation_j_ws_bytes(max_block)))
+        if sum(len(items) for items in self.rounds) > 1:
+            ns, _ = i64arr([c for items in self.rounds for (_, _, c) in items])
+            self.ws_j.get(int(Lb.sptk_permutation_j_batch_ws_bytes(_, len(ns))))
+        else:
+            self.ws_j.get(int(Lb.sptk_permutation_j_ws_bytes(max_block)))
         self.ws_fy.get(int(Lb.sptk_fy_apply_ws_bytes(self.hi - self.lo if self.batched_fy else max_block)))
         if config.update_core and self.k < self.nnz:
             self.ws_psi.get(int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
@@ -307,35 +307,18 @@ class EpochRunner:
     def draw_jseq(self, t: int, slot: int, stream) -> None:
         """Fisher-Yates j-sequences of every (own) block of epoch t:
         default_rng([seed,1,t,*block]).permutation(len(ids)), first half
-        (trainer.py:196-199).  With several blocks (DSGD) they are spread over
-        a few streams: each block's segment resolvers are serial single-warp
-        kernels, independent across blocks."""
+        (trainer.py:196-199).  Several blocks (DSGD) are drawn as one batch:
+        their segment levels advance together, one launch per phase."""
         cfg = self.cfg
         items = [it for rnd in self.rounds for it in rnd]
-        torch = self.torch
-        multi = len(items) >= self.jstream_min_blocks
-        if multi and self.jstreams is None:
-            k = min(8, len(items))
-            self.jstreams = [torch.cuda.Stream(device=self.dm.fac.device) for _ in range(k)]
-            self.ws_js = [self.ws_j] + [Workspace(self.dm.fac.device) for _ in range(k - 1)]
-            for w in self.ws_js[1:]:
-                w.get(self.ws_j.buf.numel())
-        if not multi:
-            streams, wss = [stream], [self.ws_j]
-        else:
-            start = torch.cuda.Event()
-            start.record(stream)
-            streams, wss = self.jstreams, self.ws_js
-            for st in streams:
-                st.wait_event(start)
-        for i, (block, off, cnt) in enumerate(items):
-            permutation_j(None, cnt, out=self.jbuf[slot][off:off + cnt], ws=wss[i % len(streams)],
-                          state=pcg64_state([cfg.seed, 1, t, *block]), stream=streams[i % len(streams)])
-        if multi:
-            for st in streams:
-                ev = torch.cuda.Event()
-                ev.record(st)
-                stream.wait_event(ev)
+        if len(items) == 1:
+            block, off, cnt = items[0]
+            permutation_j(None, cnt, out=self.jbuf[slot][off:off + cnt], ws=self.ws_j,
+                          state=pcg64_state([cfg.seed, 1, t, *block]), stream=stream)
+        elif items:
+            states = np.stack([pcg64_state([cfg.seed, 1, t, *block]) for block, _, _ in items])
+            permutation_j_batch(states, [c for _, _, c in items], [o for _, o, _ in items], self.jbuf[slot],
+                                ws=self.ws_j, stream=stream)
         self.j_epoch[slot] = t
 
     def apply_jseq(self, t: int, slot: int, stream) -> None:

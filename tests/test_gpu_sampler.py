@@ -155,3 +155,25 @@ def test_permute_records_netflix_size(golden_meta):
     p = out.view(-1, 4)[:, 0].cpu().numpy()
     assert p[:64].tolist() == g["head"] and p[-64:].tolist() == g["tail"]
     assert h32(p) == g["sha256_i32"]
+
+
+def test_permutation_j_batch_equals_per_block():
+    """The batched j-generation (a rank's DSGD blocks, segment levels in lock
+    step) gives every block exactly its own permutation's j-sequence, for
+    blocks of different sizes (including tiny and empty ones)."""
+    import torch
+
+    from paper_2204_07104_b200.sampler import pcg64_state, permutation_j_batch
+
+    ns = [193_001, 1, 0, 17, 5000, 262_145, 70_000, 193_777]
+    offs = np.concatenate([[0], np.cumsum(ns)[:-1]])
+    ents = [[1, 1, 0, b, 3] for b in range(len(ns))]
+    states = np.stack([pcg64_state(e) for e in ents])
+    out = torch.zeros(int(sum(ns)) + 1, dtype=torch.int32, device="cuda")
+    permutation_j_batch(states, ns, offs, out)
+    got = out.cpu().numpy()
+    for n, o, e in zip(ns, offs, ents):
+        if n < 2:
+            continue
+        _, want = O.permutation(e, n, return_j=True)
+        assert np.array_equal(got[o + 1:o + n], want[1:]), n
