@@ -36,6 +36,7 @@
 //      bucket partitions (by target, then by step) around per-bucket counting
 //      sorts, and chain walks guarded by an L2-resident has-parent bitmap.
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 
 #include <algorithm>
@@ -727,7 +728,11 @@ static SegPlan plan_segment(long long n, int k) {
   double bound = mean + 12.0 * sqrt(var) + 1024.0;
   sp.Delta = (int)ceil(4.0 * sqrt(mean) + 64.0);
   // ~24 near-margin entries per chunk (capacity PERM_E = 64)
-  double Lf = M * 24.0 / (2.0 * sp.Delta);
+  static const double target_entries = [] {
+    const char* e = getenv("SPTK_PERM_ENTRIES");
+    return e ? atof(e) : 24.0;
+  }();
+  double Lf = M * target_entries / (2.0 * sp.Delta);
   int L = 64;
   while (L * 2 <= Lf && L < 65536) L *= 2;
   sp.L = L;

@@ -31,7 +31,7 @@ for rep in range(2):
 L.sptk_debug_tc_buffer(None)
 s = st.view(16, 16).cpu().numpy()
 names = ["tile", "rows issued", "gather+sync", "cMMA issued", "cMMA done"] + \
-        [f"m{n}:{k}" for n in range(3) for k in ("W written", "W sync", "MMA done")] + ["pad", "end"]
+        [f"m{n}:{k}" for n in range(3) for k in ("W written", "W sync", "MMA done")] + ["m1:wb start", "end"]
 for t in range(2, 10):
     row = s[t]
     base = row[0]
