@@ -8,7 +8,8 @@ kernels behind the C ABI in include/sptk.h.
 
 from .sklearn_api import TuckerSGD, check_index_array, check_values
 from .synthetic import generate_large, generate_synthetic
-from .tensor import CooFormatError, DatasetSplit, SparseTensorCoo, load_coo, split, write_coo
+from .tensor import (CooFormatError, DatasetSplit, SparseTensorCoo, load_coo, load_coo_binary, split, write_coo,
+                     write_coo_binary)
 from .training import (
     METRICS_HEADER,
     MetricsRow,
@@ -29,6 +30,8 @@ from .tucker import (
     load_model,
     predict_entries,
     save_model,
+    save_model_binary,
+    load_model_binary,
 )
 
 __all__ = [
@@ -36,7 +39,8 @@ __all__ = [
     "write_coo", "TuckerSGD", "check_index_array", "check_values", "ModelConfig", "TuckerModel",
     "clone_model", "default_init_scale", "init_model", "load_model", "predict_entries", "save_model",
     "MetricsRow", "TrainConfig", "frobenius_objective", "learning_rate", "mae", "rmse", "train",
-    "write_metrics_csv", "generate_large", "METRICS_HEADER",
+    "write_metrics_csv", "generate_large", "METRICS_HEADER", "load_coo_binary", "write_coo_binary",
+    "save_model_binary", "load_model_binary",
 ]
 
 __version__ = "0.1.0"

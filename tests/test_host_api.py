@@ -122,3 +122,25 @@ def test_checkpoint_roundtrip(tmp_path):
     m2 = load_model(p)
     for a, b in zip(m.factors + m.core_factors, m2.factors + m2.core_factors):
         assert np.array_equal(a, b)
+
+
+def test_binary_coo_and_checkpoint_roundtrip(tmp_path):
+    """SURVEY 8f side formats: binary COO ingestion and binary checkpoints
+    round-trip exactly (memory-mapped load)."""
+    import numpy as np
+
+    from paper_2204_07104_b200 import (ModelConfig, SparseTensorCoo, init_model, load_coo_binary,
+                                       load_model_binary, save_model_binary, write_coo_binary)
+
+    rng = np.random.default_rng(3)
+    dims = (30, 40, 50)
+    t = SparseTensorCoo(dims, np.stack([rng.integers(0, d, 500) for d in dims], 1), rng.normal(size=500))
+    write_coo_binary(t, tmp_path / "t.npz")
+    u = load_coo_binary(tmp_path / "t.npz")
+    assert u.dims == dims and np.array_equal(u.indices, t.indices) and np.array_equal(u.values, t.values)
+    m = init_model(dims, ModelConfig((3, 4, 5), 2, 0.7, seed=4))
+    save_model_binary(m, tmp_path / "m.npz")
+    m2 = load_model_binary(tmp_path / "m.npz")
+    assert m2.dims == m.dims and m2.j_ranks == m.j_ranks and m2.r_core == m.r_core
+    for a, b in zip(m.factors + m.core_factors, m2.factors + m2.core_factors):
+        assert np.array_equal(a, b)
