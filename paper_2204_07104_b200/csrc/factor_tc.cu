@@ -32,6 +32,7 @@ struct TcParams {
   float* dbg;  // optional per-sample dump of the first tile (debug hook)
   unsigned atomic_mask;  // bit n: mode-n rows are written as red.add deltas (hot, small modes)
   int prefetch;          // v2: gather the next tile's rows during this tile (1) or at its start (0)
+  int defer_wb;          // v2: write mode n's rows back while mode n+1's MMA runs
 };
 
 static float* g_tc_debug = nullptr;
@@ -509,6 +510,27 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     }
   };
 
+  // Cooperative write-back of mode n's parked rows (new values, or deltas for
+  // red.add modes) from slot (n, pb): CH lanes per row, 16 bytes each.
+  auto flush_mode = [&](const RecReg<N, RW>& rr, int n, int pbs) {
+    const float* at = sm + a_off(n, pbs);
+    const bool red = p.atomic_mask >> n & 1u;
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int sl = k * RPI + crow;
+      const int row = __shfl_sync(0xffffffffu, rr.idx[n], sl);
+      const int ok = __shfl_sync(0xffffffffu, rr.valid ? 1 : 0, sl);
+      const float4 v = *reinterpret_cast<const float4*>(at + canon<128>(wbase + sl, 4 * cq));
+      float* dst = fac + p.foff[n] + (long long)row * J + 4 * cq;
+      if (ok) {
+        if (red)
+          tc::red_add_v4(dst, v);
+        else
+          tc::st_v4_hint(dst, v, pol_keep);
+      }
+    }
+  };
+
   // Software pipeline over this CTA's tiles: visit entries three tiles ahead,
   // records two ahead (registers), factor rows one ahead: the next tile's
   // mode-n rows are gathered (cp.async into the canonical A layout) as soon as
@@ -613,8 +635,10 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
         if (n < N - 1) issue_gemm<R, R, false>(tbase + J, a, 0, sbase + 4 * (C::OFF_G + n * R * R), 0, id_h);
         tc::mma_commit(&mbar);
       }
-      // every thread is past its mode n-1 update: that slot is free for the
-      // next tile's rows
+      // Deferred write-back of mode n-1 (parked before the barrier above): it
+      // runs while this mode's MMA executes.  Then that slot is free for the
+      // next tile's rows.
+      if (p.defer_wb && n >= 1) flush_mode(cur, n - 1, pb);
       if (n >= 1 && n - 1 < N - 1 && (pfm >> (n - 1) & 1u)) issue_mode(nxt, n - 1, 0);
       if (n == N - 1 && lpm) {
         // every thread is past modes 0..N-2 of this tile: their slots and the
@@ -662,20 +686,9 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
                        : make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
         *reinterpret_cast<float4*>(at + canon<128>(tid, 4 * q)) = v;
       }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < CH; ++k) {
-        const int sl = k * RPI + crow;
-        const int row = __shfl_sync(0xffffffffu, cur.idx[n], sl);
-        const int ok = __shfl_sync(0xffffffffu, cur.valid ? 1 : 0, sl);
-        const float4 v = *reinterpret_cast<const float4*>(at + canon<128>(wbase + sl, 4 * cq));
-        float* dst = fac + p.foff[n] + (long long)row * J + 4 * cq;
-        if (ok) {
-          if (red)
-            tc::red_add_v4(dst, v);
-          else
-            tc::st_v4_hint(dst, v, pol_keep);
-        }
+      if (!p.defer_wb || n == N - 1) {
+        __syncwarp();
+        flush_mode(cur, n, pb);
       }
       if (n < N - 1) {
         const float keep = 1.f - gm * lm, step = gm * (cur.x - inter);
@@ -1019,6 +1032,8 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   {
     const char* e = getenv("SPTK_TC_PREFETCH");
     p.prefetch = e ? atoi(e) : 1;
+    const char* d = getenv("SPTK_TC_DEFER_WB");
+    p.defer_wb = d ? atoi(d) : 0;
   }
   (void)rw;  // == rec_words(N), checked by try_factor_tc
   auto kfn = visit ? factor_tc2_kernel<N, J, R, true> : factor_tc2_kernel<N, J, R, false>;
