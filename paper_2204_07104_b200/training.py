@@ -164,6 +164,17 @@ def _dense_core(core_factors):
 AUTO_EXACT_MAX_NNZ = 1 << 22
 
 
+def _env_int(name: str, default: int) -> int:
+    """Integer tuning knob from the environment (performance only: results do
+    not depend on any of them)."""
+    import os
+
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
 def resolve_mode(update_mode: str, nnz: int) -> int:
     """libsptk factor-pass mode: 1 = exact, 0 = hogwild."""
     if update_mode in ("exact", "sequential"):
@@ -179,10 +190,15 @@ def resolve_mode(update_mode: str, nnz: int) -> int:
 class EpochRunner:
     """Device state for one training run on one GPU (workers = DSGD M).
 
-    Epochs are pipelined over two CUDA streams: while the main stream runs the
-    factor and core phases of epoch t, a side stream draws epoch t+1's visit
-    orders and core batch (they depend only on (seed, t), trainer.py:300/318)
-    into the other half of double-buffered sample arrays.
+    Samples depend only on (seed, t, block) (trainer.py:196-199, 213-220), so
+    they are drawn ahead on side streams while the main stream runs the factor
+    and core phases of epoch t: j-sequences two epochs ahead (``side_j``),
+    their application to visit orders one epoch ahead (``side``) and core
+    batches two epochs ahead (``side2``).
+
+    Tuning knobs (environment, read once): SPTK_FY_MAIN=1 applies visit orders
+    on the main stream instead; SPTK_BATCHED_FY_MIN_BLOCKS (16) is the block
+    count from which a process applies all its blocks' orders in one pass.
     """
 
     def __init__(self, model: TuckerModel, train_set: SparseTensorCoo, config: TrainConfig,
@@ -243,18 +259,16 @@ class EpochRunner:
         self.lo = own[0][0] if own else 0
         self.hi = own[-1][0] + own[-1][1] if own else 0
         contiguous = all(a[0] + a[1] == b[0] for a, b in zip(own, own[1:]))
-        import os
-
         # (measured per-rank DSGD epochs, NF: batching pays from 16 blocks up)
-        min_fy = int(os.environ.get("SPTK_BATCHED_FY_MIN_BLOCKS", "16"))
+        min_fy = _env_int("SPTK_BATCHED_FY_MIN_BLOCKS", 16)
         self.batched_fy = contiguous and len(own) > 1 and len(own) >= min_fy
         if self.batched_fy:
             offs = np.array([o - self.lo for o, _ in own] + [self.hi - self.lo], dtype=np.int32)
             self.fy_off = torch.from_numpy(offs).to(dev)
         self.ws_j, self.ws_fy, self.ws_psi = Workspace(dev), Workspace(dev), Workspace(dev)
         if sum(len(items) for items in self.rounds) > 1:
-            ns, _ = i64arr([c for items in self.rounds for (_, _, c) in items])
-            self.ws_j.get(int(Lb.sptk_permutation_j_batch_ws_bytes(_, len(ns))))
+            ns, p_ns = i64arr([c for items in self.rounds for (_, _, c) in items])
+            self.ws_j.get(int(Lb.sptk_permutation_j_batch_ws_bytes(p_ns, len(ns))))
         else:
             self.ws_j.get(int(Lb.sptk_permutation_j_ws_bytes(max_block)))
         self.ws_fy.get(int(Lb.sptk_fy_apply_ws_bytes(self.hi - self.lo if self.batched_fy else max_block)))
@@ -280,9 +294,7 @@ class EpochRunner:
         # apply is bandwidth-bound, so splitting them across epochs lets both
         # run underneath the factor pass instead of back to back.
         self.prefetch = prefetch
-        import os
-
-        self.fy_on_main = os.environ.get("SPTK_FY_MAIN", "0") == "1"
+        self.fy_on_main = _env_int("SPTK_FY_MAIN", 0) == 1
         mk = (lambda: torch.cuda.Stream(device=dev)) if prefetch else (lambda: None)
         self.side_j, self.side, self.side2 = mk(), mk(), mk()
         ev2 = lambda: [torch.cuda.Event(), torch.cuda.Event()]  # noqa: E731
