@@ -51,13 +51,26 @@ CONFIGS = {
                dims=(1_000_990, 624_961, 3_075, 133), nnz=250_272_286, n_test=2_502_723, J=16, R=16,
                alpha_a=0.001),
     "o6": dict(workload="6-order 10K^6, 1e9 nnz, J=R=8",
-               dims=(10_000,) * 6, nnz=1_000_000_000, n_test=1_000_000, J=8, R=8),
+               dims=(10_000,) * 6, nnz=1_000_000_000, n_test=1_000_000, J=8, R=8, alpha_a=0.003),
 }
 
 
 def bytes_per_nnz(order, J):
     """int32 indices + fp32 value, one read and one write of each row."""
     return 4 * (order + 1) + 8 * order * J
+
+
+def factor_kernel_name(order, J, R):
+    """The throughput factor kernel libsptk dispatches for this shape."""
+    if J != R:
+        return "factor_wps_kernel"
+    if J == 32 and order == 3:
+        return "factor_tc3_kernel"
+    if (order, J) in ((3, 4), (3, 8), (6, 8), (3, 16), (4, 16)):
+        return "factor_tc2_kernel"  # J = 4 on a zero-padded rank-8 model
+    if (order, J) in ((4, 4), (4, 8), (6, 4)):
+        return "factor_tps_kernel"
+    return "factor_wps_kernel"
 
 
 def factor_traffic(workload):
@@ -348,8 +361,7 @@ def bench_ours(args, cfg):
             "test_rmse": test_rmse,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": factor_traffic(cfg["workload"]),
-                         "kernel": "factor_tc2_kernel" if cfg["J"] == cfg["R"] and cfg["J"] in (16, 32)
-                         else "factor_tps_kernel",
+                         "kernel": factor_kernel_name(order, cfg["J"], cfg["R"]),
                          "kernel_ms": f_ms, "kernel_share": f_ms * launches_per_epoch / ms_per_step,
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
                          "frac_of_8TBs": achieved / 8000.0},
