@@ -51,7 +51,7 @@ CONFIGS = {
                dims=(1_000_990, 624_961, 3_075, 133), nnz=250_272_286, n_test=2_502_723, J=16, R=16,
                alpha_a=0.001),
     "o6": dict(workload="6-order 10K^6, 1e9 nnz, J=R=8",
-               dims=(10_000,) * 6, nnz=1_000_000_000, n_test=1_000_000, J=8, R=8, alpha_a=0.003),
+               dims=(10_000,) * 6, nnz=1_000_000_000, n_test=1_000_000, J=8, R=8, alpha_a=0.001),
 }
 
 
@@ -382,6 +382,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="nf", choices=sorted(CONFIGS))
     ap.add_argument("--rank", type=int, default=None, help="J = R override (rank sweep)")
+    ap.add_argument("--alpha-a", type=float, default=None, help="factor learning-rate override")
     ap.add_argument("--mode", default="hogwild", choices=["hogwild", "exact", "auto"])
     ap.add_argument("--e2e-epochs", type=int, default=None, help="default: --steps")
     ap.add_argument("--no-e2e", action="store_true")
@@ -393,6 +394,8 @@ def main():
         cfg["workload"] = cfg["workload"].split(", J=")[0] + f", J=R={args.rank}"
         if args.rank >= 32:
             cfg["alpha_a"] = 0.001
+    if args.alpha_a is not None:
+        cfg["alpha_a"] = args.alpha_a
     if args.impl == "reference":
         bench_reference(args, cfg)
     else:

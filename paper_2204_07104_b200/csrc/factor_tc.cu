@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   auto flush_mode = [&](const RecReg<N, RW>& rr, int n, int pbs) {
     const float* at = sm + a_off(n, pbs);
     const bool red = p.atomic_mask >> n & 1u;
+    if (red && (p.atomic_mask >> 31)) return;  // SPTK_DEBUG_DROP_HOT
 #pragma unroll
     for (int k = 0; k < CH; ++k) {
       const int sl = k * RPI + crow;
@@ -1032,6 +1033,9 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   {
     const char* e = getenv("SPTK_TC_PREFETCH");
     p.prefetch = e ? atoi(e) : 1;
+    // experiment hook (wrong results): drop the hot modes' row writes to
+    // measure what their L2 contention costs
+    if (getenv("SPTK_DEBUG_DROP_HOT")) p.atomic_mask |= 0x80000000u;
     const char* d = getenv("SPTK_TC_DEFER_WB");
     p.defer_wb = d ? atoi(d) : 0;
   }
