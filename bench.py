@@ -66,6 +66,8 @@ def factor_kernel_name(order, J, R):
         return "factor_wps_kernel"
     if J == 32 and order == 3:
         return "factor_tc3_kernel"
+    if J == 64 and order == 3:
+        return "factor_tc4_kernel"
     if (order, J) in ((3, 4), (3, 8), (6, 4), (6, 8), (3, 16), (4, 16)):
         return "factor_tc2_kernel"  # J = 4 on a zero-padded rank-8 model
     if (order, J) in ((4, 4), (4, 8)):

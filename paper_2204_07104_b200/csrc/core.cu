@@ -365,6 +365,195 @@ static int launch_core_tp(const int* rec, int rw, const int* visit, const int* m
   return 0;
 }
 
+// ----------------------------------------------------------------------------
+// Throughput K4 for uniform ranks too wide for a thread-per-sample register
+// tile (J = R = 64): core_wide_kernel<N,J,R,RW>.  256 threads, stages of 32
+// samples.
+//   phase 1: 8 threads per sample (a warp holds 4 samples); thread q gathers
+//     J/8 columns of each row into the stage, then computes c_n[s][r] for its
+//     R/8 columns against B in shared memory (row values are broadcast reads),
+//     the prediction by a fixed-order butterfly over the 8 threads, and
+//     v_n[s][r] = resid * prod_{n0!=n} c_n0[s][r] into the stage.
+//   phase 2 (as core_tp_kernel): thread owns N*(J/4)*(R/4)/256 4x4 tiles of
+//     sum_s a_n[s][j] v_n[s][r], accumulated in registers over the CTA's
+//     stages; one fp64-converted partial per CTA for the ordered reduce.
+// ----------------------------------------------------------------------------
+template <int N, int J, int R, int RW>
+__global__ void __launch_bounds__(256, 2)
+    core_wide_kernel(const int* __restrict__ rec, const int* __restrict__ visit, const int* __restrict__ map,
+                     long long n_visit, const float* __restrict__ fac, const float* __restrict__ cor, ModelDesc md,
+                     double* __restrict__ partial) {
+  constexpr int S = 32, TPS = 8, RQ = R / TPS, JQ = J / TPS;
+  constexpr int F = N * J + N * R, FP = F + 4;
+  constexpr int TJ = J / 4, TR = R / 4, TILES = N * TJ * TR, NT = (TILES + 255) / 256;
+  static_assert(RQ % 4 == 0 && JQ % 4 == 0, "core_wide: J, R multiples of 32");
+  extern __shared__ __align__(16) float smc[];
+  float* Bs = smc;                            // N*J*R, row-major B_n[j][r]
+  float* st = smc + ((N * J * R + 3) & ~3);  // S x FP
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int sl = (tid >> 5) * 4 + (lane >> 3), q = lane & 7;  // stage sample, column eighth
+  for (int i = tid; i < N * J * R; i += 256) Bs[i] = cor[i];
+  int pn[NT], pj[NT], pr[NT];
+  bool p2[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int ti = tid + t * 256;
+    p2[t] = ti < TILES;
+    const int tt = p2[t] ? ti : 0;
+    pn[t] = tt / (TJ * TR);
+    const int rem = tt % (TJ * TR);
+    pj[t] = 4 * (rem / TR);
+    pr[t] = 4 * (rem % TR);
+  }
+  float acc[NT][4][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[t][u][v] = 0.f;
+  __syncthreads();
+  float* row = st + sl * FP;
+  for (long long kb = (long long)blockIdx.x * S; kb < n_visit; kb += (long long)gridDim.x * S) {
+    const long long k = kb + sl;
+    const bool ok = k < n_visit;
+    float x = 0.f;
+    if (ok) {
+      const long long s = visit ? (long long)__ldg(visit + k) : k;
+      const long long ri = map ? (long long)__ldg(map + s) : s;
+      const int* rp = rec + ri * RW;
+      int wv[RW];
+      {
+        const int4 w0 = __ldg(reinterpret_cast<const int4*>(rp));
+        wv[0] = w0.x;
+        wv[1] = w0.y;
+        wv[2] = w0.z;
+        wv[3] = w0.w;
+        if (RW >= 8) {
+          const int4 w1 = __ldg(reinterpret_cast<const int4*>(rp) + 1);
+          wv[4 % RW] = w1.x;
+          wv[5 % RW] = w1.y;
+          wv[6 % RW] = w1.z;
+          wv[7 % RW] = w1.w;
+        }
+      }
+      x = __int_as_float(wv[N]);
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const float4* src = reinterpret_cast<const float4*>(fac + md.foff[n] + (long long)wv[n] * J + q * JQ);
+#pragma unroll
+        for (int u = 0; u < JQ / 4; ++u) *reinterpret_cast<float4*>(row + n * J + q * JQ + 4 * u) = __ldg(src + u);
+      }
+    } else {
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+#pragma unroll
+        for (int u = 0; u < JQ / 4; ++u)
+          *reinterpret_cast<float4*>(row + n * J + q * JQ + 4 * u) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    float c[N][RQ];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) c[n][r] = 0.f;
+#pragma unroll 8
+      for (int j = 0; j < J; ++j) {
+        const float a = row[n * J + j];
+#pragma unroll
+        for (int u = 0; u < RQ / 4; ++u) {
+          const float4 b = *reinterpret_cast<const float4*>(Bs + n * J * R + j * R + q * RQ + 4 * u);
+          c[n][4 * u] = fmaf(a, b.x, c[n][4 * u]);
+          c[n][4 * u + 1] = fmaf(a, b.y, c[n][4 * u + 1]);
+          c[n][4 * u + 2] = fmaf(a, b.z, c[n][4 * u + 2]);
+          c[n][4 * u + 3] = fmaf(a, b.w, c[n][4 * u + 3]);
+        }
+      }
+    }
+    float xhat = 0.f;
+#pragma unroll
+    for (int r = 0; r < RQ; ++r) {
+      float p = c[0][r];
+#pragma unroll
+      for (int n = 1; n < N; ++n) p *= c[n][r];
+      xhat += p;
+    }
+    xhat += __shfl_xor_sync(0xffffffffu, xhat, 1);
+    xhat += __shfl_xor_sync(0xffffffffu, xhat, 2);
+    xhat += __shfl_xor_sync(0xffffffffu, xhat, 4);
+    const float resid = ok ? xhat - x : 0.f;
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+      for (int u = 0; u < RQ / 4; ++u) {
+        float w4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float w = resid;
+#pragma unroll
+          for (int n0 = 0; n0 < N; ++n0)
+            if (n0 != n) w *= c[n0][4 * u + e];
+          w4[e] = w;
+        }
+        *reinterpret_cast<float4*>(row + N * J + n * R + q * RQ + 4 * u) = make_float4(w4[0], w4[1], w4[2], w4[3]);
+      }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      if (!p2[t]) continue;
+#pragma unroll 4
+      for (int s2 = 0; s2 < S; ++s2) {
+        const float* rr = st + s2 * FP;
+        const float4 a4 = *reinterpret_cast<const float4*>(rr + pn[t] * J + pj[t]);
+        const float4 v4 = *reinterpret_cast<const float4*>(rr + N * J + pn[t] * R + pr[t]);
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[t][u][v] = fmaf(av[u], vv[v], acc[t][u][v]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    if (!p2[t]) continue;
+    double* out = partial + (size_t)blockIdx.x * md.cor_size + md.coff[pn[t]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) out[(pj[t] + u) * R + pr[t] + v] = (double)acc[t][u][v];
+  }
+}
+
+template <int N, int J, int R>
+static int launch_core_wide(const int* rec, int rw, const int* visit, const int* map, long long n_visit,
+                            const float* fac, const float* cor, const ModelDesc& md, double* acc, void* ws,
+                            size_t ws_bytes, cudaStream_t s) {
+  constexpr int S = 32, F = N * J + N * R, FP = F + 4;
+  const size_t smem = sizeof(float) * (((N * J * R + 3) & ~3) + (size_t)S * FP);
+  constexpr int RW = N <= 3 ? 4 : 8;
+  (void)rw;
+  auto kfn = core_wide_kernel<N, J, R, RW>;
+  static bool configured = false;
+  if (!configured) {
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  int per_sm = (int)((226 * 1024) / (smem + 1024));
+  if (per_sm > 2) per_sm = 2;
+  if (per_sm < 1) per_sm = 1;
+  long long blocks = (n_visit + S - 1) / S;
+  if (blocks > 148LL * per_sm) blocks = 148LL * per_sm;
+  SPTK_REQUIRE(ws_bytes >= (size_t)blocks * md.cor_size * sizeof(double), "core_pass: workspace too small");
+  double* partial = (double*)ws;
+  kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, visit, map, n_visit, fac, cor, md, partial);
+  SPTK_CHECK_LAUNCH();
+  core_reduce_kernel<<<(md.cor_size + 7) / 8, 256, 0, s>>>(partial, (int)blocks, md.cor_size, acc);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
 // returns 1 if a specialised kernel handled the call
 static int try_core_tp(const int* rec, int rw, const int* visit, const int* map, long long n_visit,
                        const float* fac, const float* cor, const ModelDesc& md, double* acc, void* ws,
@@ -386,6 +575,10 @@ static int try_core_tp(const int* rec, int rw, const int* visit, const int* map,
   SPTK_CORE_CASE(4, 16)
   SPTK_CORE_CASE(6, 8)
 #undef SPTK_CORE_CASE
+  if (N == 3 && J == 64) {
+    *rc = launch_core_wide<3, 64, 64>(rec, rw, visit, map, n_visit, fac, cor, md, acc, ws, ws_bytes, s);
+    return 1;
+  }
   return 0;
 }
 

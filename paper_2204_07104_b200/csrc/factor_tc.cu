@@ -1066,8 +1066,296 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   return 0;
 }
 
+// ----------------------------------------------------------------------------
+// v4: J = R = 64 (the rank sweep's largest point).  At this rank the v2/v3
+// shared-memory plan does not fit (B_n in both K-major orientations is 96 KB
+// for N = 3, G_n would add 48 KB, the A tiles 96 KB), so the c_n refresh goes
+// back to an MMA on the updated A tile (c_n' = A_n' . B_n, v1 style), the last
+// mode's rows move to registers after the c round so W takes their slot, and
+// the plan is 194 KB: one CTA per SM, 512 threads, four threads per sample.
+// Warp w reads TMEM lane quadrant w % 4 (samples 32(w%4)..+31) and owns column
+// quarter w / 4 of every J- or R-vector (16 columns: c_n[16] x N, gs[16], a[16]
+// in registers).  inter = sum_r W_n[r] c_n[r] is summed from the four
+// quarters' partials across the barrier that precedes the gs MMA (fixed
+// order, so the four threads of a sample agree bit for bit).  Rows are
+// gathered per quarter (4 lanes per 64-byte quarter row) with cp.async and
+// written back straight from registers (plain stores, or red.add deltas for
+// the hot modes).  Tensor rounds per tile: c (N MMAs), then per mode gs and,
+// except for the last mode, the refresh: 2N rounds.
+// ----------------------------------------------------------------------------
+template <int N, int J, int R>
+struct Tc4Cfg {
+  static constexpr int M = 128;
+  static constexpr int OFF_BT = 0;                   // N x (R rows x J)
+  static constexpr int OFF_BN = OFF_BT + N * R * J;  // N x (J rows x R)
+  static constexpr int OFF_A = OFF_BN + N * J * R;   // N slots of 128 x J
+  static constexpr int OFF_W = OFF_A + (N - 1) * M * J;  // 128 x R: the last mode's A slot (see below)
+  static constexpr int OFF_X = OFF_A + N * M * J;    // 4 x 128 partial predictions
+  static constexpr int FLOATS = OFF_X + 4 * M;
+  static constexpr int NEED = N * R + J;             // c_0..c_{N-1}, gs
+  static constexpr int TCOLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
+};
+
+template <int N, int J, int R, bool HV>
+__global__ void __launch_bounds__(512, 1)
+    factor_tc4_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
+                      float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p,
+                      unsigned* __restrict__ tile_ctr) {
+  static_assert(J == R && J % 64 == 0, "v4 needs J == R, a multiple of 64");
+  constexpr int RW = N <= 3 ? 4 : (N <= 7 ? 8 : 16);
+  constexpr int Q = J / 4;  // columns per thread
+  using C = Tc4Cfg<N, J, R>;
+  extern __shared__ __align__(16) float sm[];
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qd = warp & 3, qq = warp >> 2, s = 32 * qd + lane;  // quadrant, column quarter, sample
+  const int c0 = qq * Q;                                         // first owned column
+
+  for (int e = tid; e < N * J * R; e += 512) {
+    const int n = e / (J * R), rem = e - n * (J * R), j = rem / R, r = rem - j * R;
+    const float b = __ldg(cor + e);
+    sm[C::OFF_BT + n * R * J + canon<R>(r, j)] = b;
+    sm[C::OFF_BN + n * J * R + canon<J>(j, r)] = b;
+  }
+  if (tid == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tslot, C::TCOLS);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = tslot;
+  const uint32_t tlane = tbase + ((uint32_t)(qd * 32) << 16);
+  const uint32_t tgs = N * R;  // gs columns
+  const uint32_t sbase = tc::smem_u32(sm);
+  const uint32_t id_c = tc::idesc_tf32(128, R), id_g = tc::idesc_tf32(128, J);
+  const uint64_t pol_keep = tc::policy_evict_last(), pol_stream = tc::policy_evict_first();
+  uint32_t phase = 0;
+
+  auto a_off = [&](int n) { return C::OFF_A + n * 128 * J; };
+  // this warp's quarter rows of its 32 samples: 4 lanes per quarter row (one
+  // 16-byte chunk each), 8 rows per instruction
+  constexpr int QCH = Q / 4, RPI = 32 / QCH;
+  const int cq = lane % QCH, crow = lane / QCH;
+  auto issue_mode = [&](const RecReg<N, RW>& rr, int n) {
+    const uint32_t dst = sbase + 4 * a_off(n);
+#pragma unroll
+    for (int k = 0; k < QCH; ++k) {
+      const int sl = k * RPI + crow;
+      const int row = __shfl_sync(0xffffffffu, rr.idx[n], sl);
+      const int ok = __shfl_sync(0xffffffffu, rr.valid ? 1 : 0, sl);
+      const float* src = fac + p.foff[n] + (long long)row * J + c0 + 4 * cq;
+      tc::cp_async16_nohint(dst + 4 * canon<128>(32 * qd + sl, c0 + 4 * cq), src, ok ? 16u : 0u);
+    }
+  };
+  auto mma_round_wait = [&]() {
+    tc::mbar_wait(&mbar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+  };
+
+  const long long G = gridDim.x;
+  uint32_t& s_claim = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 3);
+  long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
+  if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
+  RecReg<N, RW> cur, nxt;
+  auto vis = [&](long long t) -> int {
+    long long k = t * 128 + s;
+    k = k < n_visit ? k : n_visit - 1;
+    if (HV) return tc::ld_stream_s32(visit + k, pol_stream);
+    return (int)k;
+  };
+  auto valid_of = [&](long long t) { return t * 128 + s < n_visit; };
+  int v2 = vis(t2);
+  load_rec<N, RW>(cur, rec, vis(tile), valid_of(tile), base, pol_stream);
+  load_rec<N, RW>(nxt, rec, vis(t1), valid_of(t1), base, pol_stream);
+  __syncthreads();
+  long long t3 = 3 * G + s_claim;
+  float* px = sm + C::OFF_X;
+  float* wt = sm + C::OFF_W;
+  while (tile * 128 < n_visit) {
+    unsigned claim = 0;
+    if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
+#pragma unroll
+    for (int n = 0; n < N; ++n) issue_mode(cur, n);
+    tc::cp_async_commit();
+    RecReg<N, RW> nnxt;
+    load_rec<N, RW>(nnxt, rec, v2, valid_of(t2), base, pol_stream);
+    v2 = vis(t3);
+    tc::cp_async_wait_all();
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        issue_gemm<R, J, false>(tbase + n * R, sbase + 4 * a_off(n), 0, sbase + 4 * (C::OFF_BT + n * R * J), 0, id_c);
+      tc::mma_commit(&mbar);
+    }
+    mma_round_wait();
+    float c[N][Q];
+#pragma unroll
+    for (int n = 0; n < N; ++n) tc::tmem_ldh<Q>(tlane + n * R + c0, c[n]);
+    // The last mode's rows go to registers now: its slot then holds W (same
+    // canonical layout since J == R, so every thread overwrites exactly the
+    // entries it just read, and the c-round MMA that read them is complete).
+    float a_last[Q];
+#pragma unroll
+    for (int q = 0; q < Q / 4; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(sm + a_off(N - 1) + canon<128>(s, c0 + 4 * q));
+      a_last[4 * q] = v.x;
+      a_last[4 * q + 1] = v.y;
+      a_last[4 * q + 2] = v.z;
+      a_last[4 * q + 3] = v.w;
+    }
+
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      // W_n (my quarter) and my quarter of inter = sum_r W_n[r] c_n[r]
+      float part = 0.f;
+#pragma unroll
+      for (int q = 0; q < Q / 4; ++q) {
+        float w4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float w = 1.f;
+#pragma unroll
+          for (int n0 = 0; n0 < N; ++n0)
+            if (n0 != n) w *= c[n0][4 * q + u];
+          w4[u] = w;
+          part = fmaf(w, c[n][4 * q + u], part);
+        }
+        *reinterpret_cast<float4*>(wt + canon<128>(s, c0 + 4 * q)) = make_float4(w4[0], w4[1], w4[2], w4[3]);
+      }
+      px[qq * 128 + s] = part;
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        issue_gemm<J, R, false>(tbase + tgs, sbase + 4 * C::OFF_W, 0, sbase + 4 * (C::OFF_BN + n * J * R), 0, id_g);
+        tc::mma_commit(&mbar);
+      }
+      const float inter = ((px[s] + px[128 + s]) + px[256 + s]) + px[384 + s];
+      float* at = sm + a_off(n);
+      float a[Q];
+      if (n == N - 1) {
+#pragma unroll
+        for (int j = 0; j < Q; ++j) a[j] = a_last[j];
+      } else {
+#pragma unroll
+        for (int q = 0; q < Q / 4; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(at + canon<128>(s, c0 + 4 * q));
+          a[4 * q] = v.x;
+          a[4 * q + 1] = v.y;
+          a[4 * q + 2] = v.z;
+          a[4 * q + 3] = v.w;
+        }
+      }
+      mma_round_wait();
+      float g[Q];
+      tc::tmem_ldh<Q>(tlane + tgs + c0, g);
+      const float gm = p.gam[n], lm = p.lam[n];
+      const bool red = p.atomic_mask >> n & 1u;
+      float* dst = fac + p.foff[n] + (long long)cur.idx[n] * J + c0;
+#pragma unroll
+      for (int q = 0; q < Q / 4; ++q) {
+        float d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;
+          const float gr = -cur.x * g[j] + lm * a[j] + inter * g[j];
+          d[u] = -gm * gr;
+          a[j] += d[u];
+        }
+        if (cur.valid) {
+          if (red)
+            tc::red_add_v4(dst + 4 * q, make_float4(d[0], d[1], d[2], d[3]));
+          else
+            tc::st_v4_hint(dst + 4 * q, make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]), pol_keep);
+        }
+      }
+      if (n < N - 1) {
+        // refresh c_n from the updated rows: c_n' = A_n' . B_n
+#pragma unroll
+        for (int q = 0; q < Q / 4; ++q)
+          *reinterpret_cast<float4*>(at + canon<128>(s, c0 + 4 * q)) =
+              make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+        tc::fence_async_smem();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (tid == 0) {
+          tc::fence_after_sync();
+          issue_gemm<R, J, false>(tbase + n * R, sbase + 4 * a_off(n), 0, sbase + 4 * (C::OFF_BT + n * R * J), 0,
+                                  id_c);
+          tc::mma_commit(&mbar);
+        }
+        mma_round_wait();
+        tc::tmem_ldh<Q>(tlane + n * R + c0, c[n]);
+      }
+    }
+    cur = nxt;
+    nxt = nnxt;
+    tile = t1;
+    t1 = t2;
+    t2 = t3;
+    if (tid == 0) s_claim = claim;
+    tc::fence_before_sync();
+    __syncthreads();
+    t3 = 3 * G + s_claim;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tbase, C::TCOLS);
+  }
+}
+
+template <int N, int J, int R>
+static int launch_tc4(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                      const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+  using C = Tc4Cfg<N, J, R>;
+  TcParams<N> p;
+  for (int n = 0; n < N; ++n) {
+    p.foff[n] = md.foff[n];
+    p.gam[n] = gam[n];
+    p.lam[n] = lam[n];
+  }
+  p.dbg = nullptr;
+  p.atomic_mask = hot_mode_mask(md);
+  p.prefetch = 0;
+  p.defer_wb = 0;
+  (void)rw;
+  auto kfn = visit ? factor_tc4_kernel<N, J, R, true> : factor_tc4_kernel<N, J, R, false>;
+  static int configured = 0;
+  if (!configured) {
+    for (auto f : {factor_tc4_kernel<N, J, R, true>, factor_tc4_kernel<N, J, R, false>}) {
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    configured = 1;
+  }
+  long long tiles = (n_visit + 127) / 128;
+  long long blocks = 148;
+  if (blocks > tiles) blocks = tiles;
+  static unsigned slot = 0;
+  unsigned* ctr = nullptr;
+  SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tile_ctr));
+  ctr += (slot++ & 63u);
+  SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+  kfn<<<(unsigned)blocks, 512, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
 // 0 off (CUDA-core FMA kernel), 1 TF32 v2 (default), 2 TF32 v1, 3 3xTF32 v1,
-// 4 TF32 v3 (two threads per sample)
+// 4 TF32 v3 (two threads per sample); J = R = 64 always takes v4 when on
 static int g_tc_mode = -1;
 
 static int tc_mode_env() {
@@ -1140,6 +1428,10 @@ int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, l
   }
   SPTK_TC_CASE(3, 16)
   SPTK_TC_CASE(4, 16)
+  if (mode != 3 && N == 3 && J == 64) {  // (3xTF32 is not implemented for v4)
+    *rc = launch_tc4<3, 64, 64>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);
+    return 1;
+  }
   if (mode == 1 && N == 3 && J == 32) {
     // at J = R = 32 the one-thread-per-sample kernel needs ~250 registers (one
     // CTA per SM); two threads per sample is faster (NF: 37 vs 46 ms)

@@ -34,6 +34,7 @@ call signature working):
 from __future__ import annotations
 
 import math
+import os
 import time
 import warnings
 from dataclasses import dataclass
@@ -306,11 +307,18 @@ class EpochRunner:
         self.psi_slot = 0
         self.timeline = None  # set to [] to record per-epoch stream timelines (synchronises)
         self._marks = []
+        # experiment hook (wrong results): SPTK_EXP_SKIP=psi,jseq,perm re-uses a
+        # sampler stage's previous output instead of drawing it again, to measure
+        # what that stage's co-running costs the epoch
+        self._skip = set(filter(None, os.environ.get("SPTK_EXP_SKIP", "").split(",")))
 
     # -- samplers (K2) -----------------------------------------------------
     def draw_core_batch(self, t: int, stream) -> None:
         """Core batch Psi of epoch t (trainer.py:212-220) into psi[t % 3]."""
         cfg = self.cfg
+        if "psi" in self._skip and self.psi_epoch[t % 3] is not None:
+            self.psi_epoch[t % 3] = t
+            return
         if cfg.update_core and self.k < self.nnz:
             choice(None, self.nnz, self.k, shuffle=(self.mode == 1), out=self.psi[t % 3], ws=self.ws_psi,
                    state=pcg64_state([cfg.seed, 2, t]), stream=stream)
@@ -322,6 +330,9 @@ class EpochRunner:
         (trainer.py:196-199).  Several blocks (DSGD) are drawn as one batch:
         their segment levels advance together, one launch per phase."""
         cfg = self.cfg
+        if "jseq" in self._skip and self.j_epoch[slot] is not None:
+            self.j_epoch[slot] = t
+            return
         items = [it for rnd in self.rounds for it in rnd]
         if len(items) == 1:
             block, off, cnt = items[0]
@@ -335,6 +346,9 @@ class EpochRunner:
 
     def apply_jseq(self, t: int, slot: int, stream) -> None:
         """The visit orders of epoch t from its j-sequences (second half)."""
+        if "perm" in self._skip and self.sampled_epoch[slot] is not None:
+            self.sampled_epoch[slot] = t
+            return
         if self.batched_fy:
             lo, hi = self.lo, self.hi
             j = self.jbuf[slot][lo:hi]

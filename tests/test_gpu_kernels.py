@@ -193,6 +193,7 @@ def test_factor_seq_fp32_one_epoch(dims, J, R):
 @pytest.mark.parametrize("dims,J,R", [((4000, 4000, 4000), 4, 4), ((4000, 4000, 4000), 8, 8),
                                       ((4000, 4000, 4000), 16, 16), ((3000,) * 4, 16, 16),
                                       ((3000,) * 6, 8, 8), ((3000, 3000, 3000), 32, 32),
+                                      ((3000, 3000, 3000), 64, 64), ((300000, 3000, 3000), 64, 64),
                                       ((3000, 3000, 3000), 6, 5)])
 @pytest.mark.parametrize("tc", [0, 1, 2, 3, 4])
 def test_factor_hogwild_conflict_free_equals_sequential(dims, J, R, tc):
@@ -212,7 +213,7 @@ def test_factor_hogwild_conflict_free_equals_sequential(dims, J, R, tc):
 
 @pytest.mark.parametrize("dims,J", [((40, 50, 60), 4), ((300, 40, 30), 8), ((200, 300, 100), 16),
                                     ((50, 60, 70), 32), ((30, 40, 50, 60), 8), ((30, 40, 50, 60), 16),
-                                    ((20, 21, 22, 23, 24, 25), 8)])
+                                    ((20, 21, 22, 23, 24, 25), 8), ((50, 60, 70), 64)])
 @pytest.mark.parametrize("nnz,sub", [(5000, None), (3000, 777), (1, None)])
 def test_core_throughput_uniform_ranks(dims, J, nnz, sub):
     """Specialised K4 (uniform J = R, fp32, register-tiled outer products) vs
