@@ -438,7 +438,10 @@ __device__ __forceinline__ bool lemire_ok(uint32_t v, uint32_t rng, uint32_t* re
 #define LW_NB (LW_RING / LW_BLK)
 __global__ void __launch_bounds__(256) lemire_walk_kernel(const uint32_t* __restrict__ v, long long vcap, long long T,
                                                           long long base, int dir, uint32_t* __restrict__ out,
-                                                          long long* __restrict__ q_end_out, int* __restrict__ err) {
+                                                          long long* __restrict__ q_end_out, int* __restrict__ err,
+                                                          const int* __restrict__ only_if = nullptr) {
+  // only_if: fallback of the parallel walker (lp_*): run only if it failed
+  if (only_if && *only_if == 0) return;
   __shared__ uint32_t ring[LW_RING];
   __shared__ long long ready[LW_NB];
   __shared__ long long cons;
@@ -1448,6 +1451,219 @@ int fy_globalize(int* j, const int* off, int nb, cudaStream_t s) {
 }
 
 // --- choice ---------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Parallel Lemire walk (same contract as lemire_walk_kernel).  Draw t (bound
+// base + dir*t) consumes stream words until one is accepted, so the word
+// position of draw t is t + r_t, r_t = rejections before t.  The draws are cut
+// into chunks of LP_C; for chunk c the host predicts E[r] at its start from the
+// exact per-bound rejection probabilities (2^32 mod (rng+1)) / 2^32 and a
+// window of LP_W candidate offsets around it.  Pass 1 walks every (chunk,
+// candidate) pair and records the offset it exits with; pass 2 (one thread)
+// chains the true offsets through the chunks; pass 3 re-walks each chunk from
+// its true offset and writes the draws.  A true offset outside a window (or a
+// stream overflow) sets a flag and the sequential walker, launched after these
+// passes, redoes the whole walk; it returns at once otherwise.  Every chunk's
+// walk is the sequential algorithm itself, so the output is identical.
+// ---------------------------------------------------------------------------
+#define LP_C 4096
+struct LpPlan {
+  long long T, base, vcap;
+  int dir, nch, W;
+};
+
+__device__ __forceinline__ long long lp_walk(const uint32_t* __restrict__ v, long long vcap, long long t0,
+                                             long long t1, long long q, long long base, int dir,
+                                             uint32_t* __restrict__ out) {
+  // walk draws [t0, t1) from word q; returns the position after the last
+  // accepted word, or -1 on stream overflow
+  long long t = t0;
+  uint32_t rng = (uint32_t)(base + (long long)dir * t);
+  while (t < t1) {
+    if (q + 4 > vcap) {
+      for (; t < t1 && q < vcap; ++q) {
+        uint32_t r;
+        if (lemire_ok(__ldg(v + q), rng, &r)) {
+          if (out) out[t] = r;
+          ++t;
+          rng += (uint32_t)dir;
+        }
+      }
+      return t < t1 ? -1 : q;
+    }
+    uint32_t w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = __ldg(v + q + u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (t < t1) {
+        uint32_t r;
+        if (lemire_ok(w[u], rng, &r)) {
+          if (out) out[t] = r;
+          ++t;
+          rng += (uint32_t)dir;
+        }
+        ++q;
+      }
+    }
+  }
+  return q;
+}
+
+__global__ void __launch_bounds__(256) lp_exit_kernel(const uint32_t* __restrict__ v, LpPlan P,
+                                                      const int* __restrict__ lo, int* __restrict__ ex) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)P.nch * P.W) return;
+  const int c = (int)(i / P.W), w = (int)(i % P.W);
+  const long long r = (long long)lo[c] + w;
+  const long long t0 = (long long)c * LP_C, t1 = t0 + LP_C < P.T ? t0 + LP_C : P.T;
+  const long long q = lp_walk(v, P.vcap, t0, t1, t0 + r, P.base, P.dir, nullptr);
+  ex[i] = q < 0 ? INT_MIN : (int)(q - t1);
+}
+
+__global__ void lp_resolve_kernel(LpPlan P, const int* __restrict__ lo, const int* __restrict__ ex,
+                                  int* __restrict__ rc, long long* __restrict__ q_end_out, int* __restrict__ fail) {
+  if (threadIdx.x != 0) return;
+  long long r = 0;
+  for (int c = 0; c < P.nch; ++c) {
+    const long long w = r - lo[c];
+    if (w < 0 || w >= P.W) {
+      *fail = 1;
+      return;
+    }
+    rc[c] = (int)r;
+    const int e = ex[(long long)c * P.W + w];
+    if (e == INT_MIN) {
+      *fail = 1;
+      return;
+    }
+    r = e;
+  }
+  *q_end_out = P.T + r;
+  *fail = 0;
+}
+
+// pass 3: one warp per chunk, 32 consecutive draws tested per round against 32
+// consecutive words (the first rejecting lane ends the round, as in the
+// sequential walker)
+__global__ void __launch_bounds__(256) lp_emit_kernel(const uint32_t* __restrict__ v, LpPlan P,
+                                                      const int* __restrict__ rc, const int* __restrict__ fail,
+                                                      uint32_t* __restrict__ out) {
+  const int c = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (c >= P.nch || *fail) return;
+  const long long t0 = (long long)c * LP_C, t1 = t0 + LP_C < P.T ? t0 + LP_C : P.T;
+  long long t = t0, q = t0 + rc[c];
+  while (t < t1) {
+    if (q + 32 > P.vcap) {  // tail of the stream: finish this chunk on one lane
+      if (lane == 0) lp_walk(v, P.vcap, t, t1, q, P.base, P.dir, out);
+      return;
+    }
+    const uint32_t x = __ldg(v + q + lane);
+    const long long tt = t + lane;
+    uint32_t r = 0;
+    const bool ok = tt >= t1 || lemire_ok(x, (uint32_t)(P.base + (long long)P.dir * tt), &r);
+    const unsigned bal = __ballot_sync(0xffffffffu, !ok);
+    int nacc = bal ? __ffs(bal) - 1 : 32;
+    if (nacc > t1 - t) nacc = (int)(t1 - t);
+    if (lane < nacc) out[tt] = r;
+    t += nacc;
+    q += nacc + (bal ? 1 : 0);
+  }
+}
+
+static size_t lp_ws_bytes(long long T) {
+  const long long nch = (T + LP_C - 1) / LP_C;
+  return (size_t)nch * 4096 * 4 + (size_t)(nch + 1) * 8 + 8 * 256;
+}
+
+static double lp_p(long long rng) {  // P(reject) of one Lemire draw with bound rng (inclusive)
+  const unsigned long long ex = (unsigned long long)rng + 1ULL;
+  return (double)((1ULL << 32) % ex) / 4294967296.0;
+}
+
+// lo[c] = max(0, round(E[r at chunk c]) - W/2): expected rejections per chunk
+// from p/(1-p) sampled every 16 draws, then a block scan over the chunks
+__global__ void __launch_bounds__(1024) lp_plan_kernel(LpPlan P, int* __restrict__ lo) {
+  __shared__ double sc[1024];
+  const int c = threadIdx.x;
+  double e = 0.0;
+  if (c < P.nch) {
+    const long long t0 = (long long)c * LP_C, t1 = t0 + LP_C < P.T ? t0 + LP_C : P.T;
+    for (long long t = t0; t < t1; t += 16) {
+      const unsigned long long ex = (unsigned long long)(uint32_t)(P.base + (long long)P.dir * (t + 8)) + 1ULL;
+      const double p = (double)((1ULL << 32) % ex) / 4294967296.0;
+      const long long len = t + 16 < t1 ? 16 : t1 - t;
+      e += (double)len * p / (1.0 - p);
+    }
+  }
+  sc[c] = e;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const double y = c >= o ? sc[c - o] : 0.0;
+    __syncthreads();
+    sc[c] += y;
+    __syncthreads();
+  }
+  if (c < P.nch) {
+    const double before = c == 0 ? 0.0 : sc[c - 1];
+    const long long l = c == 0 ? 0 : llround(before) - P.W / 2;
+    lo[c] = (int)(l < 0 ? 0 : l);
+  }
+}
+
+// Lemire walk of T draws (bounds base + dir*t) over the pre-generated stream
+// v[0..vcap): out[t] = accepted draw, *d_qend = stream position after the
+// walk, *d_err = 3 on stream overflow.  Parallel for 2*LP_C <= T <= 1024*LP_C,
+// sequential otherwise (or with SPTK_LEMIRE_SERIAL=1).
+static int lemire_walk(const uint32_t* v, long long vcap, long long T, long long base, int dir, uint32_t* out,
+                       long long* d_qend, int* d_err, Carve& cv, cudaStream_t s) {
+  static int serial = -1;
+  if (serial < 0) {
+    const char* e = getenv("SPTK_LEMIRE_SERIAL");
+    serial = e && atoi(e) == 1;
+  }
+  const long long nch = (T + LP_C - 1) / LP_C;
+  int W = 0;
+  if (!serial && T >= 2 * LP_C && nch <= 1024) {
+    // spread of the rejection count (coarse sample of p(1-p) over the draws)
+    double var = 0.0;
+    const int NS = 1024;
+    for (int i = 0; i < NS; ++i) {
+      const long long t = (long long)((i + 0.5) * (double)T / NS);
+      const double p = lp_p((long long)(uint32_t)(base + (long long)dir * t));
+      var += p * (1.0 - p) * ((double)T / NS);
+    }
+    // +-4.5 sigma of the final rejection count (an offset outside its window
+    // only costs the sequential fallback)
+    const double half = 4.5 * sqrt(var) + 16.0;
+    W = (int)((2.0 * half + 63.0) / 64.0) * 64;
+    if (W > 4096) W = 0;
+    // test hook: a forced (too narrow) window exercises the sequential fallback
+    if (const char* e = getenv("SPTK_LP_W")) W = atoi(e);
+  }
+  if (W == 0) {
+    lemire_walk_kernel<<<1, 256, 0, s>>>(v, vcap, T, base, dir, out, d_qend, d_err);
+    SPTK_CHECK_LAUNCH();
+    return 0;
+  }
+  LpPlan P{T, base, vcap, dir, (int)nch, W};
+  int* lo = cv.take<int>(nch);
+  int* rc = cv.take<int>(nch + 1);
+  int* fail = cv.take<int>(1);
+  int* ex = cv.take<int>((size_t)nch * W);
+  SPTK_REQUIRE(cv.ok(), "sampler workspace too small (lemire walk)");
+  lp_plan_kernel<<<1, 1024, 0, s>>>(P, lo);
+  SPTK_CHECK_LAUNCH();
+  lp_exit_kernel<<<(unsigned)((nch * W + 255) / 256), 256, 0, s>>>(v, P, lo, ex);
+  SPTK_CHECK_LAUNCH();
+  lp_resolve_kernel<<<1, 32, 0, s>>>(P, lo, ex, rc, d_qend, fail);
+  SPTK_CHECK_LAUNCH();
+  lp_emit_kernel<<<(unsigned)((nch * 32 + 255) / 256), 256, 0, s>>>(v, P, rc, fail, out);
+  SPTK_CHECK_LAUNCH();
+  lemire_walk_kernel<<<1, 256, 0, s>>>(v, vcap, T, base, dir, out, d_qend, d_err, fail);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
 static long long lemire_vcap(long long T, double p_rej_max) {
   double mean = T * p_rej_max / (1.0 - p_rej_max);
   return T + (long long)(mean + 12.0 * sqrt(mean + 1.0) + 64.0) + 16 + 64;
@@ -1460,14 +1676,14 @@ size_t choice_ws_bytes(long long pop, long long k) {
     long long first = pop - k > 1 ? pop - k : 1;
     long long T = pop - first;
     b_tail = (size_t)(pop + 1) * 4 * 2 + (size_t)lemire_vcap(T > 0 ? T : 1, (double)pop / 4294967296.0) * 4 +
-             (size_t)(T + 1) * 4 + apply_ws_bytes(pop);
+             (size_t)(T + 1) * 4 + apply_ws_bytes(pop) + lp_ws_bytes(T > 0 ? T : 1);
   }
   {
     long long hs = 1;
     while (hs < 2 * k + 2) hs <<= 1;
     b_floyd = (size_t)(k + 1) * 4 * 3 + (size_t)lemire_vcap(k + 1, (double)pop / 4294967296.0) * 4 +
               (size_t)hs * 8 + (size_t)(k + 1) + (size_t)(k + 1) * 4 * 3 +
-              (size_t)lemire_vcap(k + 1, (double)k / 4294967296.0) * 4 + apply_ws_bytes(k);
+              (size_t)lemire_vcap(k + 1, (double)k / 4294967296.0) * 4 + apply_ws_bytes(k) + 2 * lp_ws_bytes(k + 1);
   }
   return pad + (b_tail > b_floyd ? b_tail : b_floyd);
 }
@@ -1491,8 +1707,7 @@ static int shuffle_int_jgen(Pcg64 g, long long q0, long long n, long long first,
   SPTK_REQUIRE(cv.ok(), "sampler workspace too small");
   u32_stream_kernel<<<grid_for(vcap, 256), 256, 0, s>>>(g, (unsigned long long)q0, vcap, v);
   SPTK_CHECK_LAUNCH();
-  lemire_walk_kernel<<<1, 256, 0, s>>>(v, vcap, T, n - 1, -1, tmp, d_qend, d_err);
-  SPTK_CHECK_LAUNCH();
+  if (lemire_walk(v, vcap, T, n - 1, -1, tmp, d_qend, d_err, cv, s)) return 1;
   reverse_into_kernel<<<grid_for(T, 256), 256, 0, s>>>(tmp, T, n, j);
   SPTK_CHECK_LAUNCH();
   return 0;
@@ -1537,8 +1752,7 @@ int choice(const uint64_t st[4], long long pop, long long k, int shuffle, int* o
   if (T > 0) {
     u32_stream_kernel<<<grid_for(vcap, 256), 256, 0, s>>>(g, 0ULL, vcap, v);
     SPTK_CHECK_LAUNCH();
-    lemire_walk_kernel<<<1, 256, 0, s>>>(v, vcap, T, base + t_begin, +1, vals + t_begin, d_q, d_err);
-    SPTK_CHECK_LAUNCH();
+    if (lemire_walk(v, vcap, T, base + t_begin, +1, vals + t_begin, d_q, d_err, cv, s)) return 1;
   } else {
     SPTK_CUDA_TRY(cudaMemsetAsync(d_q, 0, sizeof(long long), s));
   }

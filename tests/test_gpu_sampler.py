@@ -101,6 +101,31 @@ def test_choice_edge_cases():
         assert np.array_equal(got.cpu().numpy(), want), (pop, k)
 
 
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("pop,k", [(3_000_000, 60_000), (1_000_000, 500_000), (2_000_001, 40_000)])
+def test_choice_parallel_walk_vs_oracle(seed, pop, k):
+    """Draw counts where the chunked parallel Lemire walk runs (both choice paths,
+    and the _shuffle_int walk after Floyd): identical to the oracle."""
+    from paper_2204_07104_b200.sampler import choice
+
+    ent = [11, seed, pop, k]
+    got, _ = choice(ent, pop, k, shuffle=True)
+    want, _ = O.choice(ent, pop, k)
+    assert np.array_equal(got.cpu().numpy(), want)
+
+
+def test_choice_parallel_walk_fallback(monkeypatch):
+    """A window too narrow for the true rejection offsets makes the parallel
+    walk hand over to the sequential walker: same draws."""
+    from paper_2204_07104_b200.sampler import choice
+
+    ent = [11, 7, 3_000_000, 60_000]
+    want, _ = O.choice(ent, 3_000_000, 60_000)
+    monkeypatch.setenv("SPTK_LP_W", "1")
+    got, _ = choice(ent, 3_000_000, 60_000, shuffle=True)
+    assert np.array_equal(got.cpu().numpy(), want)
+
+
 def test_choice_netflix_core_batch(golden_meta):
     """Psi = choice(99,072,112, 2^20) of the bench (Floyd path), exact order and set."""
     from paper_2204_07104_b200.sampler import choice
