@@ -494,7 +494,11 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   // row (one 16-byte chunk each), so one cp.async instruction covers 32/CH
   // whole rows and L1 merges each row into a single L2 request.
   constexpr int CH = J / 4, RPI = 32 / CH;
-  const int lane = tid & 31, wbase = tid & ~31, cq = lane % CH, crow = lane / CH;
+  // (lane -> (row, chunk) with the row fastest: the 8 lanes of each quarter-warp
+  // then touch 8 consecutive canonical rows of one K chunk, 128 contiguous
+  // bytes, so a 16-byte shared access is one wavefront per quarter-warp
+  // instead of four; measured neutral on the NF epoch)
+  const int lane = tid & 31, wbase = tid & ~31, crow = lane % RPI, cq = lane / RPI;
   auto issue_mode = [&](const RecReg<N, RW>& rr, int n, int pb) {
     const uint32_t dst = sbase + 4 * a_off(n, pb);
     // no L2::cache_hint operand here: with it ptxas 12.9 pairs the global
@@ -793,7 +797,7 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
   // this warp's half-rows of its 32 samples: 2 lanes per row chunk pair
   // (H/4 chunks per half-row; H = 8 -> 2 chunks, 16 rows per instruction)
   constexpr int HCH = H / 4, RPI = 32 / HCH;
-  const int cq = lane % HCH, crow = lane / HCH;
+  const int crow = lane % RPI, cq = lane / RPI;  // row fastest (see v2)
   auto issue_mode = [&](const RecReg<N, RW>& rr, int n, int pb) {
     const uint32_t dst = sbase + 4 * a_off(n, pb);
 #pragma unroll
@@ -1140,7 +1144,7 @@ __global__ void __launch_bounds__(512, 1)
   // this warp's quarter rows of its 32 samples: 4 lanes per quarter row (one
   // 16-byte chunk each), 8 rows per instruction
   constexpr int QCH = Q / 4, RPI = 32 / QCH;
-  const int cq = lane % QCH, crow = lane / QCH;
+  const int crow = lane % RPI, cq = lane / RPI;  // row fastest (see v2)
   auto issue_mode = [&](const RecReg<N, RW>& rr, int n) {
     const uint32_t dst = sbase + 4 * a_off(n);
 #pragma unroll
