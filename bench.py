@@ -357,7 +357,8 @@ def bench_ours(args, cfg):
                     "model, std 4, noise 0.1)",
             "config": {"workload": cfg["workload"], "dims": list(cfg["dims"]), "nnz": cfg["nnz"],
                        "J": cfg["J"], "R": cfg["R"], "core_batch": min(cfg["nnz"], 1 << 20),
-                       "update_mode": args.mode, "parallelism": f"dsgd{world}" if world > 1 else "single",
+                       "update_mode": (args.mode if args.mode != "auto" else
+                                       "exact" if cfg["nnz"] <= (1 << 22) else "hogwild"), "parallelism": f"dsgd{world}" if world > 1 else "single",
                        "l2": "inputs larger than L2 (records + visit order ~2 GB per epoch); the 32 MB "
                              "model is L2-resident by design"},
             "test_rmse": test_rmse,
@@ -385,7 +386,9 @@ def main():
     ap.add_argument("--config", default="nf", choices=sorted(CONFIGS))
     ap.add_argument("--rank", type=int, default=None, help="J = R override (rank sweep)")
     ap.add_argument("--alpha-a", type=float, default=None, help="factor learning-rate override")
-    ap.add_argument("--mode", default="hogwild", choices=["hogwild", "exact", "auto"])
+    # auto = the library default: exact (sequential) up to 2^22 training
+    # nonzeros (cfg1), Hogwild above (NF, Y4, O6)
+    ap.add_argument("--mode", default="auto", choices=["hogwild", "exact", "auto"])
     ap.add_argument("--e2e-epochs", type=int, default=None, help="default: --steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -494,11 +494,10 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   // row (one 16-byte chunk each), so one cp.async instruction covers 32/CH
   // whole rows and L1 merges each row into a single L2 request.
   constexpr int CH = J / 4, RPI = 32 / CH;
-  // (lane -> (row, chunk) with the row fastest: the 8 lanes of each quarter-warp
-  // then touch 8 consecutive canonical rows of one K chunk, 128 contiguous
-  // bytes, so a 16-byte shared access is one wavefront per quarter-warp
-  // instead of four; measured neutral on the NF epoch)
-  const int lane = tid & 31, wbase = tid & ~31, crow = lane % RPI, cq = lane / RPI;
+  // (lane -> (row, chunk) with the chunk fastest.  The row-fastest mapping has
+  // 4x fewer shared wavefronts per access but measured 4% slower: ncu 11.95 ->
+  // 12.43 ms, more short-scoreboard stalls)
+  const int lane = tid & 31, wbase = tid & ~31, cq = lane % CH, crow = lane / CH;
   auto issue_mode = [&](const RecReg<N, RW>& rr, int n, int pb) {
     const uint32_t dst = sbase + 4 * a_off(n, pb);
     // no L2::cache_hint operand here: with it ptxas 12.9 pairs the global
@@ -797,7 +796,7 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
   // this warp's half-rows of its 32 samples: 2 lanes per row chunk pair
   // (H/4 chunks per half-row; H = 8 -> 2 chunks, 16 rows per instruction)
   constexpr int HCH = H / 4, RPI = 32 / HCH;
-  const int crow = lane % RPI, cq = lane / RPI;  // row fastest (see v2)
+  const int cq = lane % HCH, crow = lane / HCH;
   auto issue_mode = [&](const RecReg<N, RW>& rr, int n, int pb) {
     const uint32_t dst = sbase + 4 * a_off(n, pb);
 #pragma unroll
@@ -1085,7 +1084,10 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
 // gathered per quarter (4 lanes per 64-byte quarter row) with cp.async and
 // written back straight from registers (plain stores, or red.add deltas for
 // the hot modes).  Tensor rounds per tile: c (N MMAs), then per mode gs and,
-// except for the last mode, the refresh: 2N rounds.
+// except for the last mode, the refresh: 2N rounds.  (Gathering the next
+// tile's mode-0 rows during this tile, in a second slot with the partials
+// exchanged through TMEM instead of shared memory, measured no gain: 69.8 ms
+// either way on NF J = R = 64.)
 // ----------------------------------------------------------------------------
 template <int N, int J, int R>
 struct Tc4Cfg {
@@ -1144,7 +1146,7 @@ __global__ void __launch_bounds__(512, 1)
   // this warp's quarter rows of its 32 samples: 4 lanes per quarter row (one
   // 16-byte chunk each), 8 rows per instruction
   constexpr int QCH = Q / 4, RPI = 32 / QCH;
-  const int crow = lane % RPI, cq = lane / RPI;  // row fastest (see v2)
+  const int cq = lane % QCH, crow = lane / QCH;
   auto issue_mode = [&](const RecReg<N, RW>& rr, int n) {
     const uint32_t dst = sbase + 4 * a_off(n);
 #pragma unroll
