@@ -503,13 +503,17 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     // no L2::cache_hint operand here: with it ptxas 12.9 pairs the global
     // descriptor with an odd uniform register (desc[UR1]) in this loop, which
     // traps as an illegal instruction (the rows are L2-resident anyway)
+    // all row indices first (one shuffle per chunk: invalid samples carry
+    // -1), then the copies, so no copy waits on a shuffle issued after it
+    const int me = rr.valid ? rr.idx[n] : -1;
+    int row[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) row[k] = __shfl_sync(0xffffffffu, me, k * RPI + crow);
 #pragma unroll
     for (int k = 0; k < CH; ++k) {
       const int sl = k * RPI + crow;
-      const int row = __shfl_sync(0xffffffffu, rr.idx[n], sl);
-      const int ok = __shfl_sync(0xffffffffu, rr.valid ? 1 : 0, sl);
-      const float* src = fac + p.foff[n] + (long long)row * J + 4 * cq;
-      tc::cp_async16_nohint(dst + 4 * canon<128>(wbase + sl, 4 * cq), src, ok ? 16u : 0u);
+      const float* src = fac + p.foff[n] + (long long)(row[k] < 0 ? 0 : row[k]) * J + 4 * cq;
+      tc::cp_async16_nohint(dst + 4 * canon<128>(wbase + sl, 4 * cq), src, row[k] >= 0 ? 16u : 0u);
     }
   };
 
@@ -519,18 +523,22 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     const float* at = sm + a_off(n, pbs);
     const bool red = p.atomic_mask >> n & 1u;
     if (red && (p.atomic_mask >> 31)) return;  // SPTK_DEBUG_DROP_HOT
+    // shuffles and shared loads of every chunk first, then the stores
+    const int me = rr.valid ? rr.idx[n] : -1;
+    int row[CH];
+    float4 v[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) row[k] = __shfl_sync(0xffffffffu, me, k * RPI + crow);
+#pragma unroll
+    for (int k = 0; k < CH; ++k) v[k] = *reinterpret_cast<const float4*>(at + canon<128>(wbase + k * RPI + crow, 4 * cq));
 #pragma unroll
     for (int k = 0; k < CH; ++k) {
-      const int sl = k * RPI + crow;
-      const int row = __shfl_sync(0xffffffffu, rr.idx[n], sl);
-      const int ok = __shfl_sync(0xffffffffu, rr.valid ? 1 : 0, sl);
-      const float4 v = *reinterpret_cast<const float4*>(at + canon<128>(wbase + sl, 4 * cq));
-      float* dst = fac + p.foff[n] + (long long)row * J + 4 * cq;
-      if (ok) {
+      float* dst = fac + p.foff[n] + (long long)row[k] * J + 4 * cq;
+      if (row[k] >= 0) {
         if (red)
-          tc::red_add_v4(dst, v);
+          tc::red_add_v4(dst, v[k]);
         else
-          tc::st_v4_hint(dst, v, pol_keep);
+          tc::st_v4_hint(dst, v[k], pol_keep);
       }
     }
   };
