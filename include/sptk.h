@@ -118,6 +118,14 @@ int sptk_choice(const uint64_t h_state[4], long long pop, long long k, int shuff
 /* raw buffered 32-bit draws at stream positions q0..q0+n-1 (test hook). */
 int sptk_u32_stream(const uint64_t h_state[4], unsigned long long q0, long long n, uint32_t* d_out, void* stream);
 
+/* ---- host -> device upload of the input arrays ------------------------- */
+/* Synchronous copy of `bytes` from pageable host memory (the reference hands
+ * the COO tensor over as numpy arrays: SparseTensorCoo, coo.py:23-75) to
+ * device memory through pinned staging buffers filled by `threads` host
+ * threads (0: all hardware threads) with overlapped DMA.  The caller orders
+ * it against its streams (the copy runs on internal streams). */
+int sptk_h2d(void* d_dst, const void* h_src, size_t bytes, int threads);
+
 /* ---- K1: partition + device layout ------------------------------------ */
 size_t sptk_partition_ws_bytes(long long nnz, int order, long long m);
 /* d_idx int64 [nnz, order], d_vals f64 [nnz] -> d_rec (block-grouped records),

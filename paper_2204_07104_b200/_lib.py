@@ -47,6 +47,7 @@ SIGNATURES = {
     "sptk_choice": (ctypes.c_int, [_u64p, _i64, _i64, ctypes.c_int, _vp, _vp, ctypes.c_size_t,
                                    ctypes.POINTER(ctypes.c_int), _vp]),
     "sptk_u32_stream": (ctypes.c_int, [_u64p, ctypes.c_ulonglong, _i64, _vp, _vp]),
+    "sptk_h2d": (ctypes.c_int, [_vp, _vp, ctypes.c_size_t, ctypes.c_int]),
     "sptk_partition_ws_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int, _i64]),
     "sptk_partition": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, _i64p, _i64, ctypes.c_int, _vp, _vp,
                                       _vp, _vp, _vp, ctypes.c_size_t, _vp]),

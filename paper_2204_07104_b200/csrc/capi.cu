@@ -197,6 +197,10 @@ int sptk_u32_stream(const uint64_t h_state[4], unsigned long long q0, long long 
   return u32_stream(h_state, q0, n, d_out, (cudaStream_t)stream);
 }
 
+int sptk_h2d(void* d_dst, const void* h_src, size_t bytes, int threads) {
+  return h2d(d_dst, h_src, bytes, threads);
+}
+
 size_t sptk_partition_ws_bytes(long long nnz, int order, long long m) { return partition_ws_bytes(nnz, order, m); }
 
 int sptk_partition(const int64_t* d_idx, const double* d_vals, long long nnz, int order, const int64_t* h_dims,

@@ -7,6 +7,8 @@
 // read as warp-wide broadcasts, the record is one 16/32-byte load and each
 // factor row is read with vector loads.  Residual sums are accumulated in
 // fp64 (block reduction + one atomicAdd per block).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -88,11 +90,148 @@ __global__ void __launch_bounds__(256) eval_kernel(const int* __restrict__ rec, 
   }
 }
 
+// fp64 block reduction of (sq, ab) and one atomicAdd per block
+__device__ __forceinline__ void eval_block_sums(double sq, double ab, double* sums) {
+  for (int o = 16; o > 0; o >>= 1) {
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    ab += __shfl_xor_sync(0xffffffffu, ab, o);
+  }
+  __shared__ double red[2][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[0][w] = sq;
+    red[1][w] = ab;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    sq = lane < nw ? red[0][lane] : 0.0;
+    ab = lane < nw ? red[1][lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      ab += __shfl_xor_sync(0xffffffffu, ab, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&sums[0], sq);
+      atomicAdd(&sums[1], ab);
+    }
+  }
+}
+
+// fp32, uniform ranks J_n = R = J: every row of an entry is issued as J/4
+// 16-byte loads up front (N*J/4 independent loads in flight per thread), the
+// record of the next entry is loaded before this one is scored, and B(n) is
+// read from shared memory as float4 broadcasts (4 FMAs per load).
+template <int N, int J, int RW>
+__global__ void __launch_bounds__(256) eval_uniform_kernel(const int* __restrict__ rec, long long m,
+                                                           const float* __restrict__ fac,
+                                                           const float* __restrict__ cor, ModelDesc md,
+                                                           float* __restrict__ pred_out, double* __restrict__ sums) {
+  __shared__ __align__(16) float Bs[N * J * J];
+  for (int i = threadIdx.x; i < N * J * J; i += blockDim.x) Bs[i] = cor[i];
+  __syncthreads();
+  double sq = 0.0, ab = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int4 w0 = make_int4(0, 0, 0, 0), w1 = w0;
+  if (e < m) {
+    w0 = __ldg(reinterpret_cast<const int4*>(rec + e * RW));
+    if (RW >= 8) w1 = __ldg(reinterpret_cast<const int4*>(rec + e * RW) + 1);
+  }
+  for (; e < m; e += stride) {
+    const int wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    float4 row[N][J / 4];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float4* src = reinterpret_cast<const float4*>(fac + md.foff[n] + (long long)wv[n] * J);
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) row[n][q] = __ldg(src + q);
+    }
+    const float x = __int_as_float(wv[N]);
+    const long long en = e + stride;
+    if (en < m) {
+      w0 = __ldg(reinterpret_cast<const int4*>(rec + en * RW));
+      if (RW >= 8) w1 = __ldg(reinterpret_cast<const int4*>(rec + en * RW) + 1);
+    }
+    float prod[J];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      float c[J];
+#pragma unroll
+      for (int r = 0; r < J; ++r) c[r] = 0.f;
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) {
+        const float av[4] = {row[n][q].x, row[n][q].y, row[n][q].z, row[n][q].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;
+#pragma unroll
+          for (int r4 = 0; r4 < J / 4; ++r4) {
+            const float4 b = *reinterpret_cast<const float4*>(Bs + (n * J + j) * J + 4 * r4);
+            c[4 * r4] = fmaf(av[u], b.x, c[4 * r4]);
+            c[4 * r4 + 1] = fmaf(av[u], b.y, c[4 * r4 + 1]);
+            c[4 * r4 + 2] = fmaf(av[u], b.z, c[4 * r4 + 2]);
+            c[4 * r4 + 3] = fmaf(av[u], b.w, c[4 * r4 + 3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < J; ++r) prod[r] = n == 0 ? c[r] : prod[r] * c[r];
+    }
+    float xh = 0.f;
+#pragma unroll
+    for (int r = 0; r < J; ++r) xh += prod[r];
+    if (pred_out) pred_out[e] = xh;
+    const double d = (double)x - (double)xh;
+    sq += d * d;
+    ab += fabs(d);
+  }
+  if (sums) eval_block_sums(sq, ab, sums);
+}
+
+template <int N, int J>
+static int launch_eval_uniform(const int* rec, long long m, const float* fac, const float* cor, const ModelDesc& md,
+                               float* pred_out, double* sums, cudaStream_t s) {
+  constexpr int RW = N <= 3 ? 4 : 8;
+  long long blocks = (m + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  eval_uniform_kernel<N, J, RW><<<(unsigned)blocks, 256, 0, s>>>(rec, m, fac, cor, md, pred_out, sums);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// returns 1 if a specialised kernel handled the call
+static int try_eval_uniform(const int* rec, int rw, long long m, const float* fac, const float* cor,
+                            const ModelDesc& md, float* pred_out, double* sums, cudaStream_t s, int* rc) {
+  const int N = md.n_modes, J = md.jr[0];
+  for (int n = 1; n < N; ++n)
+    if (md.jr[n] != J) return 0;
+  if (J != md.rcore || rw != rec_words(N) || getenv("SPTK_EVAL_GENERIC")) return 0;
+#define SPTK_EVAL_U(NN, JJ)                                                          \
+  if (N == NN && J == JJ) {                                                          \
+    *rc = launch_eval_uniform<NN, JJ>(rec, m, fac, cor, md, pred_out, sums, s);     \
+    return 1;                                                                        \
+  }
+  SPTK_EVAL_U(3, 4)
+  SPTK_EVAL_U(3, 8)
+  SPTK_EVAL_U(3, 16)
+  SPTK_EVAL_U(4, 8)
+  SPTK_EVAL_U(4, 16)
+  SPTK_EVAL_U(6, 8)
+#undef SPTK_EVAL_U
+  return 0;
+}
+
 template <typename T>
 int eval(const int* rec, int rw, long long m, const T* fac, const T* cor, const ModelDesc& md, T* pred_out,
          double* sums, cudaStream_t s) {
   SPTK_REQUIRE(md.rcore >= 1 && md.rcore <= 64, "eval: rcore must be in [1, 64]");
   if (m <= 0) return 0;
+  if (sizeof(T) == 4) {
+    int rc = 0;
+    if (try_eval_uniform(rec, rw, m, (const float*)fac, (const float*)cor, md, (float*)pred_out, sums, s, &rc))
+      return rc;
+  }
   size_t smem = (size_t)md.cor_size * sizeof(T);
   SPTK_REQUIRE(smem <= 200 * 1024, "eval: core factors too large for shared memory");
   long long blocks = (m + 255) / 256;

@@ -30,6 +30,7 @@ size_t scan_ws_bytes(long long n);
 int exclusive_scan(const int* in, long long n, int* out, int* ws, cudaStream_t s);
 
 // partition.cu
+int h2d(void* dst, const void* src, size_t bytes, int threads);
 size_t partition_ws_bytes(long long nnz, int order, long long m);
 int partition(const long long* idx64, const double* vals64, long long nnz, int order, const long long* h_dims,
               long long m, int* rec_out, int* ids_out, int* pos_of_id_out, int* block_off_out, void* ws,

@@ -58,6 +58,21 @@ def key_to_block(key: int, m: int, order: int) -> tuple:
     return tuple(reversed(digits))
 
 
+def upload(a: np.ndarray):
+    """Host array -> new device tensor through sptk_h2d (threaded pinned
+    staging; the pageable copy runs at ~11 GB/s on the B200 hosts)."""
+    import torch
+
+    a = np.ascontiguousarray(a)
+    d = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device="cuda")
+    if a.nbytes:
+        # the copy runs on sptk's own streams: the (possibly recycled) block
+        # must be idle on the current stream first
+        torch.cuda.current_stream().synchronize()
+        check(_lib.load().sptk_h2d(ptr(d), a.ctypes.data, a.nbytes, 0), "sptk_h2d")
+    return d
+
+
 class DevicePartition:
     """Device records grouped by block + offsets (the output of K1)."""
 
@@ -79,8 +94,8 @@ class DevicePartition:
         self.ids = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) if want_ids else None
         self.pos_of_id = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
         self.block_off_dev = torch.empty(nkeys + 1, dtype=torch.int32, device=dev)
-        d_idx = torch.from_numpy(idx).to(dev)
-        d_val = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(dev)
+        d_idx = upload(idx)
+        d_val = upload(np.ascontiguousarray(values, dtype=np.float64))
         need = int(L.sptk_partition_ws_bytes(self.nnz, self.order, self.m))
         ws = torch.empty(need, dtype=torch.uint8, device=dev)
         dims_c, pd = i64arr(self.dims)

@@ -175,6 +175,25 @@ def _run_factor(idx, vals, fs, bs, visit, mode, f64, gam=0.01, lam=0.01, tc=1):
     return out, fac, foff, cor, coff, jr
 
 
+@pytest.mark.parametrize("dims,J", [((40, 50, 60), 4), ((300, 40, 30), 8), ((2000, 300, 100), 16),
+                                    ((30, 40, 50, 60), 8), ((30, 40, 50, 60), 16), ((20, 21, 22, 23, 24, 25), 8),
+                                    ((50, 60, 70), 32)])
+def test_eval_uniform_ranks_vs_oracle(dims, J):
+    """K6 specialised for uniform J = R (fp32) and the generic kernel: the
+    predictions of the oracle within fp32 rounding, RMSE/MAE sums likewise."""
+    from paper_2204_07104_b200 import TuckerModel
+    from paper_2204_07104_b200.device import DeviceCoo, DeviceModel, eval_sums, predict_device
+
+    idx, vals, fs, bs = _model_and_data(dims, (J,) * len(dims), J, 20001, 4)
+    model = TuckerModel(tuple(dims), (J,) * len(dims), J, fs, bs)
+    want = O.predict(fs, bs, idx)
+    got = predict_device(model, idx)
+    np.testing.assert_allclose(got, want, rtol=2e-5, atol=2e-5 * np.abs(want).max())
+    s = eval_sums(DeviceModel(model), DeviceCoo(idx, vals)).cpu().numpy()
+    d = vals - want
+    np.testing.assert_allclose(s, [np.sum(d * d), np.sum(np.abs(d))], rtol=1e-4)
+
+
 @pytest.mark.parametrize("dims,J,R", [((40, 50, 60), 4, 4), ((300, 40, 30), 8, 8), ((200, 300, 100), 16, 16),
                                       ((30, 40, 50, 60), 16, 16), ((20, 21, 22, 23, 24, 25), 8, 8),
                                       ((50, 60, 70), 32, 32), ((40, 50, 60), 5, 3)])
@@ -281,3 +300,15 @@ def test_rank4_zero_padding_is_exact():
     for n, d in enumerate(dims):
         rows = padded[dm.foff[n]: dm.foff[n + 1]].reshape(d, 8)
         assert not rows[:, J:].any()
+
+
+@pytest.mark.parametrize("nbytes,threads", [(1, 0), (4097, 3), (20_000_003, 0), (50 << 20, 5)])
+def test_h2d_upload_roundtrip(nbytes, threads):
+    """sptk_h2d (threaded pinned staging) delivers the host bytes unchanged."""
+    from paper_2204_07104_b200 import _lib
+
+    L = _lib.load()
+    src = np.random.default_rng(nbytes).integers(0, 256, nbytes, dtype=np.uint8)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    _lib.check(L.sptk_h2d(d.data_ptr(), src.ctypes.data, nbytes, threads), "h2d")
+    assert np.array_equal(d.cpu().numpy(), src)
