@@ -747,17 +747,23 @@ struct Tc3Cfg {
   static constexpr int OFF_BT = 0;
   static constexpr int OFF_BN = OFF_BT + N * R * J;
   static constexpr int OFF_G = OFF_BN + N * J * R;
-  static constexpr int OFF_A = OFF_G + N * R * R;        // N + 1 slots of 128 x J
-  static constexpr int OFF_W = OFF_A + (N + 1) * M * J;  // 128 x R
+  static constexpr int OFF_A = OFF_G + N * R * R;        // N slots of 128 x J
+  static constexpr int OFF_W = OFF_A + N * M * J;        // 128 x R
   static constexpr int OFF_X = OFF_W + M * R;            // 2 x 128 partial predictions
-  static constexpr int FLOATS = OFF_X + 2 * M;
+  static constexpr int OFF_BAR = OFF_X + 2 * M;          // mbarrier (2 words), TMEM slot, claim slot
+  // the last mode's second slot, only allocated when that mode is gathered a
+  // tile ahead (a cold mode); a hot last mode (NF) leaves it out, which lets
+  // two J = 32 CTAs share an SM
+  static constexpr int OFF_SPARE = OFF_BAR + 4;
+  static constexpr int FLOATS = OFF_SPARE;
   static constexpr int NEED = (N * R > J + R) ? N * R : J + R;
   static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
+  static constexpr size_t SMEM = (size_t)FLOATS * 4;
+  static constexpr size_t SMEM_SPARE = SMEM + (size_t)M * J * 4;
 };
 
 template <int N, int J, int R, bool HV>
-__global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
+__global__ void __launch_bounds__(256, (J <= 16 ? 3 : 2))
     factor_tc3_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
                       float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p,
                       unsigned* __restrict__ tile_ctr) {
@@ -766,8 +772,8 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
   constexpr int H = J / 2;  // columns per thread
   using C = Tc3Cfg<N, J, R>;
   extern __shared__ __align__(16) float sm[];
-  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
-  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 2);
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sm + C::OFF_BAR + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int qd = warp & 3, hf = warp >> 2, s = 32 * qd + lane;  // quadrant, column half, sample
   const int c0 = hf * H;                                         // first owned column
@@ -800,7 +806,7 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
   const uint64_t pol_keep = tc::policy_evict_last(), pol_stream = tc::policy_evict_first();
   uint32_t phase = 0;
 
-  auto a_off = [&](int n, int pb) { return C::OFF_A + (n < N - 1 ? n : N - 1 + pb) * 128 * J; };
+  auto a_off = [&](int n, int pb) { return n == N - 1 && pb ? C::OFF_SPARE : C::OFF_A + n * 128 * J; };
   // this warp's half-rows of its 32 samples: 2 lanes per row chunk pair
   // (H/4 chunks per half-row; H = 8 -> 2 chunks, 16 rows per instruction)
   constexpr int HCH = H / 4, RPI = 32 / HCH;
@@ -818,7 +824,7 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
   };
 
   const long long G = gridDim.x;
-  uint32_t& s_claim = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 3);
+  uint32_t& s_claim = *reinterpret_cast<uint32_t*>(sm + C::OFF_BAR + 3);
   long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
   if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
   RecReg<N, RW> cur, nxt;
@@ -835,6 +841,8 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
   load_rec<N, RW>(nxt, rec, vis(t1), valid_of(t1), base, pol_stream);
   int pb = 0;
   const unsigned pfm = p.prefetch == 0 ? 0u : p.prefetch == 2 ? ~0u : ~p.atomic_mask;
+  // the last mode alternates slots only when it is gathered a tile ahead
+  const int pbm = (pfm >> (N - 1) & 1u) ? 1 : 0;
 #pragma unroll
   for (int n = 0; n < N; ++n)
     if (pfm >> n & 1u) issue_mode(cur, n, pb);
@@ -907,11 +915,10 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
       tc::mbar_wait(&mbar, phase);
       phase ^= 1;
       tc::fence_after_sync();
-      float g[H], hv[H];
+      float g[H];
       tc::tmem_ldh<H>(tlane + c0, g);
-      if (n < N - 1) tc::tmem_ldh<H>(tlane + J + c0, hv);
       float* at = sm + a_off(n, pb);
-      float a[H], a0[H];
+      float a[H];
 #pragma unroll
       for (int q = 0; q < H / 4; ++q) {
         const float4 v = *reinterpret_cast<const float4*>(at + canon<128>(s, c0 + 4 * q));
@@ -921,17 +928,19 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
         a[4 * q + 3] = v.w;
       }
       const float gm = p.gam[n], lm = p.lam[n];
-#pragma unroll
-      for (int j = 0; j < H; ++j) {
-        a0[j] = a[j];
-        const float gr = -cur.x * g[j] + lm * a[j] + inter * g[j];
-        a[j] -= gm * gr;
-      }
       const bool red = p.atomic_mask >> n & 1u;
 #pragma unroll
       for (int q = 0; q < H / 4; ++q) {
-        const float4 v = red ? make_float4(a[4 * q] - a0[4 * q], a[4 * q + 1] - a0[4 * q + 1],
-                                           a[4 * q + 2] - a0[4 * q + 2], a[4 * q + 3] - a0[4 * q + 3])
+        float d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;
+          const float gr = -cur.x * g[j] + lm * a[j] + inter * g[j];
+          d[u] = -gm * gr;
+          a[j] += d[u];
+        }
+        // red.add modes park the delta, the others the new row
+        const float4 v = red ? make_float4(d[0], d[1], d[2], d[3])
                              : make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
         *reinterpret_cast<float4*>(at + canon<128>(s, c0 + 4 * q)) = v;
       }
@@ -951,6 +960,8 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
         }
       }
       if (n < N - 1) {
+        float hv[H];
+        tc::tmem_ldh<H>(tlane + J + c0, hv);
         const float keep = 1.f - gm * lm, step = gm * (cur.x - inter);
 #pragma unroll
         for (int r = 0; r < H; ++r) c[n][r] = fmaf(step, hv[r], keep * c[n][r]);
@@ -962,7 +973,7 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 1))
     tile = t1;
     t1 = t2;
     t2 = t3;
-    pb ^= 1;
+    pb ^= pbm;
     if (tid == 0) s_claim = claim;
     __syncthreads();
     t3 = 3 * G + s_claim;
@@ -994,18 +1005,20 @@ static int launch_tc3(const int* rec, int rw, const int* visit, long long n_visi
   }
   (void)rw;
   auto kfn = visit ? factor_tc3_kernel<N, J, R, true> : factor_tc3_kernel<N, J, R, false>;
-  static int configured = 0;
+  const unsigned pfm = p.prefetch == 0 ? 0u : p.prefetch == 2 ? ~0u : ~p.atomic_mask;
+  const size_t smem = (pfm >> (N - 1) & 1u) ? C::SMEM_SPARE : C::SMEM;
+  static size_t configured = 0;
   static int per_sm = 1;
-  if (!configured) {
+  if (configured != smem) {
     for (auto f : {factor_tc3_kernel<N, J, R, true>, factor_tc3_kernel<N, J, R, false>}) {
-      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_SPARE));
       SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
     cudaFuncAttributes fa;
     SPTK_CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)kfn));
     const int regs = fa.numRegs < 1 ? 1 : fa.numRegs;
     int by_regs = 65536 / (((regs * 32 + 255) / 256) * 256 * 8);
-    int by_smem = (int)((228 * 1024) / (C::SMEM + fa.sharedSizeBytes + 1024));
+    int by_smem = (int)((228 * 1024) / (smem + fa.sharedSizeBytes + 1024));
     int by_tmem = 512 / C::TCOLS;
     int n = by_regs < by_smem ? by_regs : by_smem;
     n = n < by_tmem ? n : by_tmem;
@@ -1013,8 +1026,8 @@ static int launch_tc3(const int* rec, int rw, const int* visit, long long n_visi
     if (const char* e = getenv("SPTK_TC_CTAS")) cap = atoi(e);
     if (cap >= 1 && cap < n) n = cap;
     per_sm = n < 1 ? 1 : n;
-    if (getenv("SPTK_DEBUG")) fprintf(stderr, "[sptk] tc3 regs=%d smem=%zu -> %d CTAs/SM\n", regs, C::SMEM, per_sm);
-    configured = 1;
+    if (getenv("SPTK_DEBUG")) fprintf(stderr, "[sptk] tc3 regs=%d smem=%zu -> %d CTAs/SM\n", regs, smem, per_sm);
+    configured = smem;
   }
   long long tiles = (n_visit + 127) / 128;
   long long blocks = 148LL * per_sm;
@@ -1024,7 +1037,7 @@ static int launch_tc3(const int* rec, int rw, const int* visit, long long n_visi
   SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tile_ctr));
   ctr += (slot++ & 63u);
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
-  kfn<<<(unsigned)blocks, 256, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
+  kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
   SPTK_CHECK_LAUNCH();
   return 0;
 }

@@ -296,6 +296,7 @@ class EpochRunner:
         # run underneath the factor pass instead of back to back.
         self.prefetch = prefetch
         self.fy_on_main = _env_int("SPTK_FY_MAIN", 0) == 1
+        self.burst = prefetch and os.environ.get("SPTK_SCHED", "overlap") == "burst"
         # stream priorities (SPTK_PRIO="j,apply,psi", lower = higher priority).
         # The Fisher-Yates apply bounds the epoch when it shares the GPU with
         # the factor pass; giving it priority measured slower on the NF bench
@@ -429,6 +430,18 @@ class EpochRunner:
             self.draw_jseq(t + 2, slot, self.side_j)
             self._mark("jseq2_end", self.side_j)
             self.j_ready[slot].record(self.side_j)
+        if self.burst:
+            # burst schedule (SPTK_SCHED=burst, with SPTK_TC_CTAS=4): this
+            # epoch's factor pass starts once the sampler stages just enqueued
+            # (apply t+1, j-sequences and core batch t+2) are done; they run
+            # side by side, then the factor pass has every CTA slot.  Measured
+            # 21.1 vs 19.1 ms per NF epoch: the latency-bound j-sequence levels
+            # take ~10 ms beside the apply, so the default overlaps them with
+            # the factor pass instead.
+            for st in (self.side, self.side_j, self.side2):
+                ev = torch.cuda.Event()
+                ev.record(st)
+                main.wait_event(ev)
         return slot
 
     # -- optional per-epoch stream timeline (timeline = [] to enable) --------
