@@ -1514,6 +1514,7 @@ __global__ void __launch_bounds__(256) lp_exit_kernel(const uint32_t* __restrict
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= (long long)P.nch * P.W) return;
   const int c = (int)(i / P.W), w = (int)(i % P.W);
+  if (w >= lo[P.nch + c]) return;  // beyond this chunk's window
   const long long r = (long long)lo[c] + w;
   const long long t0 = (long long)c * LP_C, t1 = t0 + LP_C < P.T ? t0 + LP_C : P.T;
   const long long q = lp_walk(v, P.vcap, t0, t1, t0 + r, P.base, P.dir, nullptr);
@@ -1526,7 +1527,7 @@ __global__ void lp_resolve_kernel(LpPlan P, const int* __restrict__ lo, const in
   long long r = 0;
   for (int c = 0; c < P.nch; ++c) {
     const long long w = r - lo[c];
-    if (w < 0 || w >= P.W) {
+    if (w < 0 || w >= lo[P.nch + c]) {
       *fail = 1;
       return;
     }
@@ -1572,7 +1573,7 @@ __global__ void __launch_bounds__(256) lp_emit_kernel(const uint32_t* __restrict
 
 static size_t lp_ws_bytes(long long T) {
   const long long nch = (T + LP_C - 1) / LP_C;
-  return (size_t)nch * 4096 * 4 + (size_t)(nch + 1) * 8 + 8 * 256;
+  return (size_t)nch * 4096 * 4 + (size_t)(nch + 1) * 16 + 8 * 256;
 }
 
 static double lp_p(long long rng) {  // P(reject) of one Lemire draw with bound rng (inclusive)
@@ -1580,12 +1581,14 @@ static double lp_p(long long rng) {  // P(reject) of one Lemire draw with bound 
   return (double)((1ULL << 32) % ex) / 4294967296.0;
 }
 
-// lo[c] = max(0, round(E[r at chunk c]) - W/2): expected rejections per chunk
-// from p/(1-p) sampled every 16 draws, then a block scan over the chunks
+// Per chunk c: lo[c] = max(0, round(E[r]) - W_c/2) and lo[nch + c] = W_c, the
+// window width for +-4.5 sigma of the offset at the chunk start (both from
+// p/(1-p) and p(1-p) sampled every 16 draws and block-scanned over the
+// chunks), at most P.W, so early chunks walk fewer candidates
 __global__ void __launch_bounds__(1024) lp_plan_kernel(LpPlan P, int* __restrict__ lo) {
-  __shared__ double sc[1024];
+  __shared__ double sc[1024], sv[1024];
   const int c = threadIdx.x;
-  double e = 0.0;
+  double e = 0.0, var = 0.0;
   if (c < P.nch) {
     const long long t0 = (long long)c * LP_C, t1 = t0 + LP_C < P.T ? t0 + LP_C : P.T;
     for (long long t = t0; t < t1; t += 16) {
@@ -1593,20 +1596,26 @@ __global__ void __launch_bounds__(1024) lp_plan_kernel(LpPlan P, int* __restrict
       const double p = (double)((1ULL << 32) % ex) / 4294967296.0;
       const long long len = t + 16 < t1 ? 16 : t1 - t;
       e += (double)len * p / (1.0 - p);
+      var += (double)len * p * (1.0 - p);
     }
   }
   sc[c] = e;
+  sv[c] = var;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {
-    const double y = c >= o ? sc[c - o] : 0.0;
+    const double y = c >= o ? sc[c - o] : 0.0, yv = c >= o ? sv[c - o] : 0.0;
     __syncthreads();
     sc[c] += y;
+    sv[c] += yv;
     __syncthreads();
   }
   if (c < P.nch) {
-    const double before = c == 0 ? 0.0 : sc[c - 1];
-    const long long l = c == 0 ? 0 : llround(before) - P.W / 2;
+    const double before = c == 0 ? 0.0 : sc[c - 1], vb = c == 0 ? 0.0 : sv[c - 1];
+    int w = c == 0 ? 1 : (int)((2.0 * (4.5 * sqrt(vb) + 16.0) + 63.0) / 64.0) * 64;
+    if (w > P.W) w = P.W;
+    const long long l = c == 0 ? 0 : llround(before) - w / 2;
     lo[c] = (int)(l < 0 ? 0 : l);
+    lo[P.nch + c] = w;
   }
 }
 
@@ -1646,7 +1655,7 @@ static int lemire_walk(const uint32_t* v, long long vcap, long long T, long long
     return 0;
   }
   LpPlan P{T, base, vcap, dir, (int)nch, W};
-  int* lo = cv.take<int>(nch);
+  int* lo = cv.take<int>(2 * nch);
   int* rc = cv.take<int>(nch + 1);
   int* fail = cv.take<int>(1);
   int* ex = cv.take<int>((size_t)nch * W);

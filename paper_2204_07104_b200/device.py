@@ -70,8 +70,9 @@ class DeviceModel:
         self._jr, self.p_jr = i64arr(self.jr)
 
     def download_into(self, model) -> None:
-        fac = self.fac.double().cpu().numpy()
-        cor = self.cor.double().cpu().numpy()
+        # device dtype over the bus (fp32: half the bytes), widened by copyto
+        fac = self.fac.cpu().numpy()
+        cor = self.cor.cpu().numpy()
         for n, a in enumerate(model.factors):
             full = fac[self.foff[n]: self.foff[n + 1]].reshape(a.shape[0], int(self.jr[n]))
             np.copyto(a, full[:, : a.shape[1]])
