@@ -149,6 +149,143 @@ __global__ void __launch_bounds__(128, (J <= 4 ? 6 : (N * J <= 24 ? 5 : (J <= 8 
 }
 
 // ----------------------------------------------------------------------------
+// factor_fma_kernel<N,J>: thread per sample on the CUDA cores (J = R), the
+// tcgen05 kernels' Hogwild semantics (hot modes written as red.add deltas)
+// with no tensor rounds or barriers: every thread runs its own sample's
+// whole chain, so the SM's warps are independent.  B(n) sits in shared
+// memory row-major (J x R) and is read as float4 broadcasts (4 FMAs per
+// load); per sample (3N-1) J R FMAs (the c_n refresh recomputed from the
+// updated row).  Records one sample ahead, visit entries two ahead.
+// ----------------------------------------------------------------------------
+// (a compiler-only memory barrier per row step: without it the fully unrolled
+// loops hoist all N*J*R/4 shared loads of B to the top and spill)
+#define SPTK_NO_HOIST() asm volatile("" ::: "memory")
+
+template <int N, int J, bool HV>
+__global__ void __launch_bounds__(128, (J <= 8 ? 4 : 3))
+    factor_fma_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
+                      float* __restrict__ fac, const float* __restrict__ cor, TpsParams<N> p, unsigned hot) {
+  constexpr int R = J, RW = N <= 3 ? 4 : 8;
+  __shared__ __align__(16) float Bs[N * J * R];  // B_n row-major (J x R)
+  __shared__ __align__(16) float Bt[N * R * J];  // B_n^T (R x J)
+  for (int i = threadIdx.x; i < N * J * R; i += blockDim.x) {
+    const int n = i / (J * R), rem = i % (J * R), j = rem / R, r = rem % R;
+    Bs[i] = cor[i];
+    Bt[(n * R + r) * J + j] = cor[i];
+  }
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long k0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  auto vis = [&](long long k) -> long long {
+    const long long kc = k < n_visit ? k : n_visit - 1;
+    return base + (HV ? (long long)__ldg(visit + kc) : kc);
+  };
+  long long v_next = vis(k0 + stride);
+  int4 w0 = make_int4(0, 0, 0, 0), w1 = w0;
+  tps_load_rec<RW>(rec, vis(k0), w0, w1);
+  for (long long k = k0; k < n_visit; k += stride) {
+    const int wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    int idx[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) idx[n] = wv[n];
+    const float x = __int_as_float(wv[N]);
+    tps_load_rec<RW>(rec, v_next, w0, w1);
+    v_next = vis(k + 2 * stride);
+    float a[N][J];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float4* src = reinterpret_cast<const float4*>(fac + p.foff[n] + (long long)idx[n] * J);
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) {
+        const float4 v = __ldcg(src + q);
+        a[n][4 * q] = v.x;
+        a[n][4 * q + 1] = v.y;
+        a[n][4 * q + 2] = v.z;
+        a[n][4 * q + 3] = v.w;
+      }
+    }
+    // c_n = a_n . B_n
+    float c[N][R];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) c[n][r] = 0.f;
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int r4 = 0; r4 < R / 4; ++r4) {
+          const float4 b = *reinterpret_cast<const float4*>(Bs + (n * J + j) * R + 4 * r4);
+          c[n][4 * r4] = fmaf(a[n][j], b.x, c[n][4 * r4]);
+          c[n][4 * r4 + 1] = fmaf(a[n][j], b.y, c[n][4 * r4 + 1]);
+          c[n][4 * r4 + 2] = fmaf(a[n][j], b.z, c[n][4 * r4 + 2]);
+          c[n][4 * r4 + 3] = fmaf(a[n][j], b.w, c[n][4 * r4 + 3]);
+          if (r4 == R / 4 - 1) SPTK_NO_HOIST();
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      // gs_j = sum_r W_r B_n[j][r] with W_r = prod_{n0 != n} c_n0[r] formed per
+      // r (B_n^T rows: 4 j per load); inter = a . gs
+      float gs[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) gs[j] = 0.f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float wr = 1.f;
+#pragma unroll
+        for (int n0 = 0; n0 < N; ++n0)
+          if (n0 != n) wr *= c[n0][r];
+#pragma unroll
+        for (int j4 = 0; j4 < J / 4; ++j4) {
+          const float4 b = *reinterpret_cast<const float4*>(Bt + (n * R + r) * J + 4 * j4);
+          gs[4 * j4] = fmaf(wr, b.x, gs[4 * j4]);
+          gs[4 * j4 + 1] = fmaf(wr, b.y, gs[4 * j4 + 1]);
+          gs[4 * j4 + 2] = fmaf(wr, b.z, gs[4 * j4 + 2]);
+          gs[4 * j4 + 3] = fmaf(wr, b.w, gs[4 * j4 + 3]);
+        }
+        SPTK_NO_HOIST();
+      }
+      float inter = 0.f;
+#pragma unroll
+      for (int j = 0; j < J; ++j) inter = fmaf(a[n][j], gs[j], inter);
+      const float gm = p.gam[n], lm = p.lam[n];
+      const bool red = hot >> n & 1u;
+      float4* dst = reinterpret_cast<float4*>(fac + p.foff[n] + (long long)idx[n] * J);
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) {
+        float d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;
+          const float g = -x * gs[j] + lm * a[n][j] + inter * gs[j];
+          d[u] = -gm * g;
+          a[n][j] += d[u];
+        }
+        if (red)
+          atomicAdd(dst + q, make_float4(d[0], d[1], d[2], d[3]));
+        else
+          __stcg(dst + q, make_float4(a[n][4 * q], a[n][4 * q + 1], a[n][4 * q + 2], a[n][4 * q + 3]));
+      }
+      if (n < N - 1) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) c[n][r] = 0.f;
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+#pragma unroll
+          for (int r4 = 0; r4 < R / 4; ++r4) {
+            const float4 b = *reinterpret_cast<const float4*>(Bs + (n * J + j) * R + 4 * r4);
+            c[n][4 * r4] = fmaf(a[n][j], b.x, c[n][4 * r4]);
+            c[n][4 * r4 + 1] = fmaf(a[n][j], b.y, c[n][4 * r4 + 1]);
+            c[n][4 * r4 + 2] = fmaf(a[n][j], b.z, c[n][4 * r4 + 2]);
+            c[n][4 * r4 + 3] = fmaf(a[n][j], b.w, c[n][4 * r4 + 3]);
+            if (r4 == R / 4 - 1) SPTK_NO_HOIST();
+          }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
 // warp per sample (generic ranks, J <= 64, R <= 64), Hogwild
 // ----------------------------------------------------------------------------
 struct GamLam {
@@ -383,6 +520,53 @@ static int launch_tps(const int* rec, int rw, const int* visit, long long n_visi
   return 0;
 }
 
+template <int N, int J>
+static int launch_fma(const int* rec, const int* visit, long long n_visit, long long base, float* fac,
+                      const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+  TpsParams<N> p;
+  for (int n = 0; n < N; ++n) {
+    p.foff[n] = md.foff[n];
+    p.gam[n] = gam[n];
+    p.lam[n] = lam[n];
+  }
+  // hot modes (fewer than 2^18 rows): red.add deltas, as the tcgen05 kernels
+  unsigned hot = 0;
+  for (int n = 0; n < N; ++n) {
+    const long long end = n + 1 < N ? md.foff[n + 1] : md.fac_size;
+    if ((end - md.foff[n]) / J < (1LL << 18)) hot |= 1u << n;
+  }
+  if (const char* e = getenv("SPTK_ATOMIC_MASK")) hot = (unsigned)strtoul(e, nullptr, 0);
+  int per_sm = 3;
+  if (const char* e = getenv("SPTK_TC_CTAS")) per_sm = atoi(e);
+  long long blocks = 148LL * per_sm;
+  const long long need = (n_visit + 127) / 128;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  if (visit)
+    factor_fma_kernel<N, J, true><<<(unsigned)blocks, 128, 0, s>>>(rec, visit, n_visit, base, fac, cor, p, hot);
+  else
+    factor_fma_kernel<N, J, false><<<(unsigned)blocks, 128, 0, s>>>(rec, visit, n_visit, base, fac, cor, p, hot);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
+// tc mode 5: the thread-per-sample CUDA-core kernel with red.add hot modes
+static int try_fma(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                   const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s,
+                   int* rc) {
+  const int N = md.n_modes, R = md.rcore, J = md.jr[0];
+  if (!all_equal_j(md, J) || J != R || rw != rec_words(N)) return 0;
+  if (N == 3 && J == 16) {
+    *rc = launch_fma<3, 16>(rec, visit, n_visit, base, fac, cor, md, gam, lam, s);
+    return 1;
+  }
+  if (N == 3 && J == 8) {
+    *rc = launch_fma<3, 8>(rec, visit, n_visit, base, fac, cor, md, gam, lam, s);
+    return 1;
+  }
+  return 0;
+}
+
 // returns 1 if handled (status in *rc), 0 if no specialisation
 static int try_tps(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
                    const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s,
@@ -441,6 +625,9 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
   }
   if (!f64) {
     int rc = 0;
+    if (get_tc_mode() == 5 && try_fma(rec, rw, visit, n_visit, base, (float*)fac, (const float*)cor, md,
+                                      (const float*)h_gammas, (const float*)h_lambdas, s, &rc))
+      return rc;
     if (try_factor_tc(rec, rw, visit, n_visit, base, (float*)fac, (const float*)cor, md, (const float*)h_gammas,
                       (const float*)h_lambdas, s, &rc))
       return rc;

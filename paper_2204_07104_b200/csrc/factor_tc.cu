@@ -378,12 +378,17 @@ struct Tc2Cfg {
   static constexpr int OFF_BT = 0;                       // N x (R rows x J)
   static constexpr int OFF_BN = OFF_BT + N * R * J;      // N x (J rows x R)
   static constexpr int OFF_G = OFF_BN + N * J * R;       // N x (R rows x R)
-  static constexpr int OFF_A = OFF_G + N * R * R;        // N x (128 x J), + 1 spare for the last mode
-  static constexpr int OFF_W = OFF_A + (N + 1) * M * J;  // 128 x R
-  static constexpr int FLOATS = OFF_W + M * R;  // + mbarrier (2 words), TMEM slot, claim slot
+  static constexpr int OFF_A = OFF_G + N * R * R;        // N x (128 x J)
+  static constexpr int OFF_W = OFF_A + N * M * J;        // 128 x R
+  static constexpr int OFF_BAR = OFF_W + M * R;          // mbarrier (2 words), TMEM slot, claim slot
+  // the last mode's second slot, allocated only when that mode is gathered
+  // ahead of its tile (a cold last mode); NF's and Y4's last modes are hot
+  static constexpr int OFF_SPARE = OFF_BAR + 4;
+  static constexpr int FLOATS = OFF_SPARE;
   static constexpr int NEED = (N * R > J + R) ? N * R : J + R;
   static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
+  static constexpr size_t SMEM = (size_t)FLOATS * 4;
+  static constexpr size_t SMEM_SPARE = SMEM + (size_t)M * J * 4;
 };
 
 template <int N, int RW>
@@ -440,7 +445,7 @@ __device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict
 }
 
 template <int N, int J, int R, bool HV>
-__global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 128 ? 3 : 2)))
+__global__ void __launch_bounds__(128, (N * (J + R) <= 128 ? 4 : 2))
     factor_tc2_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
                       float* __restrict__ fac, const float* __restrict__ cor, TcParams<N> p,
                       unsigned* __restrict__ tile_ctr) {
@@ -455,8 +460,8 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   constexpr int RW = N <= 3 ? 4 : (N <= 7 ? 8 : 16);
   using C = Tc2Cfg<N, J, R>;
   extern __shared__ __align__(16) float sm[];
-  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::FLOATS);
-  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 2);
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sm + C::OFF_BAR + 2);
   const int tid = threadIdx.x, warp = tid >> 5;
 
   for (int e = tid; e < N * J * R; e += 128) {
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
 
   // A-tile slot of mode n: modes 0..N-2 have one slot each, the last mode
   // alternates between two (pb).
-  auto a_off = [&](int n, int pb) { return C::OFF_A + (n < N - 1 ? n : N - 1 + pb) * 128 * J; };
+  auto a_off = [&](int n, int pb) { return n == N - 1 && pb ? C::OFF_SPARE : C::OFF_A + n * 128 * J; };
   // Row gather of one mode for this warp's 32 samples: CH = J/4 lanes share a
   // row (one 16-byte chunk each), so one cp.async instruction covers 32/CH
   // whole rows and L1 merges each row into a single L2 request.
@@ -554,7 +559,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   // consumed at its end), so CTAs that start late (another stream's kernel
   // holding the SM) or run slow simply take fewer tiles.
   const long long G = gridDim.x;
-  uint32_t& s_claim = *reinterpret_cast<uint32_t*>(sm + C::FLOATS + 3);
+  uint32_t& s_claim = *reinterpret_cast<uint32_t*>(sm + C::OFF_BAR + 3);
   long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
   if (tid == 0) s_claim = atomicAdd(tile_ctr, 1u);
   RecReg<N, RW> cur, nxt;
@@ -574,6 +579,8 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
   // tile early instead of a whole tile
   const unsigned lpm = p.prefetch == 3 ? p.atomic_mask : 0u;
   const unsigned fresh = ~(pfm | lpm);
+  // the last mode alternates between two slots only when gathered ahead
+  const int pbm = ((pfm | lpm) >> (N - 1) & 1u) ? 1 : 0;
 #pragma unroll
   for (int n = 0; n < N; ++n)
     if ((pfm | lpm) >> n & 1u) issue_mode(cur, n, pb);
@@ -663,11 +670,10 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
       phase ^= 1;
       tc::fence_after_sync();
       TC2_STAMP(7 + 3 * n);
-      float g[J], h[R];
+      float g[J];
       tc::tmem_ldh<J>(tlane, g);
-      if (n < N - 1) tc::tmem_ldh<R>(tlane + J, h);
       float* at = sm + a_off(n, pb);
-      float a[J], a0[J];
+      float a[J];
 #pragma unroll
       for (int q = 0; q < J / 4; ++q) {
         float4 v = *reinterpret_cast<const float4*>(at + canon<128>(tid, 4 * q));
@@ -676,26 +682,26 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
         a[4 * q + 2] = v.z;
         a[4 * q + 3] = v.w;
       }
-#pragma unroll
-      for (int j = 0; j < J; ++j) a0[j] = a[j];
       float inter = 0.f;
 #pragma unroll
       for (int j = 0; j < J; ++j) inter = fmaf(a[j], g[j], inter);
       const float gm = p.gam[n], lm = p.lam[n];
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        float gr = -cur.x * g[j] + lm * a[j] + inter * g[j];
-        a[j] -= gm * gr;
-      }
       // Row write-back through the (now dead) A slot: each thread parks its
       // new row (or, for red.add modes, its delta) in its own slot row, then
       // CH lanes per row write 16-byte chunks so each row is one request.
       const bool red = p.atomic_mask >> n & 1u;
 #pragma unroll
       for (int q = 0; q < J / 4; ++q) {
-        float4 v = red ? make_float4(a[4 * q] - a0[4 * q], a[4 * q + 1] - a0[4 * q + 1], a[4 * q + 2] - a0[4 * q + 2],
-                                     a[4 * q + 3] - a0[4 * q + 3])
-                       : make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+        float d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;
+          const float gr = -cur.x * g[j] + lm * a[j] + inter * g[j];
+          d[u] = -gm * gr;
+          a[j] += d[u];
+        }
+        const float4 v = red ? make_float4(d[0], d[1], d[2], d[3])
+                             : make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
         *reinterpret_cast<float4*>(at + canon<128>(tid, 4 * q)) = v;
       }
       if (!p.defer_wb || n == N - 1) {
@@ -703,6 +709,8 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
         flush_mode(cur, n, pb);
       }
       if (n < N - 1) {
+        float h[R];
+        tc::tmem_ldh<R>(tlane + J, h);
         const float keep = 1.f - gm * lm, step = gm * (cur.x - inter);
 #pragma unroll
         for (int r = 0; r < R; ++r) c[n][r] = fmaf(step, h[r], keep * c[n][r]);
@@ -714,7 +722,7 @@ __global__ void __launch_bounds__(128, (N * (J + R) <= 96 ? 4 : (N * (J + R) <= 
     tile = t1;
     t1 = t2;
     t2 = t3;
-    pb ^= 1;
+    pb ^= pbm;
     if (tid == 0) s_claim = claim;
     TC2_STAMP(15);
     __syncthreads();
@@ -1065,15 +1073,19 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   }
   (void)rw;  // == rec_words(N), checked by try_factor_tc
   auto kfn = visit ? factor_tc2_kernel<N, J, R, true> : factor_tc2_kernel<N, J, R, false>;
-  static int configured = 0;
+  // the last mode's spare slot only when it is gathered ahead (see Tc2Cfg)
+  const unsigned pfm = p.prefetch == 0 ? 0u : p.prefetch == 2 ? ~0u : ~p.atomic_mask;
+  const unsigned lpm = p.prefetch == 3 ? p.atomic_mask : 0u;
+  const size_t smem = ((pfm | lpm) >> (N - 1) & 1u) ? C::SMEM_SPARE : C::SMEM;
+  static size_t configured = 0;
   static int per_sm = 1;
-  if (!configured) {
+  if (configured != smem) {
     for (auto f : {factor_tc2_kernel<N, J, R, true>, factor_tc2_kernel<N, J, R, false>}) {
-      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_SPARE));
       SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
-    per_sm = resident_ctas((const void*)kfn, C::SMEM, C::TCOLS);
-    configured = 1;
+    per_sm = resident_ctas((const void*)kfn, smem, C::TCOLS);
+    configured = smem;
   }
   long long tiles = (n_visit + 127) / 128;
   long long blocks = 148LL * per_sm;
@@ -1085,7 +1097,7 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tile_ctr));
   ctr += (slot++ & 63u);
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
-  kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
+  kfn<<<(unsigned)blocks, 128, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
   SPTK_CHECK_LAUNCH();
   return 0;
 }
@@ -1394,7 +1406,7 @@ static int tc_mode_env() {
 }
 
 int set_tc_mode(int mode) {
-  if (mode < 0 || mode > 4) return 2;
+  if (mode < 0 || mode > 5) return 2;
   g_tc_mode = mode;
   return 0;
 }
@@ -1440,7 +1452,7 @@ static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit
 int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
                   const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc) {
   const int mode = tc_mode_env();
-  if (mode == 0) return 0;
+  if (mode == 0 || mode == 5) return 0;
   const int N = md.n_modes, R = md.rcore, J = md.jr[0];
   for (int n = 0; n < N; ++n)
     if (md.jr[n] != J) return 0;

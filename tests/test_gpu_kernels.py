@@ -214,7 +214,7 @@ def test_factor_seq_fp32_one_epoch(dims, J, R):
                                       ((3000,) * 6, 8, 8), ((3000, 3000, 3000), 32, 32),
                                       ((3000, 3000, 3000), 64, 64), ((300000, 3000, 3000), 64, 64),
                                       ((3000, 3000, 3000), 6, 5)])
-@pytest.mark.parametrize("tc", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("tc", [0, 1, 2, 3, 4, 5])
 def test_factor_hogwild_conflict_free_equals_sequential(dims, J, R, tc):
     """On samples touching pairwise-distinct rows the Hogwild kernels have no
     races, so they must equal the sequential semantics: FMA and 3xTF32 tcgen05
