@@ -364,7 +364,9 @@ def bench_ours(args, cfg):
             "test_rmse": test_rmse,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": factor_traffic(cfg["workload"]),
-                         "kernel": factor_kernel_name(order, cfg["J"], cfg["R"]),
+                         "kernel": ("factor_seq_kernel" if (args.mode == "exact" or (
+                             args.mode == "auto" and cfg["nnz"] <= (1 << 22)))
+                             else factor_kernel_name(order, cfg["J"], cfg["R"])),
                          "kernel_ms": f_ms, "kernel_share": f_ms * launches_per_epoch / ms_per_step,
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
                          "frac_of_8TBs": achieved / 8000.0},
