@@ -312,3 +312,4 @@ def test_h2d_upload_roundtrip(nbytes, threads):
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     _lib.check(L.sptk_h2d(d.data_ptr(), src.ctypes.data, nbytes, threads), "h2d")
     assert np.array_equal(d.cpu().numpy(), src)
+
