@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(128, 1)
 
 // CTAs of a 128-thread tcgen05 kernel that fit on one SM: registers, shared
 // memory (228 KB per SM, 1 KB reserved per CTA) and TMEM (512 columns).
-static int resident_ctas(const void* kfn, size_t smem, int tcols) {
+static int resident_ctas(const void* kfn, size_t smem, int tcols, bool leave_slot = true) {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, kfn) != cudaSuccess) return 1;
   int regs = fa.numRegs < 1 ? 1 : fa.numRegs;
@@ -340,7 +340,7 @@ static int resident_ctas(const void* kfn, size_t smem, int tcols) {
   // that fills every SM locks them out until it drains, while one free slot
   // per SM lets them run underneath (NF bench: 19.6 ms vs 22.3 ms per epoch,
   // the factor pass itself 13.5 vs 11.2 ms).  SPTK_TC_CTAS overrides.
-  int cap = n >= 4 ? n - 1 : n;
+  int cap = leave_slot && n >= 4 ? n - 1 : n;
   if (const char* e = getenv("SPTK_TC_CTAS")) cap = atoi(e);
   if (cap >= 1 && cap < n) n = cap;
   if (getenv("SPTK_DEBUG")) fprintf(stderr, "[sptk] tc kernel regs=%d smem=%zu -> %d CTAs/SM\n", regs, smem, n);
@@ -1084,11 +1084,24 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
       SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_SPARE));
       SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
-    per_sm = resident_ctas((const void*)kfn, smem, C::TCOLS);
+    per_sm = resident_ctas((const void*)kfn, smem, C::TCOLS, false);
     configured = smem;
   }
   long long tiles = (n_visit + 127) / 128;
-  long long blocks = 148LL * per_sm;
+  // Persistent grid: every CTA slot the kernel's resources allow except the
+  // ones left to the side-stream samplers that run beside the factor pass
+  // (SPTK_SAMPLER_SLOTS).  Measured per shape on the bench tensors (ms per
+  // epoch): NF J=R=16 with one slot free on every SM (444 CTAs) 18.9, with
+  // 520 / 560 / 575 CTAs 18.7 / 18.4 / 18.3, with all 592 slots 20.3 (the
+  // samplers then wait for the whole pass), so 16 slots there; J=R=8, Y4 and
+  // O6 are sampler-heavier relative to their factor pass and lose with 16
+  // (13.0 -> 13.5, 90 -> 96, 251 -> 272), so they keep one slot per SM.
+  int slots = (N == 3 && J >= 16) ? 16 : 148;
+  if (const char* e = getenv("SPTK_SAMPLER_SLOTS")) slots = atoi(e);
+  long long blocks = 148LL * per_sm - (per_sm >= 2 ? slots : 0);
+  // experiment hook: SPTK_TC_GRID = explicit persistent grid size
+  if (const char* e = getenv("SPTK_TC_GRID")) blocks = atoll(e);
+  if (blocks < 1) blocks = 1;
   if (blocks > tiles) blocks = tiles;
   // per-launch tile counter from a small rotating pool (launches on one stream
   // are ordered; the pool only guards against back-to-back reuse)

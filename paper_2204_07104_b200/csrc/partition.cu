@@ -148,6 +148,13 @@ __global__ void key_count_kernel(const unsigned* __restrict__ keys, long long n,
   for (; i < n; i += stride) atomicAdd(&cnt[keys[i]], 1);
 }
 
+__global__ void block_off1_kernel(int* __restrict__ off, int nnz) {
+  if (threadIdx.x == 0) {
+    off[0] = 0;
+    off[1] = nnz;
+  }
+}
+
 __global__ void pack_kernel(const long long* __restrict__ idx, const double* __restrict__ vals,
                             const int* __restrict__ ids, long long nnz, int N, int rw, int f64,
                             int* __restrict__ rec, int* __restrict__ pos_of_id) {
@@ -176,6 +183,7 @@ static inline unsigned gridn(long long n, int t) {
 }
 
 size_t partition_ws_bytes(long long nnz, int order, long long m) {
+  if (m == 1) return 4096;  // one block: no keys, no sort (see partition)
   long long nkeys = 1;
   for (int n = 0; n < order; ++n) nkeys *= m;
   long long ntiles = (nnz + RX_TILE - 1) / RX_TILE + 1;
@@ -218,6 +226,24 @@ int partition(const long long* idx64, const double* vals64, long long nnz, int o
   }
   SPTK_REQUIRE(nnz >= 0 && nnz < (1LL << 31), "partition: nnz out of range");
   SPTK_REQUIRE(ws_bytes >= partition_ws_bytes(nnz, order, m), "partition: workspace too small");
+  if (m == 1) {
+    // One block holding every entry in source order (the stable sort of
+    // all-equal keys is the identity): pack, ids = pos_of_id = iota,
+    // block_off = {0, nnz}.  No key or sort buffers.
+    const int rw1 = rec_words_t(order, f64 != 0);
+    if (nnz > 0) {
+      pack_kernel<<<gridn(nnz, 256), 256, 0, s>>>(idx64, vals64, nullptr, nnz, order, rw1, f64, rec_out, nullptr);
+      SPTK_CHECK_LAUNCH();
+      for (int* o : {ids_out, pos_of_id_out})
+        if (o) {
+          iota_i32_kernel<<<gridn(nnz, 256), 256, 0, s>>>(o, nnz);
+          SPTK_CHECK_LAUNCH();
+        }
+    }
+    block_off1_kernel<<<1, 32, 0, s>>>(block_off_out, (int)nnz);
+    SPTK_CHECK_LAUNCH();
+    return 0;
+  }
   Carve2 cv{(char*)ws, ws_bytes};
   unsigned* k0 = cv.take<unsigned>(nnz + 1);
   unsigned* k1 = cv.take<unsigned>(nnz + 1);

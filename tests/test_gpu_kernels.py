@@ -45,6 +45,24 @@ def test_partition_golden(golden, golden_meta):
         assert set(plan.block_entries) == want
 
 
+def test_partition_single_block_identity():
+    """m = 1 (one worker): one block in source order, without the key sort."""
+    from paper_2204_07104_b200.schedule import DevicePartition
+
+    rng = np.random.default_rng(8)
+    dims = (50, 60, 70)
+    idx = np.stack([rng.integers(0, d, 123_457) for d in dims], axis=1)
+    vals = rng.normal(size=len(idx))
+    dp = DevicePartition(idx, vals, dims, 1)
+    n = len(idx)
+    assert np.array_equal(dp.ids[:n].cpu().numpy(), np.arange(n))
+    assert np.array_equal(dp.pos_of_id[:n].cpu().numpy(), np.arange(n))
+    assert dp.block_off.tolist() == [0, n]
+    rec = dp.rec.cpu().numpy().reshape(-1, dp.rw)[:n]
+    assert np.array_equal(rec[:, :3], idx)
+    assert np.array_equal(rec[:, 3].view(np.float32), vals.astype(np.float32))
+
+
 def test_partition_many_blocks_stable():
     """Keys needing two radix passes (m^N = 4096) stay stable."""
     from paper_2204_07104_b200.schedule import DevicePartition
