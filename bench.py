@@ -326,20 +326,26 @@ def bench_ours(args, cfg):
     # end to end through the public API (host arrays in, model out)
     e2e = None
     if not args.no_e2e and world == 1:
-        m2 = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
         k2 = args.e2e_epochs or args.steps
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        train(m2, DatasetSplit(tr, te), TrainConfig(epochs=k2, seed=1, update_mode=args.mode,
-                                                    alpha_a=cfg.get("alpha_a", 0.009)))
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t1
+        # three end-to-end runs, the median reported (host-side phases --
+        # upload threads, page faults -- vary run to run on the GPU boxes)
+        runs = []
+        for _ in range(3):
+            m2 = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            train(m2, DatasetSplit(tr, te), TrainConfig(epochs=k2, seed=1, update_mode=args.mode,
+                                                        alpha_a=cfg.get("alpha_a", 0.009)))
+            torch.cuda.synchronize()
+            runs.append(time.perf_counter() - t1)
+        el = sorted(runs)[1]
         h2d = tr.indices.nbytes + tr.values.nbytes + te.indices.nbytes + te.values.nbytes + \
             sum(a.nbytes for a in m2.factors + m2.core_factors)
         d2h = sum(a.nbytes for a in m2.factors + m2.core_factors) + 32 * k2
         log("e2e done")
         e2e = {"value": cfg["nnz"] * k2 / el, "unit": "nnz/s", "h2d_bytes_per_step": h2d // k2,
                "d2h_bytes_per_step": d2h // k2, "epochs": k2, "seconds": el,
+               "runs_seconds": [round(x, 4) for x in runs], "statistic": "median of 3 runs",
                "what": "public train() on host numpy arrays: upload + K1 partition + epochs + per-epoch "
                        "train/test RMSE + model download, divided per epoch"}
     cpu = None
