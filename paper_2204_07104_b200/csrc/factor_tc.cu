@@ -1039,6 +1039,9 @@ static int launch_tc3(const int* rec, int rw, const int* visit, long long n_visi
   }
   long long tiles = (n_visit + 127) / 128;
   long long blocks = 148LL * per_sm;
+  // CTA slots left to the side-stream samplers (see launch_tc2); default none
+  if (const char* e = getenv("SPTK_SAMPLER_SLOTS3")) blocks -= atoi(e);
+  if (blocks < 1) blocks = 1;
   if (blocks > tiles) blocks = tiles;
   static unsigned slot = 0;
   unsigned* ctr = nullptr;
