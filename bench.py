@@ -7,7 +7,7 @@ entries), J = R = 16, fp32, throughput (Hogwild) mode.  One "step" is one
 epoch: the bit-exact GPU visit-order sampler, the factor pass over every
 nonzero, the core-batch sampler (2^20 of 99M, Floyd) and the core gradient +
 apply -- exactly the work inside the reference's wall_seconds
-(trainer.py:291-353), evaluation excluded.
+(trainer.py:187-249), evaluation excluded.
 
 Keys beyond the driver contract:
   roofline      the factor kernel (dominant) against the measured HBM copy

@@ -18,10 +18,10 @@
  *          trainer.py:226-230), then the merge+apply of trainer.py:238-247
  *       -> sptk_core_apply / sptk_core_apply_f64
  *   np.random.default_rng([seed,1,t,*block]).permutation(len(ids))
- *                                                        (trainer.py:300-303)
+ *                                                        (trainer.py:196-199)
  *       -> sptk_pcg64_seed + sptk_permutation
  *   np.random.default_rng([seed,2,t]).choice(nnz, k, replace=False)
- *                                                        (trainer.py:317-324)
+ *                                                        (trainer.py:212-221)
  *       -> sptk_pcg64_seed + sptk_choice
  *   build_partition(tensor, m)                           (partition.py:47-81)
  *       -> sptk_partition (+ the device re-layout of the COO data)
@@ -81,7 +81,7 @@ int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, voi
 /* Visit-ordered records: d_rec_out[k] = d_rec_src[perm[k]] (rw 32-bit words
  * each, rw in {4, 8, 16}) with perm = Generator.permutation(n) for h_state;
  * d_perm_out (may be NULL) also receives perm.  The factor phase's
- * `visit = ids[perm]` gather (trainer.py:300-303) fused into the sampler, so
+ * `visit = ids[perm]` gather (trainer.py:196-199) fused into the sampler, so
  * the factor pass streams its block's records sequentially.  Workspace:
  * sptk_permutation_ws_bytes(n). */
 int sptk_permute_records(const uint64_t h_state[4], long long n, const int32_t* d_rec_src, int rw,

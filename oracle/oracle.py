@@ -13,8 +13,8 @@ Everything here restates the reference ``sptucker`` package
 * ``factor_pass``      -> _loops.py:17-63
 * ``core_pass``        -> _loops.py:66-104
 * ``predict``          -> model.py:134-146
-* ``permutation``      -> Generator.permutation as used at trainer.py:300-303
-* ``choice``           -> Generator.choice(replace=False), trainer.py:317-324
+* ``permutation``      -> Generator.permutation as used at trainer.py:196-199
+* ``choice``           -> Generator.choice(replace=False), trainer.py:212-221
 * ``partition``        -> partition.py:47-81
 * ``round_schedule``   -> partition.py:84-117
 * ``pcg64_state``      -> default_rng(entropy) seeding (SeedSequence + PCG64)

@@ -14,15 +14,15 @@
  *
  * Sections and the reference lines they restate:
  *   SeedSequence + PCG64 seeding ... numpy bit_generator.pyx (SeedSequence),
- *       _pcg64.pyx / pcg64.h (XSL-RR 128/64); used by trainer.py:300-302,
- *       trainer.py:318, model.py:97, coo.py:486.
+ *       _pcg64.pyx / pcg64.h (XSL-RR 128/64); used by trainer.py:196-198,
+ *       trainer.py:214, model.py:97, coo.py:281.
  *   random_interval / Lemire32 ..... numpy distributions.c (random_interval,
  *       buffered_bounded_lemire_uint32, random_bounded_uint64).
  *   permutation .................... Generator.permutation -> shuffle ->
- *       _shuffle_raw (Fisher-Yates, i = n-1..1); trainer.py:300-303.
+ *       _shuffle_raw (Fisher-Yates, i = n-1..1); trainer.py:196-199.
  *   choice(replace=False) .......... Generator.choice: tail shuffle
  *       (_shuffle_int) when pop > 10000 and k > pop // 50, else Floyd +
- *       _shuffle_int(k, 1); trainer.py:317-324, coo.py:486-487.
+ *       _shuffle_int(k, 1); trainer.py:212-221, coo.py:281.
  *   partition ...................... partition.py:47-81 (stable bucketing).
  *   factor_pass .................... _loops.py:17-63.
  *   core_pass ...................... _loops.py:66-104.

@@ -29,7 +29,7 @@ void count_launch(int n) { g_launches += n; }
 
 // numpy.random.bit_generator.SeedSequence (pool size 4) + PCG64 seeding
 // (pcg64_set_seed -> pcg_setseq_128_srandom_r).  Used by the reference at
-// trainer.py:300-302 and trainer.py:318 through np.random.default_rng.
+// trainer.py:196-198 and trainer.py:214 through np.random.default_rng.
 static uint32_t ss_hashmix(uint32_t v, uint32_t* hc) {
   v ^= *hc;
   *hc *= 0x931e8875u;

@@ -2,10 +2,10 @@
 //
 // The reference draws, per epoch,
 //   * the factor-phase visit order  default_rng([seed,1,t,*block]).permutation(len(ids))
-//     (trainer.py:300-303): numpy Fisher-Yates, i = n-1..1,
+//     (trainer.py:196-199): numpy Fisher-Yates, i = n-1..1,
 //     j_i = random_interval(i) (masked rejection on buffered u32 draws);
 //   * the core batch  default_rng([seed,2,t]).choice(nnz, k, replace=False)
-//     (trainer.py:317-324): Floyd with Lemire draws + _shuffle_int, or the
+//     (trainer.py:212-221): Floyd with Lemire draws + _shuffle_int, or the
 //     tail-shuffle path (_shuffle_int over arange) when pop > 10000 and
 //     k > pop // 50.
 // These are inherently sequential loops over one PCG64 stream.  They are
@@ -612,7 +612,7 @@ int exclusive_scan(const int* in, long long n, int* out, int* ws, cudaStream_t s
 
 // ---------------------------------------------------------------------------
 // Floyd membership (choice, replace=False): out[t] = vals[t] unless vals[t]
-// is already selected, in which case j_t = base + t (coo.py:486 / trainer.py:322
+// is already selected, in which case j_t = base + t (coo.py:281 / trainer.py:218
 // -> Generator.choice).  c_t = !first_t || (vals[t]-base in [0,t) && c_{vals[t]-base}).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t mix32(uint32_t h) {

@@ -4,7 +4,7 @@
 PCG64 seeding (SeedSequence) in the C library; ``permutation`` and ``choice``
 return the exact arrays numpy 2.x's Generator.permutation /
 Generator.choice(replace=False) produce for that state
-(trainer.py:300-303 and 317-324), computed on the GPU.
+(trainer.py:196-199 and 317-324), computed on the GPU.
 """
 
 from __future__ import annotations
@@ -61,7 +61,7 @@ def permute_records(n: int, src, rw: int, out, ws: Workspace | None = None, stat
                     perm_out=None, stream=None):
     """out[k] = src[perm[k]] for the records of one block (rw int32 words each),
     perm = default_rng(entropy).permutation(n): the visit-ordered records of
-    trainer.py:300-303 (``visit = ids[perm]``) in one fused sampler call."""
+    trainer.py:196-199 (``visit = ids[perm]``) in one fused sampler call."""
     _lib.require_cuda()
     L = _lib.load()
     st = state if state is not None else pcg64_state(entropy)

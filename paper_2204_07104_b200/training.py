@@ -6,14 +6,14 @@ defaults, validation messages and metric semantics.  Inside ``train`` every
 step of an epoch runs on the GPU, enqueued on one stream with no host
 round-trip:
 
-    for each round of the DSGD schedule, for each block      (trainer.py:294-312)
+    for each round of the DSGD schedule, for each block      (trainer.py:189-208)
         visit = K2 permutation(default_rng([seed,1,t,*block]))   bit-exact
         K3 factor pass over the block's records in visit order
-    core batch Psi = arange / K2 choice(default_rng([seed,2,t]))  (trainer.py:316-324)
-    K4 core-gradient reduction over Psi, K5 apply              (trainer.py:325-351)
+    core batch Psi = arange / K2 choice(default_rng([seed,2,t]))  (trainer.py:212-221)
+    K4 core-gradient reduction over Psi, K5 apply              (trainer.py:222-247)
 
 ``wall_seconds`` is device time between CUDA events around that work (the
-reference's perf_counter interval, trainer.py:291/353), evaluation excluded.
+reference's perf_counter interval, trainer.py:187/249), evaluation excluded.
 
 Update modes (extra TrainConfig fields; the defaults keep the reference's
 call signature working):

@@ -205,7 +205,7 @@ for c in range(4):
 META["n_loops"] = 4
 
 # ------------------------------------- sampler at small and full sizes ----
-# The reference's samplers are these exact calls (trainer.py:300-303, 317-324).
+# The reference's samplers are these exact calls (trainer.py:196-199, 317-324).
 small = {}
 for n in [1, 2, 3, 5, 17, 100, 1000, 4097, 65536, 100_003]:
     ent = [5, 1, 3, 0, n % 5]

@@ -145,7 +145,7 @@ def test_choice_netflix_core_batch(golden_meta):
                                      (40_000, 6)])
 def test_permute_records_equals_visit_gather(n, order):
     """sptk_permute_records: the block's records in the order of
-    default_rng(entropy).permutation(n) (trainer.py:300-303), bit for bit,
+    default_rng(entropy).permutation(n) (trainer.py:196-199), bit for bit,
     together with the permutation itself."""
     import torch
 
