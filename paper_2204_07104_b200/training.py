@@ -43,7 +43,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, f64arr, i64arr, ptr, stream_ptr
-from .device import DeviceCoo, DeviceModel, rmse_mae_device
+from .device import DeviceCoo, DeviceModel, eval_sums, rmse_mae_device
 from .sampler import Workspace, choice, fy_apply, pcg64_state, permutation_j, permutation_j_batch
 from .schedule import DevicePartition, round_schedule
 from .tensor import DatasetSplit, SparseTensorCoo
@@ -116,7 +116,8 @@ def learning_rate(alpha: float, beta: float, t: int) -> float:
 def _metric(model: TuckerModel, dataset: SparseTensorCoo):
     if dataset.nnz == 0:
         raise ValueError("dataset is empty")
-    return rmse_mae_device(DeviceModel(model), DeviceCoo(dataset.indices, dataset.values))
+    # fp64 on the device, like the reference's numpy evaluation (trainer.py:89-102)
+    return rmse_mae_device(DeviceModel(model, f64=True), DeviceCoo(dataset.indices, dataset.values, f64=True))
 
 
 def rmse(model: TuckerModel, dataset: SparseTensorCoo) -> float:
@@ -142,8 +143,7 @@ def frobenius_objective(model: TuckerModel, dataset: SparseTensorCoo, lambda_cor
     if dataset.nnz == 0:
         raise ValueError("dataset is empty")
     dm = DeviceModel(model, f64=True)
-    s = rmse_mae_device(dm, DeviceCoo(dataset.indices, dataset.values, f64=True))
-    total = s[0] ** 2 * dataset.nnz
+    total = float(eval_sums(dm, DeviceCoo(dataset.indices, dataset.values, f64=True))[0].item())
     if lambda_core != 0.0:
         if math.prod(model.j_ranks) <= MAX_CORE_ELEMENTS:
             dense = _dense_core(model.core_factors)
