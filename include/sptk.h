@@ -67,6 +67,10 @@ int sptk_record_words(int order, int f64_records);
  * form.  The environment variable SPTK_TC sets the initial value. */
 int sptk_set_tc_mode(int mode);
 int sptk_get_tc_mode(void);
+/* Name of the factor kernel the most recent sptk_factor_pass dispatched to
+ * (e.g. "factor_tma_kernel"); "none" before the first call.  Lets the caller
+ * label measurements with the kernel that actually ran. */
+const char* sptk_last_factor_kernel(void);
 /* test hook: per-sample dump of the first tcgen05 tile (c, gs, refreshed c). */
 void sptk_debug_tc_buffer(float* d_buf);
 

@@ -31,6 +31,7 @@ SIGNATURES = {
     "sptk_record_words": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "sptk_set_tc_mode": (ctypes.c_int, [ctypes.c_int]),
     "sptk_get_tc_mode": (ctypes.c_int, []),
+    "sptk_last_factor_kernel": (ctypes.c_char_p, []),
     "sptk_debug_tc_buffer": (None, [_vp]),
     "sptk_pcg64_seed": (ctypes.c_int, [_u64p, ctypes.c_int, _u64p]),
     "sptk_permutation_ws_bytes": (ctypes.c_size_t, [_i64]),

@@ -92,6 +92,7 @@ int sptk_set_tc_mode(int mode) {
   return 0;
 }
 int sptk_get_tc_mode(void) { return get_tc_mode(); }
+const char* sptk_last_factor_kernel(void) { return last_factor_kernel(); }
 void sptk_debug_tc_buffer(float* d_buf) { set_tc_debug(d_buf); }
 
 int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_out[4]) {

@@ -516,6 +516,7 @@ static int launch_tps(const int* rec, int rw, const int* visit, long long n_visi
     factor_tps_kernel<N, J, R, 4><<<(unsigned)blocks, threads, 0, s>>>(rec, visit, n_visit, base, fac, p);
   else
     factor_tps_kernel<N, J, R, 8><<<(unsigned)blocks, threads, 0, s>>>(rec, visit, n_visit, base, fac, p);
+  note_factor_kernel("factor_tps_kernel");
   SPTK_CHECK_LAUNCH();
   return 0;
 }
@@ -546,6 +547,7 @@ static int launch_fma(const int* rec, const int* visit, long long n_visit, long 
     factor_fma_kernel<N, J, true><<<(unsigned)blocks, 128, 0, s>>>(rec, visit, n_visit, base, fac, cor, p, hot);
   else
     factor_fma_kernel<N, J, false><<<(unsigned)blocks, 128, 0, s>>>(rec, visit, n_visit, base, fac, cor, p, hot);
+  note_factor_kernel("factor_fma_kernel");
   SPTK_CHECK_LAUNCH();
   return 0;
 }
@@ -620,6 +622,7 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
     auto kfn = factor_seq_kernel<T>;
     SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kfn<<<1, 32, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl, cand, per_thread);
+  note_factor_kernel("factor_seq_kernel");
     SPTK_CHECK_LAUNCH();
     return 0;
   }
@@ -651,6 +654,7 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
   long long blocks = (n_visit + warps - 1) / warps;
   if (blocks > 148 * 8) blocks = 148 * 8;
   kfn<<<(unsigned)blocks, 32 * warps, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl, per_warp);
+  note_factor_kernel("factor_wps_kernel");
   SPTK_CHECK_LAUNCH();
   return 0;
 }

@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc.cuh"
+#include "factor_tc_util.cuh"
 
 #include <stdio.h>
 #include <stdlib.h>
@@ -57,11 +58,6 @@ struct TcCfg {
   static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
 };
 
-// float offset of element (row, k) in a K-major canonical operand with ROWS rows
-template <int ROWS>
-__device__ __forceinline__ int canon(int row, int k) {
-  return (k >> 2) * (ROWS * 4) + (row >> 3) * 32 + (row & 7) * 4 + (k & 3);
-}
 
 __device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
@@ -324,43 +320,7 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
-// CTAs of a 128-thread tcgen05 kernel that fit on one SM: registers, shared
-// memory (228 KB per SM, 1 KB reserved per CTA) and TMEM (512 columns).
-static int resident_ctas(const void* kfn, size_t smem, int tcols, bool leave_slot = true) {
-  cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, kfn) != cudaSuccess) return 1;
-  int regs = fa.numRegs < 1 ? 1 : fa.numRegs;
-  int by_regs = 65536 / (((regs * 32 + 255) / 256) * 256 * 4);
-  int by_smem = (int)((228 * 1024) / (smem + fa.sharedSizeBytes + 1024));
-  int by_tmem = 512 / tcols;
-  int n = by_regs < by_smem ? by_regs : by_smem;
-  n = n < by_tmem ? n : by_tmem;
-  // Default: one CTA per SM below the resource limit.  The training epoch
-  // runs the next epoch's samplers on side streams; a persistent factor grid
-  // that fills every SM locks them out until it drains, while one free slot
-  // per SM lets them run underneath (NF bench: 19.6 ms vs 22.3 ms per epoch,
-  // the factor pass itself 13.5 vs 11.2 ms).  SPTK_TC_CTAS overrides.
-  int cap = leave_slot && n >= 4 ? n - 1 : n;
-  if (const char* e = getenv("SPTK_TC_CTAS")) cap = atoi(e);
-  if (cap >= 1 && cap < n) n = cap;
-  if (getenv("SPTK_DEBUG")) fprintf(stderr, "[sptk] tc kernel regs=%d smem=%zu -> %d CTAs/SM\n", regs, smem, n);
-  return n < 1 ? 1 : n;
-}
 
-// Modes with few rows take many concurrent updates per row; their row writes
-// are issued as red.add deltas so no update is lost (Hogwild with atomic
-// deltas).  Default: modes with fewer than 2^18 rows.  SPTK_ATOMIC_MASK
-// overrides (bit n = mode n).
-static unsigned hot_mode_mask(const ModelDesc& md) {
-  if (const char* e = getenv("SPTK_ATOMIC_MASK")) return (unsigned)strtoul(e, nullptr, 0);
-  unsigned m = 0;
-  for (int n = 0; n < md.n_modes; ++n) {
-    const long long end = n + 1 < md.n_modes ? md.foff[n + 1] : md.fac_size;
-    const long long rows = (end - md.foff[n]) / (md.jr[n] > 0 ? md.jr[n] : 1);
-    if (rows < (1LL << 18)) m |= 1u << n;
-  }
-  return m;
-}
 
 // ----------------------------------------------------------------------------
 // v2 (TF32, the default throughput kernel): 1 + N tensor rounds per tile.
@@ -391,58 +351,6 @@ struct Tc2Cfg {
   static constexpr size_t SMEM_SPARE = SMEM + (size_t)M * J * 4;
 };
 
-template <int N, int RW>
-struct RecReg {
-  int idx[N];
-  float x;
-  bool valid;
-};
-
-// visit-list entry of this thread's sample in `tile` (-1 past the end)
-// Returns the raw 32-bit entry: widening it here would make the compiler
-// consume the load immediately (a sign extension right after the LDG), which
-// exposed the full visit-gather latency at the start of every tile.
-// (HV: a visit list is given; without one the k-th sample is record k.  A
-// template flag, so no predicated select ever writes the loaded register.)
-template <bool HV>
-__device__ __forceinline__ int load_vis(const int* __restrict__ visit, long long n_visit, long long tile,
-                                        uint64_t pol) {
-  // unconditional (clamped) load; validity is recomputed from the tile index
-  long long k = tile * 128 + threadIdx.x;
-  k = k < n_visit ? k : n_visit - 1;
-  if (HV) return tc::ld_stream_s32(visit + k, pol);
-  return (int)k;
-}
-__device__ __forceinline__ bool tile_valid(long long n_visit, long long tile) {
-  return tile * 128 + threadIdx.x < n_visit;
-}
-
-template <int N, int RW>
-__device__ __forceinline__ void load_rec(RecReg<N, RW>& o, const int* __restrict__ rec, int v, bool valid,
-                                         long long base, uint64_t pol) {
-  // Unconditional load (past-the-end samples read the block's first record
-  // and are masked by `valid` at use): a predicated load merged with a
-  // default value would make the compiler wait for it right here, exposing
-  // the record-gather latency instead of hiding it behind two tiles of work.
-  o.valid = valid;
-  const int* rp = rec + (base + (long long)v) * RW;
-  int wv[8];
-  int4 w0 = tc::ld_stream_v4(rp, pol);
-  wv[0] = w0.x;
-  wv[1] = w0.y;
-  wv[2] = w0.z;
-  wv[3] = w0.w;
-  if (RW >= 8) {
-    int4 w1 = tc::ld_stream_v4(rp + 4, pol);
-    wv[4] = w1.x;
-    wv[5] = w1.y;
-    wv[6] = w1.z;
-    wv[7] = w1.w;
-  }
-#pragma unroll
-  for (int n = 0; n < N; ++n) o.idx[n] = wv[n];
-  o.x = __int_as_float(wv[N]);
-}
 
 template <int N, int J, int R, bool HV>
 __global__ void __launch_bounds__(128, (N * (J + R) <= 128 ? 4 : 2))
@@ -1049,6 +957,7 @@ static int launch_tc3(const int* rec, int rw, const int* visit, long long n_visi
   ctr += (slot++ & 63u);
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
   kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
+  note_factor_kernel("factor_tc3_kernel");
   SPTK_CHECK_LAUNCH();
   return 0;
 }
@@ -1114,6 +1023,7 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   ctr += (slot++ & 63u);
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
   kfn<<<(unsigned)blocks, 128, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
+  note_factor_kernel("factor_tc2_kernel");
   SPTK_CHECK_LAUNCH();
   return 0;
 }
@@ -1405,29 +1315,33 @@ static int launch_tc4(const int* rec, int rw, const int* visit, long long n_visi
   ctr += (slot++ & 63u);
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
   kfn<<<(unsigned)blocks, 512, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
+  note_factor_kernel("factor_tc4_kernel");
   SPTK_CHECK_LAUNCH();
   return 0;
 }
 
-// 0 off (CUDA-core FMA kernel), 1 TF32 v2 (default), 2 TF32 v1, 3 3xTF32 v1,
-// 4 TF32 v3 (two threads per sample); J = R = 64 always takes v4 when on
+// 0 off (CUDA-core FMA kernel), 1 TF32 v2, 2 TF32 v1, 3 3xTF32 v1,
+// 4 TF32 v3 (two threads per sample), 5 CUDA-core thread-per-sample FMA,
+// 6 TF32 v6 with TMA row traffic (default; v2/v3/v4 for shapes it lacks);
+// J = R = 64 always takes v4 when on
 static int g_tc_mode = -1;
 
 static int tc_mode_env() {
   if (g_tc_mode < 0) {
     const char* e = getenv("SPTK_TC");
-    g_tc_mode = e ? atoi(e) : 1;
+    g_tc_mode = e ? atoi(e) : 6;
   }
   return g_tc_mode;
 }
 
 int set_tc_mode(int mode) {
-  if (mode < 0 || mode > 5) return 2;
+  if (mode < 0 || mode > 6) return 2;
   g_tc_mode = mode;
   return 0;
 }
 int get_tc_mode() { return tc_mode_env(); }
 void set_tc_debug(float* buf) { g_tc_debug = buf; }
+float* tc_debug_buffer() { return g_tc_debug; }
 
 template <int N, int J, int R, bool SPLIT>
 static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
@@ -1460,6 +1374,7 @@ static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit
   long long blocks = 148LL * per_sm;
   if (blocks > tiles) blocks = tiles;
   kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p);
+  note_factor_kernel("factor_tc_kernel");
   SPTK_CHECK_LAUNCH();
   return 0;
 }
@@ -1467,8 +1382,13 @@ static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit
 // returns 1 if handled
 int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
                   const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc) {
-  const int mode = tc_mode_env();
+  int mode = tc_mode_env();
   if (mode == 0 || mode == 5) return 0;
+  // v6 (TMA row traffic) where it has an instance, v2 / v3 / v4 elsewhere
+  if (mode == 6) {
+    if (try_factor_tma(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s, rc)) return 1;
+    mode = 1;
+  }
   const int N = md.n_modes, R = md.rcore, J = md.jr[0];
   for (int n = 0; n < N; ++n)
     if (md.jr[n] != J) return 0;

@@ -1,0 +1,536 @@
+// factor_tma.cu -- K3 v6: the tcgen05 factor kernel with its row traffic on TMA.
+//
+// Same per-sample update as factor_tc2_kernel (_loops.py:17-63, Hogwild over
+// the visit order; c refresh folded into the gs round through G_n = B_n^T B_n):
+//
+//   c_n  = A_n[tile] . B_n           (128 x R)  one MMA round per tile
+//   gs_n = W_n . B_n^T,  h_n = W_n . G_n           one MMA round per mode
+//   a'   = a - gamma(-x gs + lambda a + (a.gs) gs),  c_n' = (1 - gamma lambda) c_n + gamma (x - a.gs) h_n
+//
+// What changes against v2 is where the bytes move:
+//  * rows are gathered by the tensor memory accelerator: a 2-D tensor map per
+//    factor matrix and `tile::gather4` (four arbitrary rows per instruction)
+//    write straight into a K-major operand tile in the swizzled layout whose
+//    swizzle span is one row (32 / 64 B for J = 8 / 16), completing on an
+//    mbarrier -- no per-lane cp.async, no load/store-pipe traffic;
+//  * rows go back the same way: cold (large) modes as `tile::scatter4` stores
+//    of the updated rows, hot (small) modes as one bulk fp32 add-reduction of
+//    the 64-byte delta per sample (atomic at L2, nothing lost);
+//  * W_n is written to TMEM (tcgen05.st) and used as the MMA's A operand from
+//    there, so it never touches shared memory;
+//  * the only CTA-wide barrier per mode is the one that hands W_n to the MMA.
+// Thread t <-> sample t <-> TMEM lane t <-> row t of every operand tile; the
+// swizzle keeps each row inside its own 16*J-byte span, so a thread reads and
+// rewrites its row without conflicts and without touching other rows.
+#include "common.cuh"
+#include "factor_tc_util.cuh"
+#include "kernels.cuh"
+#include "tc.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <stdio.h>
+#include <stdlib.h>
+
+namespace sptk {
+
+template <int N>
+struct TmaMaps {
+  CUtensorMap m[N];
+};
+
+template <int N>
+struct TmaParams {
+  long long foff[N];
+  float gam[N];
+  float lam[N];
+  long long* dbg;         // optional per-phase clock stamps of block 0 (long long[16][16])
+  unsigned atomic_mask;   // bit n: mode-n rows are written back as add-reduced deltas (hot modes)
+  unsigned early_mask;    // bit n: the next tile's mode-n rows are gathered while this tile runs
+  int bulk_red;           // hot deltas as one bulk add-reduction per sample (TMA unit) instead of red.add.v4
+};
+
+template <int N, int J, int R>
+struct TmaCfg {
+  static constexpr int M = 128;
+  static constexpr int ROWB = J * 4;       // bytes per row = swizzle span
+  static constexpr int SLOT = M * J;       // floats per operand tile
+  static constexpr int NSLOT = N + 1;      // + a second slot for the last mode
+  static constexpr int OFF_A = 0;          // slots first: 1024-byte aligned
+  static constexpr int OFF_BT = OFF_A + NSLOT * SLOT;  // N x (R rows x J), canonical
+  static constexpr int OFF_BN = OFF_BT + N * R * J;    // N x (J rows x R)
+  static constexpr int OFF_G = OFF_BN + N * J * R;     // N x (R rows x R)
+  static constexpr int OFF_BAR = (OFF_G + N * R * R + 1) & ~1;  // NSLOT + 1 mbarriers
+  static constexpr int OFF_MISC = OFF_BAR + 2 * (NSLOT + 1);     // TMEM address, tile claim
+  static constexpr int OFF_IDX = (OFF_MISC + 4 + 3) & ~3;         // [2][N][128] row indices (16-B aligned)
+  static constexpr int FLOATS = OFF_IDX + 2 * N * M;
+  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 1024;       // + alignment slack
+  // TMEM columns: the c round writes c_0..c_{N-1} at n*R; afterwards W at 0,
+  // gs at R, h at R + J (c lives in registers by then)
+  static constexpr int COL_W = 0, COL_G = R, COL_H = R + J;
+  static constexpr int NEED = (N * R > 2 * R + J) ? N * R : 2 * R + J;
+  static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : 256;
+};
+
+// float offset of (row, 16-byte chunk q) in a swizzled operand tile of J-float rows
+template <int J>
+__device__ __forceinline__ int swz(int row, int q) {
+  constexpr int CH = J / 4;
+  return row * J + 4 * (q ^ (((row * J * 4) >> 7) & (CH - 1)));
+}
+
+template <int R>
+__device__ __forceinline__ void tmem_st_row(uint32_t taddr, const float* v) {
+  if (R % 16 == 0) {
+#pragma unroll
+    for (int q = 0; q < R / 16; ++q) tc::tmem_st16(taddr + 16 * q, v + 16 * q);
+  } else {
+#pragma unroll
+    for (int q = 0; q < R / 8; ++q) tc::tmem_st8(taddr + 8 * q, v + 8 * q);
+  }
+}
+
+__device__ unsigned g_tma_tile_ctr[64];
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(pred));
+  return pred != 0;
+}
+
+#ifdef SPTK_TMA_STAMPS
+#define TMA_STAMP(k)                                                                                       \
+  do {                                                                                                     \
+    if (p.dbg && blockIdx.x == 0 && tid == 0 && ntile < 16) p.dbg[ntile * 16 + (k)] = clock64();          \
+  } while (0)
+#else
+#define TMA_STAMP(k) \
+  do {               \
+  } while (0)
+#endif
+
+template <int N, int J, int R, bool HV>
+__global__ void __launch_bounds__(128, 4)
+    factor_tma_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
+                      float* __restrict__ fac, const float* __restrict__ cor, const __grid_constant__ TmaParams<N> p,
+                      const __grid_constant__ TmaMaps<N> maps, unsigned* __restrict__ tile_ctr) {
+  constexpr int RW = N <= 3 ? 4 : (N <= 7 ? 8 : 16);
+  using C = TmaCfg<N, J, R>;
+  extern __shared__ __align__(16) float sm_raw[];
+  // operand tiles need 1024-byte alignment; offsetting the __shared__ array
+  // itself keeps every access a shared-space one (LDS/STS)
+  float* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u) / 4;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // [NSLOT]: row tiles landed
+  uint64_t* mbar = full + C::NSLOT;                                 // MMA round done
+  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::OFF_MISC);   // [0] TMEM address, [1] tile claim
+  int* ids = reinterpret_cast<int*>(sm + C::OFF_IDX);               // [2 tiles][N modes][128] row indices
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int ntile = 0;
+  (void)ntile;
+
+  for (int e = tid; e < N * J * R; e += 128) {
+    const int n = e / (J * R), rem = e - n * (J * R), j = rem / R, r = rem - j * R;
+    const float b = __ldg(cor + e);
+    sm[C::OFF_BT + n * R * J + canon<R>(r, j)] = b;
+    sm[C::OFF_BN + n * J * R + canon<J>(j, r)] = b;
+  }
+  for (int e = tid; e < N * R * R; e += 128) {
+    const int n = e / (R * R), rem = e - n * (R * R), r = rem / R, r2 = rem - r * R;
+    float g = 0.f;
+    for (int j = 0; j < J; ++j) g = fmaf(__ldg(cor + n * J * R + j * R + r), __ldg(cor + n * J * R + j * R + r2), g);
+    sm[C::OFF_G + n * R * R + canon<R>(r, r2)] = g;
+  }
+  if (tid == 0) {
+    for (int s = 0; s <= C::NSLOT; ++s) tc::mbar_init(&full[s], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&misc[0], C::TCOLS);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = misc[0];
+  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);
+  const uint32_t sbase = tc::smem_u32(sm);
+  const uint32_t id_c = tc::idesc_tf32(128, R), id_g = tc::idesc_tf32(128, J), id_h = tc::idesc_tf32(128, R);
+  const uint64_t pol_stream = tc::policy_evict_first();
+  uint32_t mphase = 0, fphase = 0;  // fphase bit s: parity of slot s's next completion
+
+  const unsigned early = p.early_mask;
+  const int spare = (early >> (N - 1)) & 1u;  // the last mode double-buffers only when gathered early
+  auto slot_of = [&](int n, int pb) { return (n == N - 1 && pb) ? N : n; };
+  auto slot_addr = [&](int s) { return sbase + 4u * (uint32_t)(C::OFF_A + s * C::SLOT); };
+
+  // Row indices of a tile, one int per (mode, sample), so that an elected lane
+  // of each warp reads four rows with one LDS.128 and issues the warp's eight
+  // gather4 / scatter4 operations in a uniform loop.  Past-the-end samples
+  // carry row 0 (gathered, never written back).
+  auto stage_ids = [&](const RecReg<N, RW>& rr, int par) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) ids[(par * N + n) * 128 + tid] = rr.valid ? rr.idx[n] : 0;
+  };
+  auto gather = [&](int n, int s, int par) {
+    if (tid == 0) tc::mbar_expect_tx(&full[s], C::SLOT * 4);
+    if (elect_one()) {
+      const int4* id4 = reinterpret_cast<const int4*>(ids + (par * N + n) * 128 + warp * 32);
+      const uint32_t dst = slot_addr(s) + warp * 32 * C::ROWB, bar = tc::smem_u32(&full[s]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int4 r = id4[k];
+        tc::tma_gather4(dst + 4 * k * C::ROWB, &maps.m[n], r.x, r.y, r.z, r.w, bar);
+      }
+    }
+  };
+
+  const long long G = gridDim.x;
+  long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
+  if (tid == 0) misc[1] = atomicAdd(tile_ctr, 1u);
+  RecReg<N, RW> cur, nxt;
+  int v2 = load_vis<HV>(visit, n_visit, t2, pol_stream);
+  load_rec<N, RW>(cur, rec, load_vis<HV>(visit, n_visit, tile, pol_stream), tile_valid(n_visit, tile), base,
+                  pol_stream);
+  load_rec<N, RW>(nxt, rec, load_vis<HV>(visit, n_visit, t1, pol_stream), tile_valid(n_visit, t1), base, pol_stream);
+  int pb = 0, par = 0;
+  stage_ids(cur, 0);
+  __syncwarp();
+#pragma unroll
+  for (int n = 0; n < N; ++n)
+    if (early >> n & 1u) gather(n, slot_of(n, pb), 0);
+  __syncthreads();
+  long long t3 = 3 * G + misc[1];
+  while (tile * 128 < n_visit) {
+    TMA_STAMP(0);
+    unsigned claim = 0;
+    if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
+    // late modes (the hot ones by default) are read at the start of their own
+    // tile, which keeps their Hogwild read-to-write window short
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+      if (!(early >> n & 1u)) gather(n, slot_of(n, pb), par);
+    // the next tile's indices, for its early gathers during this tile
+    stage_ids(nxt, par ^ 1);
+    RecReg<N, RW> nnxt;
+    load_rec<N, RW>(nnxt, rec, v2, tile_valid(n_visit, t2), base, pol_stream);
+    v2 = load_vis<HV>(visit, n_visit, t3, pol_stream);
+    const bool full_tile = (tile + 1) * 128 <= n_visit;
+    TMA_STAMP(1);
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const int s = slot_of(n, pb);
+      tc::mbar_wait(&full[s], (fphase >> s) & 1u);
+      fphase ^= 1u << s;
+    }
+    TMA_STAMP(2);
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const uint32_t a = slot_addr(slot_of(n, pb));
+        const uint32_t b = sbase + 4u * (C::OFF_BT + n * R * J);
+#pragma unroll
+        for (int kk = 0; kk < J / 8; ++kk)
+          tc::mma_tf32(tbase + n * R, tc::smem_desc_sw<C::ROWB>(a + 32 * kk),
+                       tc::smem_desc(b + kk * 2 * (R * 16), R * 16, 128), id_c, kk > 0 ? 1u : 0u);
+      }
+      tc::mma_commit(mbar);
+    }
+    tc::mbar_wait(mbar, mphase);
+    mphase ^= 1;
+    tc::fence_after_sync();
+    TMA_STAMP(3);
+    float c[N][R];
+#pragma unroll
+    for (int n = 0; n < N; ++n) tc::tmem_ldh<R>(tlane + n * R, c[n]);
+
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      {
+        float w[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float v = 0.f;
+          bool first = true;
+#pragma unroll
+          for (int n0 = 0; n0 < N; ++n0)
+            if (n0 != n) {
+              v = first ? c[n0][r] : v * c[n0][r];
+              first = false;
+            }
+          w[r] = v;
+        }
+        tmem_st_row<R>(tlane + C::COL_W, w);
+      }
+      tc::tmem_wait_st();
+      // earlier write-backs have read their slots (slot n-1 is re-gathered below)
+      tc::bulk_wait_read();
+      tc::fence_before_sync();
+      TMA_STAMP(4 + 3 * n);
+      __syncthreads();
+      TMA_STAMP(5 + 3 * n);
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t bn = sbase + 4u * (C::OFF_BN + n * J * R);
+#pragma unroll
+        for (int kk = 0; kk < R / 8; ++kk)
+          tc::mma_tf32_ts(tbase + C::COL_G, tbase + C::COL_W + 8 * kk, tc::smem_desc(bn + kk * 2 * (J * 16), J * 16, 128),
+                          id_g, kk > 0 ? 1u : 0u);
+        // the refreshed c of the last mode is never read again: no h for it
+        if (n < N - 1) {
+          const uint32_t gg = sbase + 4u * (C::OFF_G + n * R * R);
+#pragma unroll
+          for (int kk = 0; kk < R / 8; ++kk)
+            tc::mma_tf32_ts(tbase + C::COL_H, tbase + C::COL_W + 8 * kk,
+                            tc::smem_desc(gg + kk * 2 * (R * 16), R * 16, 128), id_h, kk > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(mbar);
+      }
+      // every thread is past its mode-(n-1) update and that mode's write-back
+      // has read the slot: the next tile's rows can land there
+      if (n >= 1 && n - 1 < N - 1 && (early >> (n - 1) & 1u)) gather(n - 1, n - 1, par ^ 1);
+      if (n == N - 1 && spare) gather(N - 1, slot_of(N - 1, pb ^ 1), par ^ 1);
+      tc::mbar_wait(mbar, mphase);
+      mphase ^= 1;
+      tc::fence_after_sync();
+      TMA_STAMP(6 + 3 * n);
+      float g[J];
+      tc::tmem_ldh<J>(tlane + C::COL_G, g);
+      float* slot = sm + C::OFF_A + slot_of(n, pb) * C::SLOT;
+      float a[J];
+#pragma unroll
+      for (int q = 0; q < J / 4; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(slot + swz<J>(tid, q));
+        a[4 * q] = v.x;
+        a[4 * q + 1] = v.y;
+        a[4 * q + 2] = v.z;
+        a[4 * q + 3] = v.w;
+      }
+      float inter = 0.f;
+#pragma unroll
+      for (int j = 0; j < J; ++j) inter = fmaf(a[j], g[j], inter);
+      // a' = a - gamma (-x gs + lambda a + inter gs) = keep a + step gs
+      const float gm = p.gam[n], lm = p.lam[n];
+      const float keep = 1.f - gm * lm, step = gm * (cur.x - inter), shrink = -gm * lm;
+      const bool red = p.atomic_mask >> n & 1u;
+      if (red || !full_tile) {
+        // own row in natural order (it stays inside the row's swizzle span):
+        // the delta for add-reduced modes, the new row otherwise
+#pragma unroll
+        for (int q = 0; q < J / 4; ++q) {
+          float v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * q + u;
+            v[u] = red ? fmaf(step, g[j], shrink * a[j]) : fmaf(step, g[j], keep * a[j]);
+          }
+          *reinterpret_cast<float4*>(slot + tid * J + 4 * q) = make_float4(v[0], v[1], v[2], v[3]);
+        }
+        if (red && !p.bulk_red) {
+          // the warp's 32 deltas go out as red.add.v4 with CH = J/4 lanes per
+          // row (one L2 request per row; concurrent updates all land)
+          __syncwarp();
+          constexpr int CH = J / 4, RPI = 32 / CH;
+          const int cq = lane % CH, crow = lane / CH, wbase = tid & ~31;
+          const int me = cur.valid ? cur.idx[n] : -1;
+          int row[CH];
+          float4 v[CH];
+#pragma unroll
+          for (int k = 0; k < CH; ++k) row[k] = __shfl_sync(0xffffffffu, me, k * RPI + crow);
+#pragma unroll
+          for (int k = 0; k < CH; ++k)
+            v[k] = *reinterpret_cast<const float4*>(slot + (wbase + k * RPI + crow) * J + 4 * cq);
+#pragma unroll
+          for (int k = 0; k < CH; ++k)
+            if (row[k] >= 0) tc::red_add_v4(fac + p.foff[n] + (long long)row[k] * J + 4 * cq, v[k]);
+        } else {
+          // one bulk add-reduction (delta) or store (new row) per sample
+          tc::fence_async_smem();
+          if (cur.valid) {
+            float* dst = fac + p.foff[n] + (long long)cur.idx[n] * J;
+            const uint32_t src = slot_addr(slot_of(n, pb)) + tid * C::ROWB;
+            if (red)
+              tc::bulk_red_add(dst, src, C::ROWB);
+            else
+              tc::bulk_store(dst, src, C::ROWB);
+            tc::bulk_commit();
+          }
+        }
+      } else {
+        // new rows in place (swizzled), then the warp's rows go out as eight
+        // scatter4 stores issued by one lane
+#pragma unroll
+        for (int q = 0; q < J / 4; ++q) {
+          float v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = fmaf(step, g[4 * q + u], keep * a[4 * q + u]);
+          *reinterpret_cast<float4*>(slot + swz<J>(tid, q)) = make_float4(v[0], v[1], v[2], v[3]);
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (elect_one()) {
+          const int4* id4 = reinterpret_cast<const int4*>(ids + (par * N + n) * 128 + warp * 32);
+          const uint32_t src = slot_addr(slot_of(n, pb)) + warp * 32 * C::ROWB;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int4 r = id4[k];
+            tc::tma_scatter4(&maps.m[n], r.x, r.y, r.z, r.w, src + 4 * k * C::ROWB);
+          }
+          tc::bulk_commit();
+        }
+      }
+      if (n < N - 1) {
+        float h[R];
+        tc::tmem_ldh<R>(tlane + C::COL_H, h);
+#pragma unroll
+        for (int r = 0; r < R; ++r) c[n][r] = fmaf(step, h[r], keep * c[n][r]);
+      }
+    }
+    cur = nxt;
+    nxt = nnxt;
+    tile = t1;
+    t1 = t2;
+    t2 = t3;
+    pb ^= spare;
+    par ^= 1;
+    if (tid == 0) misc[1] = claim;
+    // late slots are re-gathered at the top of the next tile; the next c
+    // round overwrites TMEM columns this tile's last loads read
+    tc::bulk_wait_read();
+    tc::fence_before_sync();
+    TMA_STAMP(15);
+    __syncthreads();
+    t3 = 3 * G + misc[1];
+    ++ntile;
+  }
+  tc::bulk_wait_all();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tbase, C::TCOLS);
+  }
+}
+#undef TMA_STAMP
+
+// ---------------------------------------------------------------- host side --
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int encode_fn() {
+  if (g_encode) return 0;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+    set_error("cuTensorMapEncodeTiled is not available from the driver");
+    return 1;
+  }
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  return 0;
+}
+
+// One tensor map per factor matrix: [rows][J] fp32, box = one row, swizzle
+// span = one row (the operand-tile layout the MMA descriptors expect).
+static int encode_row_map(CUtensorMap* m, float* base, long long rows, int J) {
+  cuuint64_t dims[2] = {(cuuint64_t)J, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)J * 4};
+  cuuint32_t box[2] = {(cuuint32_t)J, 1};
+  cuuint32_t es[2] = {1, 1};
+  const CUtensorMapSwizzle sw = J == 8 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                : J == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                          : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d) for a %lld x %d factor matrix", (int)r, rows, J);
+    return 1;
+  }
+  return 0;
+}
+
+static std::atomic<unsigned> g_tma_ctr_slot{0};
+static const char* g_last_kernel = "none";
+const char* last_factor_kernel() { return g_last_kernel; }
+void note_factor_kernel(const char* name) { g_last_kernel = name; }
+
+template <int N, int J, int R>
+static int launch_tma(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                      const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+  using C = TmaCfg<N, J, R>;
+  if (encode_fn()) return 1;
+  (void)rw;
+  TmaParams<N> p;
+  for (int n = 0; n < N; ++n) {
+    p.foff[n] = md.foff[n];
+    p.gam[n] = gam[n];
+    p.lam[n] = lam[n];
+  }
+  p.dbg = reinterpret_cast<long long*>(tc_debug_buffer());
+  p.atomic_mask = hot_mode_mask(md);
+  p.early_mask = ~p.atomic_mask & ((1u << N) - 1u);
+  if (const char* e = getenv("SPTK_TMA_EARLY")) p.early_mask = (unsigned)strtoul(e, nullptr, 0) & ((1u << N) - 1u);
+  {
+    const char* e = getenv("SPTK_TMA_BULKRED");
+    p.bulk_red = e ? atoi(e) : 0;
+  }
+  // tensor maps, re-encoded only when the model buffer changes
+  static TmaMaps<N> maps;
+  static const float* maps_fac = nullptr;
+  static long long maps_foff[N];
+  bool same = maps_fac == fac;
+  for (int n = 0; n < N && same; ++n) same = maps_foff[n] == md.foff[n];
+  if (!same) {
+    for (int n = 0; n < N; ++n) {
+      const long long end = n + 1 < N ? md.foff[n + 1] : md.fac_size;
+      if (encode_row_map(&maps.m[n], fac + md.foff[n], (end - md.foff[n]) / J, J)) return 1;
+      maps_foff[n] = md.foff[n];
+    }
+    maps_fac = fac;
+  }
+  auto kfn = visit ? factor_tma_kernel<N, J, R, true> : factor_tma_kernel<N, J, R, false>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    for (auto f : {factor_tma_kernel<N, J, R, true>, factor_tma_kernel<N, J, R, false>}) {
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    per_sm = resident_ctas((const void*)kfn, C::SMEM, C::TCOLS, false);
+  }
+  const long long tiles = (n_visit + 127) / 128;
+  // persistent grid minus the CTA slots left to the side-stream samplers
+  int slots = (N == 3 && J >= 16) ? 16 : 148;
+  if (const char* e = getenv("SPTK_SAMPLER_SLOTS")) slots = atoi(e);
+  long long blocks = 148LL * per_sm - (per_sm >= 2 ? slots : 0);
+  if (const char* e = getenv("SPTK_TC_GRID")) blocks = atoll(e);
+  if (blocks < 1) blocks = 1;
+  if (blocks > tiles) blocks = tiles;
+  unsigned* ctr = nullptr;
+  SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tma_tile_ctr));
+  ctr += g_tma_ctr_slot.fetch_add(1u) & 63u;
+  SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+  kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, maps, ctr);
+  SPTK_CHECK_LAUNCH();
+  note_factor_kernel("factor_tma_kernel");
+  return 0;
+}
+
+// returns 1 if handled (uniform J = R in {8, 16}; N = 3, 4 at J = 16; N = 3, 6 at J = 8)
+int try_factor_tma(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                   const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc) {
+  const int N = md.n_modes, R = md.rcore, J = md.jr[0];
+  for (int n = 0; n < N; ++n)
+    if (md.jr[n] != J) return 0;
+  if (J != R || rw != rec_words(N)) return 0;
+#define SPTK_TMA_CASE(NN, JJ)                                                                    \
+  if (N == NN && J == JJ) {                                                                      \
+    *rc = launch_tma<NN, JJ, JJ>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);      \
+    return 1;                                                                                    \
+  }
+  SPTK_TMA_CASE(3, 16)
+  SPTK_TMA_CASE(4, 16)
+  SPTK_TMA_CASE(3, 8)
+  SPTK_TMA_CASE(6, 8)
+#undef SPTK_TMA_CASE
+  return 0;
+}
+
+}  // namespace sptk

@@ -51,6 +51,14 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
 int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
                   const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc);
 
+// factor_tma.cu (tcgen05 + TMA row traffic; returns 1 if it handled the launch)
+int try_factor_tma(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                   const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc);
+// name of the factor kernel the last factor_pass dispatched to
+const char* last_factor_kernel();
+void note_factor_kernel(const char* name);
+float* tc_debug_buffer();
+
 int set_tc_mode(int mode);
 int get_tc_mode();
 void set_tc_debug(float* buf);

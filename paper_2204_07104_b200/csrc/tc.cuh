@@ -174,3 +174,78 @@ __device__ __forceinline__ void red_add_v4(float* ptr, float4 v) {
 }
 }  // namespace tc
 }  // namespace sptk
+
+// ---- TMA row gathers / write-backs (tcgen05 factor kernel v6) ----------------------
+// A 2-D tensor map over one factor matrix ([rows][J] fp32, box {J, 1}, swizzle
+// span = one row: 32 / 64 / 128 B for J = 8 / 16 / 32) lets one instruction
+// move four arbitrary rows between global memory and a K-major swizzled
+// operand tile, without the SM's load/store pipe.
+#include <cuda.h>
+namespace sptk {
+namespace tc {
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int r0, int r1, int r2, int r3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, int r0, int r1, int r2, int r3, uint32_t src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+          map),
+      "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(src)
+      : "memory");
+}
+// contiguous global <- shared copies / element-wise fp32 add-reductions (16-byte multiples)
+__device__ __forceinline__ void bulk_store(void* gdst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_red_add(void* gdst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst), "r"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the shared-memory sources of every committed bulk group have been read
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// K-major operand in the swizzled layout the row gathers produce (8-row atoms
+// of ROWB-byte rows; SBO = 8 rows).  Layout codes: SW32 = 6, SW64 = 4, SW128 = 2.
+template <int ROWB>
+__device__ __forceinline__ uint64_t smem_desc_sw(uint32_t saddr) {
+  constexpr uint64_t layout = ROWB == 32 ? 6 : ROWB == 64 ? 4 : 2;
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ULL << 16) | ((uint64_t)((8 * ROWB) >> 4) << 32) | (1ULL << 46) |
+         (layout << 61);
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T (A: M x K in TMEM columns, one lane per row)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// registers -> TMEM: lane = thread's row, 8 / 16 consecutive fp32 columns
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+}  // namespace tc
+}  // namespace sptk
