@@ -238,8 +238,9 @@ def bench_ours(args, cfg):
     scale = default_init_scale(tr.values, order)
     model = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
     # +3: every timed epoch also draws the next epoch's samples (steady state)
+    workers = args.workers if args.workers else (world if world > 1 else 1)
     tcfg = TrainConfig(epochs=args.warmup + args.steps + 3, seed=1, update_mode=args.mode,
-                       workers=world if world > 1 else 1, alpha_a=cfg.get("alpha_a", 0.009))
+                       workers=workers, alpha_a=cfg.get("alpha_a", 0.009))
     sim = int(os.environ.get("BENCH_DSGD_SIM", "0"))
     if distributed:
         from paper_2204_07104_b200 import dist
@@ -321,7 +322,7 @@ def bench_ours(args, cfg):
             m2 = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
             torch.cuda.synchronize()
             t1 = time.perf_counter()
-            train(m2, DatasetSplit(tr, te), TrainConfig(epochs=k2, seed=1, update_mode=args.mode,
+            train(m2, DatasetSplit(tr, te), TrainConfig(epochs=k2, seed=1, update_mode=args.mode, workers=workers,
                                                         alpha_a=cfg.get("alpha_a", 0.009)))
             torch.cuda.synchronize()
             runs.append(time.perf_counter() - t1)
@@ -353,7 +354,7 @@ def bench_ours(args, cfg):
             "config": {"workload": cfg["workload"], "dims": list(cfg["dims"]), "nnz": cfg["nnz"],
                        "J": cfg["J"], "R": cfg["R"], "core_batch": min(cfg["nnz"], 1 << 20),
                        "update_mode": (args.mode if args.mode != "auto" else
-                                       "exact" if cfg["nnz"] <= (1 << 22) else "hogwild"), "parallelism": f"dsgd{world}" if world > 1 else "single",
+                                       "exact" if cfg["nnz"] <= (1 << 22) else "hogwild"), "parallelism": f"dsgd{world}" if world > 1 else "single", "workers": workers,
                        "l2": "inputs larger than L2 (records + visit order ~2 GB per epoch); the 32 MB "
                              "model is L2-resident by design"},
             "test_rmse": test_rmse,
@@ -381,6 +382,8 @@ def main():
     ap.add_argument("--config", default="nf", choices=sorted(CONFIGS))
     ap.add_argument("--rank", type=int, default=None, help="J = R override (rank sweep)")
     ap.add_argument("--alpha-a", type=float, default=None, help="factor learning-rate override")
+    ap.add_argument("--workers", type=int, default=None,
+                    help="DSGD workers W (the reference's TrainConfig.workers) on the GPU(s)")
     # auto = the library default: exact (sequential) up to 2^22 training
     # nonzeros (cfg1), Hogwild above (NF, Y4, O6)
     ap.add_argument("--mode", default="auto", choices=["hogwild", "exact", "auto"])

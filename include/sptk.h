@@ -78,6 +78,23 @@ void sptk_debug_tc_buffer(float* d_buf);
 /* default_rng(entropy).bit_generator state: {state_hi, state_lo, inc_hi, inc_lo}
  * (SeedSequence(entropy) -> PCG64 seeding), computed on the host. */
 int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_out[4]);
+
+/* DSGD block visit orders (workers > 1), one CTA per block in shared memory:
+ * for every block b of the table, default_rng([seed, 1, t, *coords[b]])
+ * .permutation(n_b) (trainer.py:196-199, bit-exact), written as
+ * visit[slot] = off_b + perm[p] at the round-interleaved slot
+ * out_base_b + sum_s min(n_s, p) + #{s < slot_b : n_s > p} over the blocks s
+ * of b's round.  d_jobs: n_jobs records of sptk_block_job_bytes() bytes
+ * {int64 off, int64 out_base, int32 n, int32 first, int32 m, int32 slot, int32 nmin
+ * (the round's smallest block), int32 pad},
+ * round-major (first = index of the round's first job, m <= 64 jobs per round);
+ * d_coords: n_jobs x order block coordinates; cap >= max n_b, <= 23000 (10 bytes
+ * of shared memory per nonzero); d_js: uint16 scratch for the j-sequences, one
+ * entry per record of the jobs (indexed like the records: off_b + p).
+ * Replaces the per-block permutation + `visit = ids[perm]` of the round loop. */
+size_t sptk_block_job_bytes(void);
+int sptk_block_perm(const void* d_jobs, const int32_t* d_coords, int n_jobs, int order, uint64_t seed, long long t,
+                    int cap, uint16_t* d_js, int32_t* d_visit, void* stream);
 size_t sptk_permutation_ws_bytes(long long n);
 /* d_out[n] (int32) = Generator.permutation(n) for the generator in h_state. */
 int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, void* d_ws, size_t ws_bytes,

@@ -10,6 +10,7 @@
 #include "../../include/sptk.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "pcg64.cuh"
 
 #include <stdlib.h>
 
@@ -26,22 +27,6 @@ void set_error(const char* fmt, ...) {
 }
 
 void count_launch(int n) { g_launches += n; }
-
-// numpy.random.bit_generator.SeedSequence (pool size 4) + PCG64 seeding
-// (pcg64_set_seed -> pcg_setseq_128_srandom_r).  Used by the reference at
-// trainer.py:196-198 and trainer.py:214 through np.random.default_rng.
-static uint32_t ss_hashmix(uint32_t v, uint32_t* hc) {
-  v ^= *hc;
-  *hc *= 0x931e8875u;
-  v *= *hc;
-  v ^= v >> 16;
-  return v;
-}
-static uint32_t ss_mix(uint32_t x, uint32_t y) {
-  uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
-  r ^= r >> 16;
-  return r;
-}
 
 static int build_model_desc(ModelDesc* md, const int64_t* h_foff, const int64_t* h_coff, const int64_t* h_jr,
                             int n_modes, int rcore) {
@@ -95,55 +80,26 @@ int sptk_get_tc_mode(void) { return get_tc_mode(); }
 const char* sptk_last_factor_kernel(void) { return last_factor_kernel(); }
 void sptk_debug_tc_buffer(float* d_buf) { set_tc_debug(d_buf); }
 
+// numpy SeedSequence + PCG64 seeding (pcg64.cuh); used by the reference at
+// trainer.py:196-198 and trainer.py:214 through np.random.default_rng.
 int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_out[4]) {
   uint32_t words[512];
-  int nw = 0;
-  for (int e = 0; e < n_entropy; ++e) {
-    uint64_t x = h_entropy[e];
-    if (x == 0) {
-      SPTK_REQUIRE(nw < 512, "entropy too long");
-      words[nw++] = 0;
-    }
-    while (x) {
-      SPTK_REQUIRE(nw < 512, "entropy too long");
-      words[nw++] = (uint32_t)(x & 0xffffffffu);
-      x >>= 32;
-    }
-  }
-  uint32_t pool[4];
-  uint32_t hc = 0x43b0d7e5u;
-  for (int i = 0; i < 4; ++i) pool[i] = ss_hashmix(i < nw ? words[i] : 0u, &hc);
-  for (int s = 0; s < 4; ++s)
-    for (int d = 0; d < 4; ++d)
-      if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], &hc));
-  for (int s = 4; s < nw; ++s)
-    for (int d = 0; d < 4; ++d) pool[d] = ss_mix(pool[d], ss_hashmix(words[s], &hc));
-  uint32_t out[8];
-  uint32_t hb = 0x8b51f9ddu;
-  for (int i = 0; i < 8; ++i) {
-    uint32_t v = pool[i % 4];
-    v ^= hb;
-    hb *= 0x58f38dedu;
-    v *= hb;
-    v ^= v >> 16;
-    out[i] = v;
-  }
-  uint64_t v64[4];
-  for (int k = 0; k < 4; ++k) v64[k] = (uint64_t)out[2 * k] | ((uint64_t)out[2 * k + 1] << 32);
-  typedef unsigned __int128 u128;
-  const u128 mult = (((u128)0x2360ED051FC65DA4ULL) << 64) | (u128)0x4385DF649FCCF645ULL;
-  u128 initstate = ((u128)v64[0] << 64) | v64[1];
-  u128 initseq = ((u128)v64[2] << 64) | v64[3];
-  u128 inc = (initseq << 1) | 1u;
-  u128 state = 0;
-  state = state * mult + inc;
-  state += initstate;
-  state = state * mult + inc;
-  h_state_out[0] = (uint64_t)(state >> 64);
-  h_state_out[1] = (uint64_t)state;
-  h_state_out[2] = (uint64_t)(inc >> 64);
-  h_state_out[3] = (uint64_t)inc;
+  const int nw = seedseq_words(h_entropy, n_entropy, words, 512);
+  SPTK_REQUIRE(nw >= 0, "entropy too long");
+  const Pcg64 g = seedseq_pcg64(words, nw);
+  h_state_out[0] = (uint64_t)(g.state >> 64);
+  h_state_out[1] = (uint64_t)g.state;
+  h_state_out[2] = (uint64_t)(g.inc >> 64);
+  h_state_out[3] = (uint64_t)g.inc;
   return 0;
+}
+
+size_t sptk_block_job_bytes(void) { return block_job_bytes(); }
+
+int sptk_block_perm(const void* d_jobs, const int32_t* d_coords, int n_jobs, int order, uint64_t seed, long long t,
+                    int cap, uint16_t* d_js, int32_t* d_visit, void* stream) {
+  return block_perm(d_jobs, d_coords, n_jobs, order, (unsigned long long)seed, t, cap, d_js, d_visit,
+                    (cudaStream_t)stream);
 }
 
 size_t sptk_permutation_ws_bytes(long long n) { return perm_ws_bytes(n); }

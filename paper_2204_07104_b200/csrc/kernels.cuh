@@ -24,6 +24,9 @@ int permutation_j(const uint64_t st[4], long long n, int* j_out, void* ws, size_
 size_t choice_ws_bytes(long long pop, long long k);
 int choice(const uint64_t st[4], long long pop, long long k, int shuffle, int* out, void* ws,
            size_t ws_bytes, int* path_out, cudaStream_t s);
+int block_perm(const void* d_jobs, const int* d_coords, int n_jobs, int order, unsigned long long seed,
+               long long t, int cap, uint16_t* d_js, int* d_visit, cudaStream_t s);
+size_t block_job_bytes();
 int u32_stream(const uint64_t st[4], unsigned long long q0, long long n, uint32_t* out, cudaStream_t s);
 int iota(int* out, long long n, int offset, cudaStream_t s);
 size_t scan_ws_bytes(long long n);

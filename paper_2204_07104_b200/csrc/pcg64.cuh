@@ -56,4 +56,69 @@ __device__ inline uint32_t pcg_u32_at(const Pcg64& g, uint64_t q) {
   return (q & 1) ? (uint32_t)(out >> 32) : (uint32_t)out;
 }
 
+// numpy.random.SeedSequence(entropy) (pool size 4) -> PCG64 seeding
+// (pcg64_set_seed -> pcg_setseq_128_srandom_r), as np.random.default_rng
+// does it (trainer.py:196-198, trainer.py:214).  Entropy values are split
+// into little-endian 32-bit words (0 -> one zero word); at most 64 words.
+__host__ __device__ inline uint32_t ss_hashmix(uint32_t v, uint32_t* hc) {
+  v ^= *hc;
+  *hc *= 0x931e8875u;
+  v *= *hc;
+  v ^= v >> 16;
+  return v;
+}
+__host__ __device__ inline uint32_t ss_mix(uint32_t x, uint32_t y) {
+  uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+  r ^= r >> 16;
+  return r;
+}
+// returns the number of 32-bit words, or -1 if the entropy is too long
+__host__ __device__ inline int seedseq_words(const uint64_t* ent, int n_ent, uint32_t* words, int cap) {
+  int nw = 0;
+  for (int e = 0; e < n_ent; ++e) {
+    uint64_t x = ent[e];
+    if (x == 0) {
+      if (nw >= cap) return -1;
+      words[nw++] = 0;
+    }
+    while (x) {
+      if (nw >= cap) return -1;
+      words[nw++] = (uint32_t)(x & 0xffffffffu);
+      x >>= 32;
+    }
+  }
+  return nw;
+}
+__host__ __device__ inline Pcg64 seedseq_pcg64(const uint32_t* words, int nw) {
+  uint32_t pool[4];
+  uint32_t hc = 0x43b0d7e5u;
+  for (int i = 0; i < 4; ++i) pool[i] = ss_hashmix(i < nw ? words[i] : 0u, &hc);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], &hc));
+  for (int s = 4; s < nw; ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = ss_mix(pool[d], ss_hashmix(words[s], &hc));
+  uint32_t out[8];
+  uint32_t hb = 0x8b51f9ddu;
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i % 4];
+    v ^= hb;
+    hb *= 0x58f38dedu;
+    v *= hb;
+    v ^= v >> 16;
+    out[i] = v;
+  }
+  uint64_t v64[4];
+  for (int k = 0; k < 4; ++k) v64[k] = (uint64_t)out[2 * k] | ((uint64_t)out[2 * k + 1] << 32);
+  const u128 initstate = ((u128)v64[0] << 64) | v64[1];
+  const u128 initseq = ((u128)v64[2] << 64) | v64[3];
+  Pcg64 g;
+  g.inc = (initseq << 1) | 1u;
+  g.state = 0;
+  g.state = g.state * pcg_mult() + g.inc;
+  g.state += initstate;
+  g.state = g.state * pcg_mult() + g.inc;
+  return g;
+}
+
 }  // namespace sptk

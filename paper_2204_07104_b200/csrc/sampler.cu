@@ -74,33 +74,44 @@ struct Seg {
 __device__ __forceinline__ void group_accept(int a, int y0, int y1, bool v0, bool v1, int cap,
                                              bool& acc0, bool& acc1) {
   const int lane = threadIdx.x & 31;
-  bool c0 = v0 && (long long)y0 >= (long long)a + 63;
-  bool r0 = !v0 || y0 < a;
-  bool c1 = v1 && (long long)y1 >= (long long)a + 63;
-  bool r1 = !v1 || y1 < a;
-  unsigned unc = __ballot_sync(FULLMASK, !(c0 || r0) || !(c1 || r1));
-  if (unc == 0) {
-    acc0 = c0;
-    acc1 = c1;
-  } else {
-    int cur = a;
-    acc0 = acc1 = false;
-#pragma unroll 1
-    for (int l = 0; l < 32; ++l) {
-      int yy0 = __shfl_sync(FULLMASK, y0, l), yy1 = __shfl_sync(FULLMASK, y1, l);
-      bool vv0 = __shfl_sync(FULLMASK, v0, l), vv1 = __shfl_sync(FULLMASK, v1, l);
-      bool x0 = vv0 && cur <= yy0;
-      cur += x0;
-      bool x1 = vv1 && cur <= yy1;
-      cur += x1;
-      if (lane == l) {
-        acc0 = x0;
-        acc1 = x1;
+  const unsigned lt = (1u << lane) - 1u;
+  // d = y - a: a word is accepted iff (accepts before it in the group) <= d.
+  // At most 63 words precede one, so d >= 63 accepts and d < 0 rejects for
+  // sure; the rest are resolved by bounds: with L / H the accepts before the
+  // word counting the undecided ones as rejected / accepted, d >= H accepts
+  // and d < L rejects.  The first undecided word has L == H, so every pass
+  // settles at least one (in practice one or two passes per group).
+  const long long d0 = (long long)y0 - a, d1 = (long long)y1 - a;
+  bool c0 = v0 && d0 >= 63, c1 = v1 && d1 >= 63;
+  bool u0 = v0 && d0 >= 0 && d0 < 63, u1 = v1 && d1 >= 0 && d1 < 63;
+  unsigned U0 = __ballot_sync(FULLMASK, u0), U1 = __ballot_sync(FULLMASK, u1);
+  while (U0 | U1) {
+    const unsigned A0 = __ballot_sync(FULLMASK, c0), A1 = __ballot_sync(FULLMASK, c1);
+    const int lo0 = __popc(A0 & lt) + __popc(A1 & lt);
+    const int hi0 = lo0 + __popc(U0 & lt) + __popc(U1 & lt);
+    const int lo1 = lo0 + (c0 ? 1 : 0), hi1 = hi0 + ((c0 || u0) ? 1 : 0);
+    if (u0) {
+      if (d0 >= hi0) {
+        c0 = true;
+        u0 = false;
+      } else if (d0 < lo0) {
+        u0 = false;
       }
     }
+    if (u1) {
+      if (d1 >= hi1) {
+        c1 = true;
+        u1 = false;
+      } else if (d1 < lo1) {
+        u1 = false;
+      }
+    }
+    U0 = __ballot_sync(FULLMASK, u0);
+    U1 = __ballot_sync(FULLMASK, u1);
   }
+  acc0 = c0;
+  acc1 = c1;
   if (cap != 0x7fffffff) {
-    unsigned lt = (1u << lane) - 1u;
     unsigned b0 = __ballot_sync(FULLMASK, acc0), b1 = __ballot_sync(FULLMASK, acc1);
     int before0 = __popc(b0 & lt) + __popc(b1 & lt);
     int before1 = before0 + (acc0 ? 1 : 0);
@@ -1815,5 +1826,224 @@ int iota(int* out, long long n, int offset, cudaStream_t s) {
   SPTK_CHECK_LAUNCH();
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// (5) DSGD block visit orders in shared memory.
+//
+// With W > 1 workers the reference draws one permutation per block,
+// default_rng([seed, 1, t, *block]).permutation(len(ids)) (trainer.py:
+// 196-199), and runs the W blocks of a round in parallel.  Blocks of up to
+// 23,000 nonzeros are done entirely by one CTA:
+//   j-sequence   one warp walks the PCG64 stream level by level (the same
+//                masked-rejection walk as walk_exact, with the lane states
+//                carried across levels) into J[1..n-1]
+//   apply        Fisher-Yates by target lists: counting sort of the steps by
+//                target, each list sorted (short), V(p) = root of the chain
+//                p -> smallest step > p targeting p (pointer jumping), then
+//                final[i] = V(previous step of i's list) or the target itself
+//   output       visit[slot] = block offset + final[p], where slot interleaves
+//                the round's blocks (the round's blocks share no rows, so
+//                interleaving them is the reference's parallel round; it also
+//                spreads the GPU's samples in flight over every block)
+// Two launches: the j-sequences (one warp per block, 2 bytes per nonzero of
+// global scratch), then the apply (one CTA per block, shared memory 10 bytes
+// per nonzero: 16-bit J / L / V, 32-bit counts).
+// ---------------------------------------------------------------------------
+struct BlockJob {
+  long long off;       // first record of the block (partitioned layout)
+  long long out_base;  // first visit slot of the block's round
+  int n;               // nonzeros in the block
+  int first;           // index of the round's first job (jobs are round-major)
+  int m;               // jobs in the round
+  int slot;            // this job's index within its round
+  int nmin;            // smallest block of the round (below it the interleave is p * m + slot)
+  int pad;
+};
+
+// one warp: J[hi - count] = draw for every level (numpy's random_interval)
+__device__ void block_jgen(const Pcg64& g, int n, uint16_t* J) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  if (n < 2) return;
+  u128 A32, C32;
+  pcg_jump_coeffs(g.inc, 32, &A32, &C32);
+  Pcg64 st;
+  st.inc = g.inc;
+  st.state = pcg_advance(g, (uint64_t)lane + 1);  // output m = lane
+  long long mbase = 0, qs = 0;
+  const int kb = 32 - __clz((unsigned)(n - 1));
+  for (int k = kb; k >= 1; --k) {
+    const int hi = min((1 << k) - 1, n - 1), lo = 1 << (k - 1), S = hi - lo + 1;
+    const unsigned mask = (1u << k) - 1u;
+    int a = 0;
+    while (a < S) {
+      const uint64_t out = pcg_xsl_rr(st.state);
+      const long long q0 = 2 * (mbase + lane), q1 = q0 + 1;
+      const bool v0 = q0 >= qs, v1 = q1 >= qs;
+      const unsigned u0 = (uint32_t)out & mask, u1 = (uint32_t)(out >> 32) & mask;
+      bool acc0, acc1;
+      group_accept(a, hi - (int)u0, hi - (int)u1, v0, v1, S, acc0, acc1);
+      const unsigned b0 = __ballot_sync(FULLMASK, acc0), b1 = __ballot_sync(FULLMASK, acc1);
+      const int before0 = __popc(b0 & lt) + __popc(b1 & lt), before1 = before0 + (acc0 ? 1 : 0);
+      if (acc0) J[hi - (a + before0)] = (uint16_t)u0;
+      if (acc1) J[hi - (a + before1)] = (uint16_t)u1;
+      const int total = __popc(b0) + __popc(b1);
+      if (a + total >= S) {
+        // the level ends inside this group; the next one continues after it
+        long long p = -1;
+        if (acc0 && a + before0 == S - 1) p = q0;
+        if (acc1 && a + before1 == S - 1) p = q1;
+        const unsigned who = __ballot_sync(FULLMASK, p >= 0);
+        qs = __shfl_sync(FULLMASK, p, __ffs(who) - 1) + 1;
+        a = S;
+        if (qs >= 2 * (mbase + 32)) {
+          st.state = st.state * A32 + C32;
+          mbase += 32;
+        }
+      } else {
+        a += total;
+        st.state = st.state * A32 + C32;
+        mbase += 32;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ Pcg64 block_seed(const BlockJob& jb, const int* __restrict__ coords, int order,
+                                              unsigned long long seed, long long t, long long b) {
+  uint64_t ent[3 + SPTK_MAX_MODES];
+  ent[0] = seed;
+  ent[1] = 1;
+  ent[2] = (uint64_t)t;
+  for (int d = 0; d < order; ++d) ent[3 + d] = (uint64_t)coords[b * order + d];
+  uint32_t words[64];
+  const int nw = seedseq_words(ent, 3 + order, words, 64);
+  return seedseq_pcg64(words, nw < 0 ? 0 : nw);
+}
+
+// j-sequences: one warp per block, into the block's slice of js (record order)
+#define BP_JW 8
+__global__ void __launch_bounds__(32 * BP_JW) block_jgen_kernel(const BlockJob* __restrict__ jobs, int n_jobs,
+                                                                 const int* __restrict__ coords, int order,
+                                                                 unsigned long long seed, long long t,
+                                                                 uint16_t* __restrict__ js) {
+  const long long b = (long long)blockIdx.x * BP_JW + (threadIdx.x >> 5);
+  if (b >= n_jobs) return;
+  const BlockJob jb = jobs[b];
+  const Pcg64 g = block_seed(jb, coords, order, seed, t, b);  // every lane, same value
+  block_jgen(g, jb.n, js + jb.off);
+  if ((threadIdx.x & 31) == 0 && jb.n > 0) js[jb.off] = 0;  // virtual step 0 (position 0 keeps what is left)
+}
+
+#define BP_T 256
+__global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restrict__ jobs,
+                                                        const uint16_t* __restrict__ js,
+                                                        int* __restrict__ visit, int cap) {
+  extern __shared__ __align__(16) unsigned char bp_sm[];
+  unsigned* C = reinterpret_cast<unsigned*>(bp_sm);           // [cap] counts -> list ends
+  uint16_t* J = reinterpret_cast<uint16_t*>(C + cap);         // [cap] targets, later final values
+  uint16_t* L = J + cap;                                      // [cap] target-sorted steps
+  uint16_t* V = L + cap;                                      // [cap] chain roots
+  __shared__ int sh[33];
+  __shared__ int sizes[64];
+  const BlockJob jb = jobs[blockIdx.x];
+  const int n = jb.n, tid = threadIdx.x;
+  if (tid < jb.m && tid < 64) sizes[tid] = jobs[jb.first + tid].n;
+  for (int p = tid; p < n; p += BP_T) {
+    C[p] = 0u;
+    J[p] = js[jb.off + p];
+  }
+  __syncthreads();
+  // counting sort of the steps by target
+  for (int i = tid; i < n; i += BP_T) atomicAdd(&C[J[i]], 1u);
+  __syncthreads();
+  {
+    const int per = (n + BP_T - 1) / BP_T, a = tid * per, z = min(n, a + per);
+    int run = 0;
+    for (int p = a; p < z; ++p) run += (int)C[p];
+    int tot;
+    int ex = block_excl_scan(run, sh, &tot);
+    for (int p = a; p < z; ++p) {
+      const int c = (int)C[p];
+      C[p] = (unsigned)ex;
+      ex += c;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += BP_T) L[atomicAdd(&C[J[i]], 1u)] = (uint16_t)i;
+  __syncthreads();
+  // per target: its steps in descending order (the order Fisher-Yates runs
+  // them); every step targeting p is >= p, so the smallest one above p is
+  // the last (or, after p's own step, the second to last)
+  for (int p = tid; p < n; p += BP_T) {
+    const int s0 = p ? (int)C[p - 1] : 0, s1 = (int)C[p];
+    for (int x = s0 + 1; x < s1; ++x) {
+      const uint16_t v = L[x];
+      int c = x - 1;
+      while (c >= s0 && L[c] < v) {
+        L[c + 1] = L[c];
+        --c;
+      }
+      L[c + 1] = v;
+    }
+    int par = p;
+    if (s1 > s0) par = (int)L[s1 - 1] > p ? (int)L[s1 - 1] : (s1 - s0 >= 2 ? (int)L[s1 - 2] : p);
+    V[p] = (uint16_t)par;
+  }
+  __syncthreads();
+  // V(p) = root of p's chain
+  for (;;) {
+    int changed = 0;
+    for (int p = tid; p < n; p += BP_T) {
+      const uint16_t v = V[p], w = V[v];
+      if (w != v) {
+        V[p] = w;
+        changed = 1;
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  // final[i]: the value its target held just before step i
+  for (int p = tid; p < n; p += BP_T) {
+    const int s0 = p ? (int)C[p - 1] : 0, s1 = (int)C[p];
+    for (int x = s0; x < s1; ++x) J[L[x]] = x == s0 ? (uint16_t)p : V[L[x - 1]];
+  }
+  __syncthreads();
+  // round-interleaved output: slot(p) = sum_s min(n_s, p) + #{s < slot : n_s > p}
+  const int m = min(jb.m, 64);
+  for (int p = tid; p < n; p += BP_T) {
+    long long pos = jb.out_base;
+    if (p < jb.nmin) {
+      pos += (long long)p * m + jb.slot;  // every block of the round still has entries
+    } else {
+      for (int s = 0; s < m; ++s) {
+        const int ns = sizes[s];
+        pos += ns < p ? ns : p;
+        if (s < jb.slot && ns > p) ++pos;
+      }
+    }
+    visit[pos] = (int)(jb.off + J[p]);
+  }
+}
+
+int block_perm(const void* d_jobs, const int* d_coords, int n_jobs, int order, unsigned long long seed,
+               long long t, int cap, uint16_t* d_js, int* d_visit, cudaStream_t s) {
+  SPTK_REQUIRE(n_jobs >= 0 && order >= 1 && order <= SPTK_MAX_MODES, "block_perm: bad arguments");
+  SPTK_REQUIRE(cap >= 1 && cap <= 23000, "block_perm: block capacity must be in [1, 23000]");
+  if (n_jobs == 0) return 0;
+  const BlockJob* jobs = (const BlockJob*)d_jobs;
+  block_jgen_kernel<<<(n_jobs + BP_JW - 1) / BP_JW, 32 * BP_JW, 0, s>>>(jobs, n_jobs, d_coords, order, seed, t, d_js);
+  SPTK_CHECK_LAUNCH();
+  const size_t smem = (size_t)cap * 10 + 16;
+  static size_t configured = 0;
+  if (smem > configured) {
+    SPTK_CUDA_TRY(cudaFuncSetAttribute(block_fy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  block_fy_kernel<<<n_jobs, BP_T, smem, s>>>(jobs, d_js, d_visit, cap);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+size_t block_job_bytes() { return sizeof(BlockJob); }
 
 }  // namespace sptk

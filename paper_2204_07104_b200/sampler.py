@@ -144,3 +144,52 @@ def u32_stream(entropy, n: int, q0: int = 0):
     out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
     check(_lib.load().sptk_u32_stream(sp, q0, n, ptr(out), stream_ptr()), "sptk_u32_stream")
     return out[:n]
+
+
+BLOCK_JOB_DTYPE = np.dtype([("off", "<i8"), ("out_base", "<i8"), ("n", "<i4"), ("first", "<i4"), ("m", "<i4"),
+                            ("slot", "<i4"), ("nmin", "<i4"), ("pad", "<i4")])
+BLOCK_PERM_MAX = 23000  # 10 bytes of shared memory per nonzero in one CTA
+
+
+class BlockOrders:
+    """Visit orders of every DSGD block of an epoch in one launch
+    (sptk_block_perm): block b's default_rng([seed, 1, t, *b]).permutation(n_b)
+    (trainer.py:196-199), mapped to record positions (visit = ids[perm], the
+    block's records lying at [off_b, off_b + n_b) in the partitioned layout)
+    and laid out round by round with the round's blocks interleaved.
+
+    rounds: list of rounds, each a list of (block tuple, off, n)."""
+
+    def __init__(self, rounds, order: int, device):
+        import torch
+
+        jobs, coords, base = [], [], 0
+        for rnd in rounds:
+            first, m = len(jobs), len(rnd)
+            if m > 64:
+                raise ValueError("at most 64 blocks per round")
+            nmin = min((n for _, _, n in rnd), default=0)
+            for slot, (block, off, n) in enumerate(rnd):
+                if n > BLOCK_PERM_MAX:
+                    raise ValueError(f"block of {n} nonzeros exceeds {BLOCK_PERM_MAX}")
+                jobs.append((off, base, n, first, m, slot, nmin, 0))
+                coords.append(tuple(int(c) for c in block))
+            base += sum(n for _, _, n in rnd)
+        self.total = base
+        self.n_jobs = len(jobs)
+        self.order = order
+        self.cap = max([j[2] for j in jobs], default=1)
+        if int(_lib.load().sptk_block_job_bytes()) != BLOCK_JOB_DTYPE.itemsize:
+            raise RuntimeError("BlockJob layout mismatch between libsptk and sampler.py")
+        tab = np.array(jobs, dtype=BLOCK_JOB_DTYPE)
+        self.jobs = torch.from_numpy(tab.view(np.uint8).copy()).to(device)
+        self.coords = torch.from_numpy(np.asarray(coords, dtype=np.int32).reshape(-1, order)).to(device)
+        # j-sequence scratch (uint16, indexed like the records)
+        span = max([j[0] + j[2] for j in jobs], default=1)
+        self.js = torch.empty(max(span, 1), dtype=torch.int16, device=device)
+
+    def draw(self, seed: int, t: int, out, stream=None) -> None:
+        """visit orders of epoch t into out[0:total] (int32, device)."""
+        check(_lib.load().sptk_block_perm(ptr(self.jobs), ptr(self.coords), self.n_jobs, self.order, int(seed),
+                                          int(t), max(self.cap, 1), ptr(self.js), ptr(out), stream_ptr(stream)),
+              "sptk_block_perm")

@@ -44,7 +44,8 @@ import numpy as np
 from . import _lib
 from ._lib import check, f64arr, i64arr, ptr, stream_ptr
 from .device import DeviceCoo, DeviceModel, eval_sums, rmse_mae_device
-from .sampler import Workspace, choice, fy_apply, pcg64_state, permutation_j, permutation_j_batch
+from .sampler import (BLOCK_PERM_MAX, BlockOrders, Workspace, choice, fy_apply, pcg64_state, permutation_j,
+                      permutation_j_batch)
 from .schedule import DevicePartition, round_schedule
 from .tensor import DatasetSplit, SparseTensorCoo
 from .tucker import TuckerModel
@@ -239,10 +240,21 @@ class EpochRunner:
                     self.nnz_local += cnt
             self.rounds.append(items)
         dev = self.dm.fac.device
+        # Flat DSGD (throughput mode, W > 1 workers on one GPU): every block's
+        # visit order comes from one shared-memory CTA (sptk_block_perm) and
+        # the epoch's factor phase is ONE pass over the rounds' visit lists
+        # laid end to end, each round's row-disjoint blocks interleaved -- the
+        # reference's W parallel workers per round (trainer.py:189-208).
+        self.flat = (self.m > 1 and self.mode == 0 and not self.f64 and owner_rank is None
+                     and _env_int("SPTK_FLAT", 1) == 1
+                     and all(len(items) <= 64 for items in self.rounds)
+                     and max((c for items in self.rounds for (_, _, c) in items), default=0) <= BLOCK_PERM_MAX)
+        self.block_orders = BlockOrders(self.rounds, self.order, dev) if self.flat else None
         # Sampler state (K2), double-buffered by epoch parity: Fisher-Yates
         # j-sequences (jbuf), visit orders (perm, laid out like the
-        # partitioned records) and core batches (psi).
-        self.jbuf = [torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
+        # partitioned records; flat: the epoch's visit list) and core batches (psi).
+        self.jbuf = [torch.empty(1 if self.flat else max(self.nnz, 1), dtype=torch.int32, device=dev)
+                     for _ in range(2)]
         self.perm = [torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
         self.k = min(self.nnz, int(config.core_batch_cap))
         # core batches run two epochs ahead (the Floyd/Lemire draw is a serial
@@ -267,12 +279,15 @@ class EpochRunner:
             offs = np.array([o - self.lo for o, _ in own] + [self.hi - self.lo], dtype=np.int32)
             self.fy_off = torch.from_numpy(offs).to(dev)
         self.ws_j, self.ws_fy, self.ws_psi = Workspace(dev), Workspace(dev), Workspace(dev)
-        if sum(len(items) for items in self.rounds) > 1:
+        if self.flat:
+            pass
+        elif sum(len(items) for items in self.rounds) > 1:
             ns, p_ns = i64arr([c for items in self.rounds for (_, _, c) in items])
             self.ws_j.get(int(Lb.sptk_permutation_j_batch_ws_bytes(p_ns, len(ns))))
         else:
             self.ws_j.get(int(Lb.sptk_permutation_j_ws_bytes(max_block)))
-        self.ws_fy.get(int(Lb.sptk_fy_apply_ws_bytes(self.hi - self.lo if self.batched_fy else max_block)))
+        if not self.flat:
+            self.ws_fy.get(int(Lb.sptk_fy_apply_ws_bytes(self.hi - self.lo if self.batched_fy else max_block)))
         if config.update_core and self.k < self.nnz:
             self.ws_psi.get(int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
         self.acc = torch.zeros(max(self.dm.cor_size, 1), dtype=torch.float64, device=dev)
@@ -336,7 +351,8 @@ class EpochRunner:
         (trainer.py:196-199).  Several blocks (DSGD) are drawn as one batch:
         their segment levels advance together, one launch per phase."""
         cfg = self.cfg
-        if "jseq" in self._skip and self.j_epoch[slot] is not None:
+        if self.flat or ("jseq" in self._skip and self.j_epoch[slot] is not None):
+            # (flat: the block CTAs draw their j-sequences themselves)
             self.j_epoch[slot] = t
             return
         items = [it for rnd in self.rounds for it in rnd]
@@ -355,7 +371,9 @@ class EpochRunner:
         if "perm" in self._skip and self.sampled_epoch[slot] is not None:
             self.sampled_epoch[slot] = t
             return
-        if self.batched_fy:
+        if self.flat:
+            self.block_orders.draw(self.cfg.seed, t, self.perm[slot], stream=stream)
+        elif self.batched_fy:
             lo, hi = self.lo, self.hi
             j = self.jbuf[slot][lo:hi]
             check(self.L.sptk_fy_globalize(ptr(j), ptr(self.fy_off), self.fy_off.numel() - 1, stream_ptr(stream)),
@@ -468,6 +486,19 @@ class EpochRunner:
         fn = L.sptk_factor_pass_f64 if self.f64 else L.sptk_factor_pass
         s = stream_ptr()
         processed = 0
+        if self.flat:
+            if self.factor_events is not None:
+                e0 = self.torch.cuda.Event(enable_timing=True)
+                e0.record()
+            check(fn(ptr(self.part.rec), self.part.rw, ptr(self.perm[slot]), self.nnz, 0, ptr(dm.fac), dm.p_foff,
+                     ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam, self.mode, s),
+                  "sptk_factor_pass")
+            if self.factor_events is not None:
+                e1 = self.torch.cuda.Event(enable_timing=True)
+                e1.record()
+                self.factor_events.append((e0, e1))
+            self.after_factor_phase()
+            return self.nnz
         for r, items in enumerate(self.rounds):
             for block, off, cnt in items:
                 if self.factor_events is not None:

@@ -202,3 +202,59 @@ def test_permutation_j_batch_equals_per_block():
             continue
         _, want = O.permutation(e, n, return_j=True)
         assert np.array_equal(got[o + 1:o + n], want[1:]), n
+
+
+def _interleave_reference(rounds, perms):
+    """Host restatement of the flattened DSGD visit list: per round, the
+    blocks' visit lists (off + perm) interleaved position by position."""
+    out = []
+    for rnd, prs in zip(rounds, perms):
+        longest = max((n for _, _, n in rnd), default=0)
+        for p in range(longest):
+            for (block, off, n), pr in zip(rnd, prs):
+                if p < n:
+                    out.append(off + pr[p])
+    return np.array(out, dtype=np.int64)
+
+
+@pytest.mark.parametrize("order,sizes_seed", [(3, 0), (4, 1), (2, 2)])
+def test_block_perm_matches_reference(order, sizes_seed):
+    """sptk_block_perm: every block's permutation equals
+    default_rng([seed,1,t,*block]).permutation(n) (via the pinned oracle),
+    placed at the round-interleaved slots."""
+    import torch
+
+    from paper_2204_07104_b200.sampler import BlockOrders
+
+    rng = np.random.default_rng(sizes_seed)
+    rounds, off = [], 0
+    for r in range(5):
+        rnd = []
+        for s in range(int(rng.integers(1, 9))):
+            n = int(rng.choice([0, 1, 2, 3, 17, 255, 256, 257, 1000, 4097, 20000]))
+            block = tuple(int(x) for x in rng.integers(0, 9, order))
+            rnd.append((block, off, n))
+            off += n
+        rounds.append(rnd)
+    bo = BlockOrders(rounds, order, "cuda")
+    out = torch.full((max(bo.total, 1),), -1, dtype=torch.int32, device="cuda")
+    seed, t = 12345, 3
+    bo.draw(seed, t, out)
+    got = out[:bo.total].cpu().numpy().astype(np.int64)
+    perms = [[O.permutation([seed, 1, t, *block], n) if n else np.zeros(0, np.int64) for block, _, n in rnd]
+             for rnd in rounds]
+    np.testing.assert_array_equal(got, _interleave_reference(rounds, perms))
+
+
+def test_block_perm_max_block():
+    """The largest block one CTA takes (23,000 nonzeros: 10 bytes of shared memory each), bit-exact."""
+    import torch
+
+    from paper_2204_07104_b200.sampler import BlockOrders
+
+    rounds = [[((3, 1, 4), 0, 23000), ((2, 7, 1), 23000, 1)]]
+    bo = BlockOrders(rounds, 3, "cuda")
+    out = torch.empty(bo.total, dtype=torch.int32, device="cuda")
+    bo.draw(7, 0, out)
+    perms = [[O.permutation([7, 1, 0, 3, 1, 4], 23000), O.permutation([7, 1, 0, 2, 7, 1], 1)]]
+    np.testing.assert_array_equal(out.cpu().numpy().astype(np.int64), _interleave_reference(rounds, perms))
