@@ -88,7 +88,7 @@ int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_o
  * {int64 off, int64 out_base, int32 n, int32 first, int32 m, int32 slot, int32 nmin
  * (the round's smallest block), int32 pad},
  * round-major (first = index of the round's first job, m <= 64 jobs per round);
- * d_coords: n_jobs x order block coordinates; cap >= max n_b, <= 23000 (10 bytes
+ * d_coords: n_jobs x order block coordinates; cap >= max n_b, <= 18000 (12 bytes
  * of shared memory per nonzero); d_js: uint16 scratch for the j-sequences, one
  * entry per record of the jobs (indexed like the records: off_b + p).
  * Replaces the per-block permutation + `visit = ids[perm]` of the round loop. */

@@ -56,16 +56,17 @@ struct TmaCfg {
   static constexpr int M = 128;
   static constexpr int ROWB = J * 4;       // bytes per row = swizzle span
   static constexpr int SLOT = M * J;       // floats per operand tile
-  static constexpr int NSLOT = N + 1;      // + a second slot for the last mode
+  static constexpr int NSLOT = N + 1;      // + a second slot for the last mode (only when it is gathered early)
   static constexpr int OFF_A = 0;          // slots first: 1024-byte aligned
-  static constexpr int OFF_BT = OFF_A + NSLOT * SLOT;  // N x (R rows x J), canonical
+  static constexpr int OFF_BT = OFF_A + N * SLOT;      // N x (R rows x J), canonical
   static constexpr int OFF_BN = OFF_BT + N * R * J;    // N x (J rows x R)
   static constexpr int OFF_G = OFF_BN + N * J * R;     // N x (R rows x R)
   static constexpr int OFF_BAR = (OFF_G + N * R * R + 1) & ~1;  // NSLOT + 1 mbarriers
   static constexpr int OFF_MISC = OFF_BAR + 2 * (NSLOT + 1);     // TMEM address, tile claim
   static constexpr int OFF_IDX = (OFF_MISC + 4 + 3) & ~3;         // [2][N][128] row indices (16-B aligned)
-  static constexpr int FLOATS = OFF_IDX + 2 * N * M;
-  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 1024;       // + alignment slack
+  static constexpr int OFF_SPARE = (OFF_IDX + 2 * N * M + 255) & ~255;  // the spare slot, last (1024-B aligned)
+  static constexpr size_t SMEM = (size_t)OFF_SPARE * 4 + 1024;          // + alignment slack
+  static constexpr size_t SMEM_SPARE = SMEM + (size_t)SLOT * 4;
   // TMEM columns: the c round writes c_0..c_{N-1} at n*R; afterwards W at 0,
   // gs at R, h at R + J (c lives in registers by then)
   static constexpr int COL_W = 0, COL_G = R, COL_H = R + J;
@@ -110,8 +111,18 @@ __device__ __forceinline__ bool elect_one() {
   } while (0)
 #endif
 
+// CTAs per SM the register budget is sized for: four (128 registers).  Five
+// (96 registers, ~100 bytes of spill) measured slower at N = 3, J = 16: NF
+// factor pass 7.8 -> 8.9 ms.
+#ifndef SPTK_TMA_MINB_3_16
+#define SPTK_TMA_MINB_3_16 4
+#endif
+template <int N, int J>
+constexpr int tma_min_blocks() {
+  return (N == 3 && J == 16) ? SPTK_TMA_MINB_3_16 : 4;
+}
 template <int N, int J, int R, bool HV>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
     factor_tma_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
                       float* __restrict__ fac, const float* __restrict__ cor, const __grid_constant__ TmaParams<N> p,
                       const __grid_constant__ TmaMaps<N> maps, unsigned* __restrict__ tile_ctr) {
@@ -160,7 +171,8 @@ __global__ void __launch_bounds__(128, 4)
   const unsigned early = p.early_mask;
   const int spare = (early >> (N - 1)) & 1u;  // the last mode double-buffers only when gathered early
   auto slot_of = [&](int n, int pb) { return (n == N - 1 && pb) ? N : n; };
-  auto slot_addr = [&](int s) { return sbase + 4u * (uint32_t)(C::OFF_A + s * C::SLOT); };
+  auto slot_off = [&](int s) { return s < N ? C::OFF_A + s * C::SLOT : C::OFF_SPARE; };
+  auto slot_addr = [&](int s) { return sbase + 4u * (uint32_t)slot_off(s); };
 
   // Row indices of a tile, one int per (mode, sample), so that an elected lane
   // of each warp reads four rows with one LDS.128 and issues the warp's eight
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(128, 4)
       TMA_STAMP(6 + 3 * n);
       float g[J];
       tc::tmem_ldh<J>(tlane + C::COL_G, g);
-      float* slot = sm + C::OFF_A + slot_of(n, pb) * C::SLOT;
+      float* slot = sm + slot_off(slot_of(n, pb));
       float a[J];
 #pragma unroll
       for (int q = 0; q < J / 4; ++q) {
@@ -487,13 +499,16 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
     maps_fac = fac;
   }
   auto kfn = visit ? factor_tma_kernel<N, J, R, true> : factor_tma_kernel<N, J, R, false>;
+  const size_t smem = (p.early_mask >> (N - 1) & 1u) ? C::SMEM_SPARE : C::SMEM;
   static int per_sm = 0;
-  if (!per_sm) {
+  static size_t per_sm_smem = 0;
+  if (per_sm_smem != smem) {
     for (auto f : {factor_tma_kernel<N, J, R, true>, factor_tma_kernel<N, J, R, false>}) {
-      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_SPARE));
       SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
-    per_sm = resident_ctas((const void*)kfn, C::SMEM, C::TCOLS, false);
+    per_sm = resident_ctas((const void*)kfn, smem, C::TCOLS, false);
+    per_sm_smem = smem;
   }
   const long long tiles = (n_visit + 127) / 128;
   // persistent grid minus the CTA slots left to the side-stream samplers
@@ -507,7 +522,7 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
   SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tma_tile_ctr));
   ctr += g_tma_ctr_slot.fetch_add(1u) & 63u;
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
-  kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, maps, ctr);
+  kfn<<<(unsigned)blocks, 128, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, maps, ctr);
   SPTK_CHECK_LAUNCH();
   note_factor_kernel("factor_tma_kernel");
   return 0;

@@ -1482,21 +1482,68 @@ struct LpPlan {
   int dir, nch, W;
 };
 
+// Lemire rejection threshold 2^32 mod R kept incrementally while the bound
+// R = rng + 1 steps by +-1 per accepted draw: with 2^32 = Q R + M, moving R
+// by one changes M by -Q / +Q and Q by at most one (valid while Q < R; small
+// bounds recompute).  Lets the walkers test a draw without the modulo the
+// rare "left < R" branch of lemire_ok needs (which, taken by any of 32 lanes,
+// stalled the whole warp on about half of the steps).
+struct LemireThr {
+  uint32_t R, Q, M;
+  __device__ __forceinline__ void set(uint32_t rng) {
+    R = rng + 1u;
+    const unsigned long long two32 = 1ULL << 32;
+    Q = (uint32_t)(two32 / R);
+    M = (uint32_t)(two32 - (unsigned long long)Q * R);
+  }
+  __device__ __forceinline__ void step(int dir) {
+    if (R < 65536u) {
+      set(R - 1u + (uint32_t)dir);
+      return;
+    }
+    if (dir > 0) {
+      if (M >= Q) {
+        M -= Q;
+      } else {
+        M = M + R + 1u - Q;
+        --Q;
+      }
+      ++R;
+    } else {
+      const unsigned long long mq = (unsigned long long)M + Q;
+      if (mq < (unsigned long long)(R - 1u)) {
+        M = (uint32_t)mq;
+      } else {
+        M = (uint32_t)(mq - (R - 1u));
+        ++Q;
+      }
+      --R;
+    }
+  }
+  // lemire_ok with the threshold at hand
+  __device__ __forceinline__ bool ok(uint32_t v, uint32_t* res) const {
+    const uint64_t m = (uint64_t)v * R;
+    *res = (uint32_t)(m >> 32);
+    return (uint32_t)m >= M;
+  }
+};
+
 __device__ __forceinline__ long long lp_walk(const uint32_t* __restrict__ v, long long vcap, long long t0,
                                              long long t1, long long q, long long base, int dir,
                                              uint32_t* __restrict__ out) {
   // walk draws [t0, t1) from word q; returns the position after the last
   // accepted word, or -1 on stream overflow
   long long t = t0;
-  uint32_t rng = (uint32_t)(base + (long long)dir * t);
+  LemireThr th;
+  th.set((uint32_t)(base + (long long)dir * t));
   while (t < t1) {
     if (q + 4 > vcap) {
       for (; t < t1 && q < vcap; ++q) {
         uint32_t r;
-        if (lemire_ok(__ldg(v + q), rng, &r)) {
+        if (th.ok(__ldg(v + q), &r)) {
           if (out) out[t] = r;
           ++t;
-          rng += (uint32_t)dir;
+          th.step(dir);
         }
       }
       return t < t1 ? -1 : q;
@@ -1508,10 +1555,10 @@ __device__ __forceinline__ long long lp_walk(const uint32_t* __restrict__ v, lon
     for (int u = 0; u < 4; ++u) {
       if (t < t1) {
         uint32_t r;
-        if (lemire_ok(w[u], rng, &r)) {
+        if (th.ok(w[u], &r)) {
           if (out) out[t] = r;
           ++t;
-          rng += (uint32_t)dir;
+          th.step(dir);
         }
         ++q;
       }
@@ -1833,7 +1880,7 @@ int iota(int* out, long long n, int offset, cudaStream_t s) {
 // With W > 1 workers the reference draws one permutation per block,
 // default_rng([seed, 1, t, *block]).permutation(len(ids)) (trainer.py:
 // 196-199), and runs the W blocks of a round in parallel.  Blocks of up to
-// 23,000 nonzeros are done entirely by one CTA:
+// 18,000 nonzeros are done entirely by one CTA:
 //   j-sequence   one warp walks the PCG64 stream level by level (the same
 //                masked-rejection walk as walk_exact, with the lane states
 //                carried across levels) into J[1..n-1]
@@ -1846,8 +1893,8 @@ int iota(int* out, long long n, int offset, cudaStream_t s) {
 //                interleaving them is the reference's parallel round; it also
 //                spreads the GPU's samples in flight over every block)
 // Two launches: the j-sequences (one warp per block, 2 bytes per nonzero of
-// global scratch), then the apply (one CTA per block, shared memory 10 bytes
-// per nonzero: 16-bit J / L / V, 32-bit counts).
+// global scratch), then the apply (one CTA per block, 12 bytes of shared
+// memory per nonzero), every phase of it parallel over the block's steps.
 // ---------------------------------------------------------------------------
 struct BlockJob {
   long long off;       // first record of the block (partitioned layout)
@@ -1860,49 +1907,67 @@ struct BlockJob {
   int pad;
 };
 
-// one warp: J[hi - count] = draw for every level (numpy's random_interval)
-__device__ void block_jgen(const Pcg64& g, int n, uint16_t* J) {
+// one warp: J[hi - count] = draw for every level (numpy's random_interval).
+// group_accept specialised to small blocks: 32-bit arithmetic and one set of
+// ballots per group.
+__device__ __forceinline__ void block_jgen(const Pcg64& g, int n, uint16_t* J) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   if (n < 2) return;
   u128 A32, C32;
   pcg_jump_coeffs(g.inc, 32, &A32, &C32);
-  Pcg64 st;
-  st.inc = g.inc;
-  st.state = pcg_advance(g, (uint64_t)lane + 1);  // output m = lane
-  long long mbase = 0, qs = 0;
+  u128 state = pcg_advance(g, (uint64_t)lane + 1);  // output m = lane
+  int mbase = 0, qs = 0;
   const int kb = 32 - __clz((unsigned)(n - 1));
   for (int k = kb; k >= 1; --k) {
-    const int hi = min((1 << k) - 1, n - 1), lo = 1 << (k - 1), S = hi - lo + 1;
+    const int hi = min((1 << k) - 1, n - 1), S = hi - (1 << (k - 1)) + 1;
     const unsigned mask = (1u << k) - 1u;
     int a = 0;
     while (a < S) {
-      const uint64_t out = pcg_xsl_rr(st.state);
-      const long long q0 = 2 * (mbase + lane), q1 = q0 + 1;
-      const bool v0 = q0 >= qs, v1 = q1 >= qs;
+      const uint64_t out = pcg_xsl_rr(state);
+      const int q0 = 2 * (mbase + lane);
       const unsigned u0 = (uint32_t)out & mask, u1 = (uint32_t)(out >> 32) & mask;
-      bool acc0, acc1;
-      group_accept(a, hi - (int)u0, hi - (int)u1, v0, v1, S, acc0, acc1);
-      const unsigned b0 = __ballot_sync(FULLMASK, acc0), b1 = __ballot_sync(FULLMASK, acc1);
-      const int before0 = __popc(b0 & lt) + __popc(b1 & lt), before1 = before0 + (acc0 ? 1 : 0);
-      if (acc0) J[hi - (a + before0)] = (uint16_t)u0;
-      if (acc1) J[hi - (a + before1)] = (uint16_t)u1;
+      const int d0 = hi - (int)u0 - a, d1 = hi - (int)u1 - a;  // accept iff (accepts before) <= d
+      const bool v0 = q0 >= qs, v1 = q0 + 1 >= qs;
+      bool c0 = v0 && d0 >= 63, c1 = v1 && d1 >= 63;
+      bool x0 = v0 && (unsigned)d0 < 63u, x1 = v1 && (unsigned)d1 < 63u;
+      unsigned X0 = __ballot_sync(FULLMASK, x0), X1 = __ballot_sync(FULLMASK, x1);
+      while (X0 | X1) {
+        const unsigned A0 = __ballot_sync(FULLMASK, c0), A1 = __ballot_sync(FULLMASK, c1);
+        const int lo0 = __popc(A0 & lt) + __popc(A1 & lt), hi0 = lo0 + __popc(X0 & lt) + __popc(X1 & lt);
+        const int lo1 = lo0 + (c0 ? 1 : 0), hi1 = hi0 + ((c0 || x0) ? 1 : 0);
+        if (x0 && (d0 >= hi0 || d0 < lo0)) {
+          c0 = d0 >= hi0;
+          x0 = false;
+        }
+        if (x1 && (d1 >= hi1 || d1 < lo1)) {
+          c1 = d1 >= hi1;
+          x1 = false;
+        }
+        X0 = __ballot_sync(FULLMASK, x0);
+        X1 = __ballot_sync(FULLMASK, x1);
+      }
+      const unsigned b0 = __ballot_sync(FULLMASK, c0), b1 = __ballot_sync(FULLMASK, c1);
+      const int before0 = a + __popc(b0 & lt) + __popc(b1 & lt), before1 = before0 + (c0 ? 1 : 0);
       const int total = __popc(b0) + __popc(b1);
+      // accepts past the level's S-th are not this level's
+      if (c0 && before0 < S) J[hi - before0] = (uint16_t)u0;
+      if (c1 && before1 < S) J[hi - before1] = (uint16_t)u1;
       if (a + total >= S) {
         // the level ends inside this group; the next one continues after it
-        long long p = -1;
-        if (acc0 && a + before0 == S - 1) p = q0;
-        if (acc1 && a + before1 == S - 1) p = q1;
+        int p = -1;
+        if (c0 && before0 == S - 1) p = q0;
+        if (c1 && before1 == S - 1) p = q0 + 1;
         const unsigned who = __ballot_sync(FULLMASK, p >= 0);
         qs = __shfl_sync(FULLMASK, p, __ffs(who) - 1) + 1;
         a = S;
         if (qs >= 2 * (mbase + 32)) {
-          st.state = st.state * A32 + C32;
+          state = state * A32 + C32;
           mbase += 32;
         }
       } else {
         a += total;
-        st.state = st.state * A32 + C32;
+        state = state * A32 + C32;
         mbase += 32;
       }
     }
@@ -1936,14 +2001,18 @@ __global__ void __launch_bounds__(32 * BP_JW) block_jgen_kernel(const BlockJob* 
 }
 
 #define BP_T 256
+// Shared memory per nonzero: J (target, later the result), L (steps grouped by
+// target), S (each group sorted by step, descending), V (chain roots): 16-bit;
+// C (group ends): 32-bit -- 12 bytes.
 __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restrict__ jobs,
                                                         const uint16_t* __restrict__ js,
                                                         int* __restrict__ visit, int cap) {
   extern __shared__ __align__(16) unsigned char bp_sm[];
-  unsigned* C = reinterpret_cast<unsigned*>(bp_sm);           // [cap] counts -> list ends
-  uint16_t* J = reinterpret_cast<uint16_t*>(C + cap);         // [cap] targets, later final values
-  uint16_t* L = J + cap;                                      // [cap] target-sorted steps
-  uint16_t* V = L + cap;                                      // [cap] chain roots
+  unsigned* C = reinterpret_cast<unsigned*>(bp_sm);  // [cap] counts -> group ends
+  uint16_t* J = reinterpret_cast<uint16_t*>(C + cap);
+  uint16_t* L = J + cap;
+  uint16_t* S = L + cap;
+  uint16_t* V = S + cap;
   __shared__ int sh[33];
   __shared__ int sizes[64];
   const BlockJob jb = jobs[blockIdx.x];
@@ -1952,9 +2021,9 @@ __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restri
   for (int p = tid; p < n; p += BP_T) {
     C[p] = 0u;
     J[p] = js[jb.off + p];
+    V[p] = (uint16_t)p;  // no step above p targets p: p keeps its own value
   }
   __syncthreads();
-  // counting sort of the steps by target
   for (int i = tid; i < n; i += BP_T) atomicAdd(&C[J[i]], 1u);
   __syncthreads();
   {
@@ -1972,23 +2041,24 @@ __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restri
   __syncthreads();
   for (int i = tid; i < n; i += BP_T) L[atomicAdd(&C[J[i]], 1u)] = (uint16_t)i;
   __syncthreads();
-  // per target: its steps in descending order (the order Fisher-Yates runs
-  // them); every step targeting p is >= p, so the smallest one above p is
-  // the last (or, after p's own step, the second to last)
-  for (int p = tid; p < n; p += BP_T) {
-    const int s0 = p ? (int)C[p - 1] : 0, s1 = (int)C[p];
-    for (int x = s0 + 1; x < s1; ++x) {
-      const uint16_t v = L[x];
-      int c = x - 1;
-      while (c >= s0 && L[c] < v) {
-        L[c + 1] = L[c];
-        --c;
-      }
-      L[c + 1] = v;
+  // each step's place in its target's group, largest step first (the order
+  // Fisher-Yates runs them): rank = number of larger steps in the group
+  for (int i = tid; i < n; i += BP_T) {
+    const int t = J[i], s0 = t ? (int)C[t - 1] : 0, s1 = (int)C[t];
+    int rank = 0;
+    for (int x = s0; x < s1; ++x) rank += (int)L[x] > i;
+    S[s0 + rank] = (uint16_t)i;
+  }
+  __syncthreads();
+  // every step targeting t is >= t: the smallest step above t (t's parent)
+  // is the last of the group, or the second to last after t's own step
+  for (int t = tid; t < n; t += BP_T) {
+    const int s0 = t ? (int)C[t - 1] : 0, s1 = (int)C[t];
+    if (s1 > s0) {
+      const int last = S[s1 - 1];
+      if (last > t) V[t] = (uint16_t)last;
+      else if (s1 - s0 >= 2) V[t] = S[s1 - 2];
     }
-    int par = p;
-    if (s1 > s0) par = (int)L[s1 - 1] > p ? (int)L[s1 - 1] : (s1 - s0 >= 2 ? (int)L[s1 - 2] : p);
-    V[p] = (uint16_t)par;
   }
   __syncthreads();
   // V(p) = root of p's chain
@@ -2003,10 +2073,10 @@ __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restri
     }
     if (!__syncthreads_or(changed)) break;
   }
-  // final[i]: the value its target held just before step i
-  for (int p = tid; p < n; p += BP_T) {
-    const int s0 = p ? (int)C[p - 1] : 0, s1 = (int)C[p];
-    for (int x = s0; x < s1; ++x) J[L[x]] = x == s0 ? (uint16_t)p : V[L[x - 1]];
+  // result[i]: the value its target held just before step i (L is free now)
+  for (int x = tid; x < n; x += BP_T) {
+    const int i = S[x], t = J[i], s0 = t ? (int)C[t - 1] : 0;
+    L[i] = x == s0 ? (uint16_t)t : V[S[x - 1]];
   }
   __syncthreads();
   // round-interleaved output: slot(p) = sum_s min(n_s, p) + #{s < slot : n_s > p}
@@ -2022,19 +2092,19 @@ __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restri
         if (s < jb.slot && ns > p) ++pos;
       }
     }
-    visit[pos] = (int)(jb.off + J[p]);
+    visit[pos] = (int)(jb.off + L[p]);
   }
 }
 
 int block_perm(const void* d_jobs, const int* d_coords, int n_jobs, int order, unsigned long long seed,
                long long t, int cap, uint16_t* d_js, int* d_visit, cudaStream_t s) {
   SPTK_REQUIRE(n_jobs >= 0 && order >= 1 && order <= SPTK_MAX_MODES, "block_perm: bad arguments");
-  SPTK_REQUIRE(cap >= 1 && cap <= 23000, "block_perm: block capacity must be in [1, 23000]");
+  SPTK_REQUIRE(cap >= 1 && cap <= 18000, "block_perm: block capacity must be in [1, 18000]");
   if (n_jobs == 0) return 0;
   const BlockJob* jobs = (const BlockJob*)d_jobs;
   block_jgen_kernel<<<(n_jobs + BP_JW - 1) / BP_JW, 32 * BP_JW, 0, s>>>(jobs, n_jobs, d_coords, order, seed, t, d_js);
   SPTK_CHECK_LAUNCH();
-  const size_t smem = (size_t)cap * 10 + 16;
+  const size_t smem = (size_t)cap * 12 + 16;
   static size_t configured = 0;
   if (smem > configured) {
     SPTK_CUDA_TRY(cudaFuncSetAttribute(block_fy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -231,7 +231,7 @@ def test_block_perm_matches_reference(order, sizes_seed):
     for r in range(5):
         rnd = []
         for s in range(int(rng.integers(1, 9))):
-            n = int(rng.choice([0, 1, 2, 3, 17, 255, 256, 257, 1000, 4097, 20000]))
+            n = int(rng.choice([0, 1, 2, 3, 17, 255, 256, 257, 1000, 4097, 17000]))
             block = tuple(int(x) for x in rng.integers(0, 9, order))
             rnd.append((block, off, n))
             off += n
@@ -247,14 +247,14 @@ def test_block_perm_matches_reference(order, sizes_seed):
 
 
 def test_block_perm_max_block():
-    """The largest block one CTA takes (23,000 nonzeros: 10 bytes of shared memory each), bit-exact."""
+    """The largest block one CTA takes (18,000 nonzeros: 12 bytes of shared memory each), bit-exact."""
     import torch
 
     from paper_2204_07104_b200.sampler import BlockOrders
 
-    rounds = [[((3, 1, 4), 0, 23000), ((2, 7, 1), 23000, 1)]]
+    rounds = [[((3, 1, 4), 0, 18000), ((2, 7, 1), 18000, 1)]]
     bo = BlockOrders(rounds, 3, "cuda")
     out = torch.empty(bo.total, dtype=torch.int32, device="cuda")
     bo.draw(7, 0, out)
-    perms = [[O.permutation([7, 1, 0, 3, 1, 4], 23000), O.permutation([7, 1, 0, 2, 7, 1], 1)]]
+    perms = [[O.permutation([7, 1, 0, 3, 1, 4], 18000), O.permutation([7, 1, 0, 2, 7, 1], 1)]]
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.int64), _interleave_reference(rounds, perms))
