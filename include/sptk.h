@@ -147,6 +147,22 @@ int sptk_u32_stream(const uint64_t h_state[4], unsigned long long q0, long long 
  * it against its streams (the copy runs on internal streams). */
 int sptk_h2d(void* d_dst, const void* h_src, size_t bytes, int threads);
 
+/* ---- COO text ingestion (host) ---------------------------------------- */
+/* load_coo(path, index_base) (coo.py:90-148), multi-threaded: the file is
+ * memory-mapped and parsed by `threads` host threads (0: all hardware
+ * threads) with the reference's grammar and error order.  Returns 0; 1 = the
+ * reference's CooFormatError (sptk_last_error(): "line N: <message>", the
+ * earliest bad line in file order; N = 0 for whole-file errors); 2 = OS error
+ * (open/mmap); 3 = an index outside int64 (the reference's OverflowError).
+ * On success *handle owns the entries: sptk_coo_text_dims reads the dims (the
+ * "# dims:" header if any, else max index + 1) and sptk_coo_text_take copies
+ * indices (int64 [nnz, order], 0-based, C order) and values (float64 [nnz])
+ * in file order into caller memory and frees the handle. */
+int sptk_coo_text_parse(const char* path, int index_base, int threads, void** handle, int64_t* nnz, int* order);
+int sptk_coo_text_dims(void* handle, int64_t* dims, int* from_header);
+int sptk_coo_text_take(void* handle, int64_t* indices, double* values, int threads);
+void sptk_coo_text_free(void* handle);
+
 /* ---- K1: partition + device layout ------------------------------------ */
 size_t sptk_partition_ws_bytes(long long nnz, int order, long long m);
 /* d_idx int64 [nnz, order], d_vals f64 [nnz] -> d_rec (block-grouped records),

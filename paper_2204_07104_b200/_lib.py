@@ -52,6 +52,11 @@ SIGNATURES = {
                                    ctypes.POINTER(ctypes.c_int), _vp]),
     "sptk_u32_stream": (ctypes.c_int, [_u64p, ctypes.c_ulonglong, _i64, _vp, _vp]),
     "sptk_h2d": (ctypes.c_int, [_vp, _vp, ctypes.c_size_t, ctypes.c_int]),
+    "sptk_coo_text_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp),
+                                           _i64p, ctypes.POINTER(ctypes.c_int)]),
+    "sptk_coo_text_dims": (ctypes.c_int, [_vp, _i64p, ctypes.POINTER(ctypes.c_int)]),
+    "sptk_coo_text_take": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int]),
+    "sptk_coo_text_free": (None, [_vp]),
     "sptk_partition_ws_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int, _i64]),
     "sptk_partition": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, _i64p, _i64, ctypes.c_int, _vp, _vp,
                                       _vp, _vp, _vp, ctypes.c_size_t, _vp]),

@@ -9,7 +9,6 @@ layout used by the kernels is built by ``schedule.build_partition`` /
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -97,63 +96,44 @@ def empty_like(tensor: SparseTensorCoo) -> SparseTensorCoo:
 
 # ------------------------------------------------------------------ text I/O
 
-def _records(fh):
-    """Yield (line number, tokens) for data lines and ('dims', values) headers."""
-    for lineno, raw in enumerate(fh, start=1):
-        text = raw.strip()
-        if not text:
-            continue
-        if text[0] == "#":
-            body = text[1:].strip()
-            if body[:5].lower() == "dims:":
-                try:
-                    yield lineno, ("dims", tuple(int(t) for t in body[5:].split()))
-                except ValueError:
-                    raise CooFormatError(f"line {lineno}: bad dims header") from None
-            continue
-        yield lineno, text.split()
+def load_coo(path, index_base: int = 1, threads: int = 0) -> SparseTensorCoo:
+    """Read ``i_1 .. i_N value`` lines (``#`` comments, optional ``# dims:``),
+    the reference's text format and errors (coo.py:90-148).
 
+    Parsed natively (libsptk ``sptk_coo_text_parse``: memory-mapped file,
+    ``threads`` parser threads, 0 = all) with the reference's grammar; the
+    CooFormatError raised names the earliest bad line, as the reference's
+    sequential reader would."""
+    import ctypes
+    import os
 
-def load_coo(path, index_base: int = 1) -> SparseTensorCoo:
-    """Read ``i_1 .. i_N value`` lines (``#`` comments, optional ``# dims:``)."""
+    from . import _lib
+
     if index_base not in (0, 1):
         raise ValueError("index_base must be 0 or 1")
-    header = None
-    coords: list[list[int]] = []
-    vals: list[float] = []
-    width = None
-    with open(path) as fh:
-        for lineno, item in _records(fh):
-            if isinstance(item, tuple):
-                header = item[1]
-                continue
-            if width is None:
-                width = len(item)
-                if width < 3:
-                    raise CooFormatError(f"line {lineno}: need at least 2 indices and a value")
-            if len(item) != width:
-                raise CooFormatError(f"line {lineno}: expected {width} tokens, got {len(item)}")
-            try:
-                c = [int(t) for t in item[:-1]]
-                v = float(item[-1])
-            except ValueError:
-                raise CooFormatError(f"line {lineno}: unparseable token") from None
-            if min(c) < index_base:
-                raise CooFormatError(f"line {lineno}: index below base {index_base}")
-            if not math.isfinite(v):
-                raise CooFormatError(f"line {lineno}: non-finite value")
-            coords.append([k - index_base for k in c])
-            vals.append(v)
-    if not coords:
-        raise CooFormatError("no entries in file")
-    idx = np.array(coords, dtype=np.int64)
-    if header is None:
-        dims = tuple(int(x) + 1 for x in idx.max(axis=0))
-    elif len(header) != width - 1:
-        raise CooFormatError("dims header length does not match entry order")
-    else:
-        dims = header
-    return SparseTensorCoo(dims, idx, np.array(vals, dtype=np.float64))
+    L = _lib.load()
+    handle = ctypes.c_void_p()
+    nnz = ctypes.c_int64()
+    order = ctypes.c_int()
+    rc = L.sptk_coo_text_parse(os.fsencode(path), int(index_base), int(threads), ctypes.byref(handle),
+                               ctypes.byref(nnz), ctypes.byref(order))
+    if rc != 0:
+        msg = L.sptk_last_error().decode(errors="replace")
+        if rc == 1:
+            raise CooFormatError(msg[len("line 0: "):] if msg.startswith("line 0: ") else msg)
+        if rc == 3:
+            raise OverflowError(msg)
+        if not os.path.exists(path):
+            raise FileNotFoundError(2, "No such file or directory", str(path))
+        raise OSError(msg)
+    n, N = int(nnz.value), int(order.value)
+    dims = np.zeros(N, dtype=np.int64)
+    hdr = ctypes.c_int()
+    L.sptk_coo_text_dims(handle, dims.ctypes.data_as(_lib._i64p), ctypes.byref(hdr))
+    idx = np.empty((n, N), dtype=np.int64)
+    vals = np.empty(n, dtype=np.float64)
+    L.sptk_coo_text_take(handle, idx.ctypes.data, vals.ctypes.data, int(threads))
+    return SparseTensorCoo(tuple(int(d) for d in dims), idx, vals)
 
 
 def write_coo(tensor: SparseTensorCoo, path, index_base: int = 1) -> None:
