@@ -95,6 +95,12 @@ int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_o
 size_t sptk_block_job_bytes(void);
 int sptk_block_perm(const void* d_jobs, const int32_t* d_coords, int n_jobs, int order, uint64_t seed, long long t,
                     int cap, uint16_t* d_js, int32_t* d_visit, void* stream);
+/* The same round-interleaved visit list from per-block visit orders already
+ * in the partitioned layout (d_perm[off_b + p]; entries relative to off_b, or
+ * to rel_lo when rel_lo >= 0): for blocks above sptk_block_perm's capacity,
+ * whose orders come from sptk_permutation_j_batch + sptk_fy_apply. */
+int sptk_interleave_rounds(const void* d_jobs, int n_jobs, const int32_t* d_perm, long long rel_lo,
+                           int32_t* d_visit, void* stream);
 size_t sptk_permutation_ws_bytes(long long n);
 /* d_out[n] (int32) = Generator.permutation(n) for the generator in h_state. */
 int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, void* d_ws, size_t ws_bytes,
@@ -187,6 +193,24 @@ int sptk_factor_pass_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, l
                          double* d_fac, const int64_t* h_foff, const double* d_cor, const int64_t* h_coff,
                          const int64_t* h_jr, int n_modes, int rcore, const double* h_gammas,
                          const double* h_lambdas, int mode, void* stream);
+
+/* Exact (sequential-equivalent) factor pass across the whole GPU: the result
+ * equals mode 1 of sptk_factor_pass (the reference's strictly sequential
+ * loop, _loops.py:17-63, bit for bit) but every sample runs as soon as the
+ * earlier samples sharing one of its rows are done (per-mode predecessors
+ * from a stable sort of the visit positions by row), so the critical path is
+ * the longest row chain instead of the visit length.  d_ws: at least
+ * sptk_factor_pass_exact_ws_bytes(n_visit, n_modes) bytes. */
+size_t sptk_factor_pass_exact_ws_bytes(long long n_visit, int n_modes);
+int sptk_factor_pass_exact(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, long long base,
+                           float* d_fac, const int64_t* h_foff, const float* d_cor, const int64_t* h_coff,
+                           const int64_t* h_jr, int n_modes, int rcore, const double* h_gammas,
+                           const double* h_lambdas, void* d_ws, size_t ws_bytes, void* stream);
+int sptk_factor_pass_exact_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit,
+                               long long base, double* d_fac, const int64_t* h_foff, const double* d_cor,
+                               const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore,
+                               const double* h_gammas, const double* h_lambdas, void* d_ws, size_t ws_bytes,
+                               void* stream);
 
 /* ---- K4/K5: core gradient + apply ------------------------------------- */
 size_t sptk_core_ws_bytes(const int64_t* h_jr, int n_modes, int rcore, int exact_chunks);

@@ -37,6 +37,7 @@ SIGNATURES = {
     "sptk_block_job_bytes": (ctypes.c_size_t, []),
     "sptk_block_perm": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _i64, ctypes.c_int,
                                        _vp, _vp, _vp]),
+    "sptk_interleave_rounds": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _vp, _vp]),
     "sptk_permutation_ws_bytes": (ctypes.c_size_t, [_i64]),
     "sptk_permutation": (ctypes.c_int, [_u64p, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
     "sptk_permute_records": (ctypes.c_int, [_u64p, _i64, _vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
@@ -66,6 +67,12 @@ SIGNATURES = {
     "sptk_factor_pass_f64": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _i64, _vp, _i64p, _vp, _i64p,
                                             _i64p, ctypes.c_int, ctypes.c_int, _f64p, _f64p, ctypes.c_int,
                                             _vp]),
+    "sptk_factor_pass_exact_ws_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int]),
+    "sptk_factor_pass_exact": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _i64, _vp, _i64p, _vp, _i64p, _i64p,
+                                              ctypes.c_int, ctypes.c_int, _f64p, _f64p, _vp, ctypes.c_size_t, _vp]),
+    "sptk_factor_pass_exact_f64": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _i64, _vp, _i64p, _vp, _i64p,
+                                                  _i64p, ctypes.c_int, ctypes.c_int, _f64p, _f64p, _vp,
+                                                  ctypes.c_size_t, _vp]),
     "sptk_core_ws_bytes": (ctypes.c_size_t, [_i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "sptk_core_pass": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _i64, _vp, _i64p, _vp, _i64p, _i64p,
                                       ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_size_t,

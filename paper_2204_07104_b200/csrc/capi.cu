@@ -102,6 +102,11 @@ int sptk_block_perm(const void* d_jobs, const int32_t* d_coords, int n_jobs, int
                     (cudaStream_t)stream);
 }
 
+int sptk_interleave_rounds(const void* d_jobs, int n_jobs, const int32_t* d_perm, long long rel_lo,
+                           int32_t* d_visit, void* stream) {
+  return interleave_rounds(d_jobs, n_jobs, d_perm, rel_lo, d_visit, (cudaStream_t)stream);
+}
+
 size_t sptk_permutation_ws_bytes(long long n) { return perm_ws_bytes(n); }
 
 int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, void* d_ws, size_t ws_bytes,
@@ -194,6 +199,36 @@ int sptk_factor_pass_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, l
   if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
   return factor_pass<double>(d_rec, rw, d_visit, n_visit, base, d_fac, d_cor, md, h_gammas, h_lambdas, mode,
                              (cudaStream_t)stream);
+}
+
+size_t sptk_factor_pass_exact_ws_bytes(long long n_visit, int n_modes) {
+  return factor_dep_ws_bytes(n_visit, n_modes);
+}
+
+int sptk_factor_pass_exact(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, long long base,
+                           float* d_fac, const int64_t* h_foff, const float* d_cor, const int64_t* h_coff,
+                           const int64_t* h_jr, int n_modes, int rcore, const double* h_gammas,
+                           const double* h_lambdas, void* d_ws, size_t ws_bytes, void* stream) {
+  ModelDesc md;
+  if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
+  float g[SPTK_MAX_MODES], l[SPTK_MAX_MODES];
+  for (int n = 0; n < n_modes; ++n) {
+    g[n] = (float)h_gammas[n];
+    l[n] = (float)h_lambdas[n];
+  }
+  return factor_pass_dep<float>(d_rec, rw, d_visit, n_visit, base, d_fac, d_cor, md, g, l, d_ws, ws_bytes,
+                                (cudaStream_t)stream);
+}
+
+int sptk_factor_pass_exact_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit,
+                               long long base, double* d_fac, const int64_t* h_foff, const double* d_cor,
+                               const int64_t* h_coff, const int64_t* h_jr, int n_modes, int rcore,
+                               const double* h_gammas, const double* h_lambdas, void* d_ws, size_t ws_bytes,
+                               void* stream) {
+  ModelDesc md;
+  if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
+  return factor_pass_dep<double>(d_rec, rw, d_visit, n_visit, base, d_fac, d_cor, md, h_gammas, h_lambdas, d_ws,
+                                 ws_bytes, (cudaStream_t)stream);
 }
 
 size_t sptk_core_ws_bytes(const int64_t* h_jr, int n_modes, int rcore, int exact_chunks) {

@@ -511,6 +511,7 @@ static int launch_tps(const int* rec, int rw, const int* visit, long long n_visi
   long long blocks = (n_visit + threads - 1) / threads;
   const long long cap = 148LL * 3 * 8;
   if (blocks > cap) blocks = cap;
+  if (blocks > hogwild_cta_cap(n_visit, threads)) blocks = hogwild_cta_cap(n_visit, threads);
   if (blocks < 1) blocks = 1;
   if (rw == 4)
     factor_tps_kernel<N, J, R, 4><<<(unsigned)blocks, threads, 0, s>>>(rec, visit, n_visit, base, fac, p);
@@ -542,6 +543,7 @@ static int launch_fma(const int* rec, const int* visit, long long n_visit, long 
   long long blocks = 148LL * per_sm;
   const long long need = (n_visit + 127) / 128;
   if (blocks > need) blocks = need;
+  if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
   if (blocks < 1) blocks = 1;
   if (visit)
     factor_fma_kernel<N, J, true><<<(unsigned)blocks, 128, 0, s>>>(rec, visit, n_visit, base, fac, cor, p, hot);
@@ -653,6 +655,7 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
       SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   long long blocks = (n_visit + warps - 1) / warps;
   if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > hogwild_cta_cap(n_visit, warps)) blocks = hogwild_cta_cap(n_visit, warps);
   kfn<<<(unsigned)blocks, 32 * warps, smem, s>>>(rec, rw, vo, visit, n_visit, base, fac, cor, md, gl, per_warp);
   note_factor_kernel("factor_wps_kernel");
   SPTK_CHECK_LAUNCH();

@@ -950,6 +950,7 @@ static int launch_tc3(const int* rec, int rw, const int* visit, long long n_visi
   // CTA slots left to the side-stream samplers (see launch_tc2); default none
   if (const char* e = getenv("SPTK_SAMPLER_SLOTS3")) blocks -= atoi(e);
   if (blocks < 1) blocks = 1;
+  if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
   if (blocks > tiles) blocks = tiles;
   static unsigned slot = 0;
   unsigned* ctr = nullptr;
@@ -1014,6 +1015,7 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   // experiment hook: SPTK_TC_GRID = explicit persistent grid size
   if (const char* e = getenv("SPTK_TC_GRID")) blocks = atoll(e);
   if (blocks < 1) blocks = 1;
+  if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
   if (blocks > tiles) blocks = tiles;
   // per-launch tile counter from a small rotating pool (launches on one stream
   // are ordered; the pool only guards against back-to-back reuse)
@@ -1308,6 +1310,7 @@ static int launch_tc4(const int* rec, int rw, const int* visit, long long n_visi
   }
   long long tiles = (n_visit + 127) / 128;
   long long blocks = 148;
+  if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
   if (blocks > tiles) blocks = tiles;
   static unsigned slot = 0;
   unsigned* ctr = nullptr;
@@ -1372,6 +1375,7 @@ static int launch_tc(const int* rec, int rw, const int* visit, long long n_visit
   }
   long long tiles = (n_visit + 127) / 128;
   long long blocks = 148LL * per_sm;
+  if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
   if (blocks > tiles) blocks = tiles;
   kfn<<<(unsigned)blocks, 128, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p);
   note_factor_kernel("factor_tc_kernel");

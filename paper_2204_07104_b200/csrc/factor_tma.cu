@@ -516,6 +516,7 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
   if (const char* e = getenv("SPTK_SAMPLER_SLOTS")) slots = atoi(e);
   long long blocks = 148LL * per_sm - (per_sm >= 2 ? slots : 0);
   if (const char* e = getenv("SPTK_TC_GRID")) blocks = atoll(e);
+  if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
   if (blocks < 1) blocks = 1;
   if (blocks > tiles) blocks = tiles;
   unsigned* ctr = nullptr;

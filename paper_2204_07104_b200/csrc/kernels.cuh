@@ -27,6 +27,8 @@ int choice(const uint64_t st[4], long long pop, long long k, int shuffle, int* o
 int block_perm(const void* d_jobs, const int* d_coords, int n_jobs, int order, unsigned long long seed,
                long long t, int cap, uint16_t* d_js, int* d_visit, cudaStream_t s);
 size_t block_job_bytes();
+int interleave_rounds(const void* d_jobs, int n_jobs, const int* d_perm, long long rel_lo, int* d_visit,
+                      cudaStream_t s);
 int u32_stream(const uint64_t st[4], unsigned long long q0, long long n, uint32_t* out, cudaStream_t s);
 int iota(int* out, long long n, int offset, cudaStream_t s);
 size_t scan_ws_bytes(long long n);
@@ -49,6 +51,13 @@ template <typename T>
 int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, long long base, T* fac,
                 const T* cor, const ModelDesc& md, const T* h_gammas, const T* h_lambdas, int mode,
                 cudaStream_t s);
+
+// factor_dep.cu (exact mode across the GPU: predecessor-driven schedule)
+size_t factor_dep_ws_bytes(long long nv, int n_modes);
+template <typename T>
+int factor_pass_dep(const int* rec, int rw, const int* visit, long long nv, long long base, T* fac, const T* cor,
+                    const ModelDesc& md, const T* h_gammas, const T* h_lambdas, void* ws, size_t ws_bytes,
+                    cudaStream_t s);
 
 // factor_tc.cu (tcgen05 path; returns 1 if it handled the launch)
 int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,

@@ -2115,5 +2115,42 @@ int block_perm(const void* d_jobs, const int* d_coords, int n_jobs, int order, u
   return 0;
 }
 size_t block_job_bytes() { return sizeof(BlockJob); }
+// Round-interleaved visit list from per-block visit orders that lie in the
+// partitioned layout (perm[off_b + p], relative to off_b when rel_lo < 0,
+// else to rel_lo): the layout block_fy_kernel writes, for blocks too large for
+// one CTA's shared memory (their orders come from the batched j-sequence +
+// Fisher-Yates apply).  One CTA per block.
+__global__ void __launch_bounds__(256) interleave_kernel(const BlockJob* __restrict__ jobs,
+                                                         const int* __restrict__ perm, long long rel_lo,
+                                                         int* __restrict__ visit) {
+  __shared__ int sizes[64];
+  const BlockJob jb = jobs[blockIdx.x];
+  const int m = min(jb.m, 64);
+  if (threadIdx.x < m) sizes[threadIdx.x] = jobs[jb.first + threadIdx.x].n;
+  __syncthreads();
+  const long long add = rel_lo < 0 ? jb.off : rel_lo;
+  for (int p = threadIdx.x; p < jb.n; p += blockDim.x) {
+    long long pos = jb.out_base;
+    if (p < jb.nmin) {
+      pos += (long long)p * m + jb.slot;
+    } else {
+      for (int s2 = 0; s2 < m; ++s2) {
+        const int ns = sizes[s2];
+        pos += ns < p ? ns : p;
+        if (s2 < jb.slot && ns > p) ++pos;
+      }
+    }
+    visit[pos] = (int)(add + __ldg(perm + jb.off + p));
+  }
+}
+
+int interleave_rounds(const void* d_jobs, int n_jobs, const int* d_perm, long long rel_lo, int* d_visit,
+                      cudaStream_t s) {
+  if (n_jobs <= 0) return 0;
+  interleave_kernel<<<n_jobs, 256, 0, s>>>((const BlockJob*)d_jobs, d_perm, rel_lo, d_visit);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
+
 
 }  // namespace sptk

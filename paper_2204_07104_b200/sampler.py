@@ -160,9 +160,12 @@ class BlockOrders:
 
     rounds: list of rounds, each a list of (block tuple, off, n)."""
 
-    def __init__(self, rounds, order: int, device):
+    def __init__(self, rounds, order: int, device, big: bool = False):
         import torch
 
+        # big=True: blocks above BLOCK_PERM_MAX; only the job table is built
+        # and interleave() lays out visit orders drawn elsewhere
+        self.big = big
         jobs, coords, base = [], [], 0
         for rnd in rounds:
             first, m = len(jobs), len(rnd)
@@ -170,7 +173,7 @@ class BlockOrders:
                 raise ValueError("at most 64 blocks per round")
             nmin = min((n for _, _, n in rnd), default=0)
             for slot, (block, off, n) in enumerate(rnd):
-                if n > BLOCK_PERM_MAX:
+                if n > BLOCK_PERM_MAX and not big:
                     raise ValueError(f"block of {n} nonzeros exceeds {BLOCK_PERM_MAX}")
                 jobs.append((off, base, n, first, m, slot, nmin, 0))
                 coords.append(tuple(int(c) for c in block))
@@ -186,10 +189,16 @@ class BlockOrders:
         self.coords = torch.from_numpy(np.asarray(coords, dtype=np.int32).reshape(-1, order)).to(device)
         # j-sequence scratch (uint16, indexed like the records)
         span = max([j[0] + j[2] for j in jobs], default=1)
-        self.js = torch.empty(max(span, 1), dtype=torch.int16, device=device)
+        self.js = None if big else torch.empty(max(span, 1), dtype=torch.int16, device=device)
 
     def draw(self, seed: int, t: int, out, stream=None) -> None:
         """visit orders of epoch t into out[0:total] (int32, device)."""
         check(_lib.load().sptk_block_perm(ptr(self.jobs), ptr(self.coords), self.n_jobs, self.order, int(seed),
                                           int(t), max(self.cap, 1), ptr(self.js), ptr(out), stream_ptr(stream)),
               "sptk_block_perm")
+
+    def interleave(self, perm, rel_lo: int, out, stream=None) -> None:
+        """out[0:total] = the round-interleaved visit list of per-block orders
+        perm[off_b + p] (entries relative to off_b, or to rel_lo >= 0)."""
+        check(_lib.load().sptk_interleave_rounds(ptr(self.jobs), self.n_jobs, ptr(perm), int(rel_lo), ptr(out),
+                                                 stream_ptr(stream)), "sptk_interleave_rounds")

@@ -249,7 +249,17 @@ class EpochRunner:
                      and _env_int("SPTK_FLAT", 1) == 1
                      and all(len(items) <= 64 for items in self.rounds)
                      and max((c for items in self.rounds for (_, _, c) in items), default=0) <= BLOCK_PERM_MAX)
-        self.block_orders = BlockOrders(self.rounds, self.order, dev) if self.flat else None
+        # Blocks too large for one CTA (NF at W = 16: ~24K nonzeros): their
+        # orders come from the batched sampler below and are then interleaved
+        # the same way (sptk_interleave_rounds), so the factor phase is still
+        # one pass -- per-block launches would put a whole block's samples in
+        # flight over its 1/W of the rows (Hogwild contention, divergence).
+        self.flat_big = (not self.flat and self.m > 1 and self.mode == 0 and not self.f64 and owner_rank is None
+                         and _env_int("SPTK_FLAT", 1) == 1 and all(len(items) <= 64 for items in self.rounds))
+        self.block_orders = (BlockOrders(self.rounds, self.order, dev) if self.flat else
+                             BlockOrders(self.rounds, self.order, dev, big=True) if self.flat_big else None)
+        self.fvis = ([torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
+                     if self.flat_big else None)
         # Sampler state (K2), double-buffered by epoch parity: Fisher-Yates
         # j-sequences (jbuf), visit orders (perm, laid out like the
         # partitioned records; flat: the epoch's visit list) and core batches (psi).
@@ -290,6 +300,14 @@ class EpochRunner:
             self.ws_fy.get(int(Lb.sptk_fy_apply_ws_bytes(self.hi - self.lo if self.batched_fy else max_block)))
         if config.update_core and self.k < self.nnz:
             self.ws_psi.get(int(Lb.sptk_choice_ws_bytes(self.nnz, self.k)))
+        # exact mode: blocks of at least SPTK_EXACT_DEP_MIN samples (default
+        # 2048) run the predecessor-driven kernel (sptk_factor_pass_exact);
+        # smaller ones the one-warp conflict-free-prefix walker
+        self.dep_min = _env_int("SPTK_EXACT_DEP_MIN", 2048)
+        self.ws_dep = None
+        if self.mode == 1 and max_block >= self.dep_min:
+            self.ws_dep = torch.empty(int(Lb.sptk_factor_pass_exact_ws_bytes(max_block, self.order)),
+                                      dtype=torch.uint8, device=dev)
         self.acc = torch.zeros(max(self.dm.cor_size, 1), dtype=torch.float64, device=dev)
         L = _lib.load()
         chunks = self.m if self.mode == 1 else 0
@@ -379,11 +397,15 @@ class EpochRunner:
             check(self.L.sptk_fy_globalize(ptr(j), ptr(self.fy_off), self.fy_off.numel() - 1, stream_ptr(stream)),
                   "sptk_fy_globalize")
             fy_apply(j, hi - lo, out=self.perm[slot][lo:hi], ws=self.ws_fy, stream=stream)
+            if self.flat_big:
+                self.block_orders.interleave(self.perm[slot], lo, self.fvis[slot], stream=stream)
         else:
             for items in self.rounds:
                 for block, off, cnt in items:
                     fy_apply(self.jbuf[slot][off:off + cnt], cnt, out=self.perm[slot][off:off + cnt], ws=self.ws_fy,
                              stream=stream)
+            if self.flat_big:
+                self.block_orders.interleave(self.perm[slot], -1, self.fvis[slot], stream=stream)
         self.sampled_epoch[slot] = t
 
     def draw_samples(self, t: int, slot: int, stream) -> None:
@@ -486,11 +508,12 @@ class EpochRunner:
         fn = L.sptk_factor_pass_f64 if self.f64 else L.sptk_factor_pass
         s = stream_ptr()
         processed = 0
-        if self.flat:
+        if self.flat or self.flat_big:
             if self.factor_events is not None:
                 e0 = self.torch.cuda.Event(enable_timing=True)
                 e0.record()
-            check(fn(ptr(self.part.rec), self.part.rw, ptr(self.perm[slot]), self.nnz, 0, ptr(dm.fac), dm.p_foff,
+            vis = self.fvis[slot] if self.flat_big else self.perm[slot]
+            check(fn(ptr(self.part.rec), self.part.rw, ptr(vis), self.nnz, 0, ptr(dm.fac), dm.p_foff,
                      ptr(dm.cor), dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam, self.mode, s),
                   "sptk_factor_pass")
             if self.factor_events is not None:
@@ -506,9 +529,16 @@ class EpochRunner:
                     e0.record()
                 rec, visit = self.part.rec, self.perm[slot][off:off + cnt]
                 vbase = self.lo if self.batched_fy else off  # visit entries are relative to vbase
-                check(fn(ptr(rec), self.part.rw, ptr(visit), cnt, vbase, ptr(dm.fac), dm.p_foff, ptr(dm.cor),
-                         dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam, self.mode, s),
-                      "sptk_factor_pass")
+                if self.ws_dep is not None and cnt >= self.dep_min:
+                    # exact mode across the GPU (predecessor-driven schedule)
+                    fx = L.sptk_factor_pass_exact_f64 if self.f64 else L.sptk_factor_pass_exact
+                    check(fx(ptr(rec), self.part.rw, ptr(visit), cnt, vbase, ptr(dm.fac), dm.p_foff, ptr(dm.cor),
+                             dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam, ptr(self.ws_dep),
+                             self.ws_dep.numel(), s), "sptk_factor_pass_exact")
+                else:
+                    check(fn(ptr(rec), self.part.rw, ptr(visit), cnt, vbase, ptr(dm.fac), dm.p_foff, ptr(dm.cor),
+                             dm.p_coff, dm.p_jr, self.order, dm.rcore, self.p_gam, self.p_lam, self.mode, s),
+                          "sptk_factor_pass")
                 if self.factor_events is not None:
                     e1 = self.torch.cuda.Event(enable_timing=True)
                     e1.record()
