@@ -248,11 +248,21 @@ def bench_ours(args, cfg):
         runner = dist.DistRunner(model, tr, tcfg)
     elif sim > 1:
         # one rank's share of an M-GPU DSGD epoch (its blocks, their samplers,
-        # the core phase) without the exchanges: a per-rank compute estimate
+        # the core phase): the fused per-rank launch with its pushes aimed at
+        # its own replica and its ready flag raised in advance (no peer to
+        # wait for) -- a per-rank compute estimate without NVLink transfers
         from dataclasses import replace
 
+        from paper_2204_07104_b200.dsgd_fused import FusedRankRunner, fused_supported
+
         tcfg = replace(tcfg, workers=sim)
-        runner = EpochRunner(model, tr, tcfg, owner_rank=0)
+        if fused_supported(model, replace(tcfg, update_mode="hogwild")) and os.environ.get("BENCH_SIM_FUSED", "1") == "1":
+            runner = FusedRankRunner(model, tr, replace(tcfg, update_mode="hogwild"), 0, sim)
+            fa, ra = runner.fused.peer_addresses()
+            runner.set_peers([fa] * sim, [ra] * sim)
+            runner.fused.ready.fill_(1 << 30)
+        else:
+            runner = EpochRunner(model, tr, tcfg, owner_rank=0)
     else:
         runner = EpochRunner(model, tr, tcfg)
     # warm-up epochs (not timed)

@@ -212,6 +212,36 @@ int sptk_factor_pass_exact_f64(const int32_t* d_rec, int rw, const int32_t* d_vi
                                const double* h_gammas, const double* h_lambdas, void* d_ws, size_t ws_bytes,
                                void* stream);
 
+/* ---- multi-GPU DSGD, fused (one launch per rank per epoch) ------------- */
+/* One rank's factor phase of a whole DSGD epoch (trainer.py:189-208 with the
+ * rounds of partition.py:100-117 spread over processes/GPUs): d_visit holds
+ * the rank's block of each round, round after round, each round padded with
+ * -1 entries to whole 128-sample tiles; round r occupies
+ * [d_rstart[r], d_rstart[r+1]) with valid samples below d_rend[r].  Tiles of
+ * round r >= 1 start once *d_ready >= gen0 + r (the block rotated in for
+ * round r has landed); after its last tile of round r the rank copies the
+ * block described by d_push[r] (sptk_dsgd_push_bytes() bytes each: {int64
+ * row_lo, int64 nrows, int64 mode, float* dst, int32* dst_ready}; nrows = 0:
+ * none) to its next owner's model (peer pointer: NVLink stores) and raises
+ * that rank's flag to gen0 + r + 1 (release, system scope).  d_done:
+ * n_rounds ints of scratch.  grid > 0 caps the persistent grid (all CTAs of
+ * every rank sharing a GPU must be resident).  Uniform J = R, TMA kernel
+ * shapes (order 3/4 at J = 16, 3/6 at J = 8). */
+int sptk_factor_pass_dsgd(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, float* d_fac,
+                          const int64_t* h_foff, const float* d_cor, const int64_t* h_coff, const int64_t* h_jr,
+                          int n_modes, int rcore, const double* h_gammas, const double* h_lambdas,
+                          const long long* d_rstart, const long long* d_rend, const void* d_push, int32_t* d_done,
+                          int32_t* d_ready, int n_rounds, int gen0, int grid, void* stream);
+size_t sptk_dsgd_push_bytes(void);
+/* Device memory other processes can map (cudaMalloc'd, zeroed) and its CUDA
+ * IPC handle (64 bytes); sptk_ipc_open maps a peer's allocation (peer access
+ * enabled lazily: NVLink loads/stores on NVSwitch systems). */
+int sptk_shared_alloc(size_t bytes, void** d_ptr);
+int sptk_shared_free(void* d_ptr);
+int sptk_ipc_get(void* d_ptr, unsigned char* h_handle);
+int sptk_ipc_open(const unsigned char* h_handle, void** d_ptr);
+int sptk_ipc_close(void* d_ptr);
+
 /* ---- K4/K5: core gradient + apply ------------------------------------- */
 size_t sptk_core_ws_bytes(const int64_t* h_jr, int n_modes, int rcore, int exact_chunks);
 /* d_acc (fp64, layout coff) += sum over visited samples.  sample id of the

@@ -231,11 +231,68 @@ int sptk_factor_pass_exact_f64(const int32_t* d_rec, int rw, const int32_t* d_vi
                                  ws_bytes, (cudaStream_t)stream);
 }
 
+int sptk_factor_pass_dsgd(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, float* d_fac,
+                          const int64_t* h_foff, const float* d_cor, const int64_t* h_coff, const int64_t* h_jr,
+                          int n_modes, int rcore, const double* h_gammas, const double* h_lambdas,
+                          const long long* d_rstart, const long long* d_rend, const void* d_push, int32_t* d_done,
+                          int32_t* d_ready, int n_rounds, int gen0, int grid, void* stream) {
+  ModelDesc md;
+  if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
+  float g[SPTK_MAX_MODES], l[SPTK_MAX_MODES];
+  for (int n = 0; n < n_modes; ++n) {
+    g[n] = (float)h_gammas[n];
+    l[n] = (float)h_lambdas[n];
+  }
+  return factor_pass_dsgd(d_rec, rw, d_visit, n_visit, d_fac, d_cor, md, g, l, d_rstart, d_rend, d_push, d_done,
+                          d_ready, n_rounds, gen0, grid, (cudaStream_t)stream);
+}
+
+size_t sptk_dsgd_push_bytes(void) { return dsgd_push_bytes(); }
+
+int sptk_shared_alloc(size_t bytes, void** d_ptr) {
+  *d_ptr = nullptr;
+  SPTK_CUDA_TRY(cudaMalloc(d_ptr, bytes));
+  SPTK_CUDA_TRY(cudaMemset(*d_ptr, 0, bytes));
+  return 0;
+}
+
+int sptk_shared_free(void* d_ptr) {
+  SPTK_CUDA_TRY(cudaFree(d_ptr));
+  return 0;
+}
+
+int sptk_ipc_get(void* d_ptr, unsigned char* h_handle) {
+  cudaIpcMemHandle_t h;
+  SPTK_CUDA_TRY(cudaIpcGetMemHandle(&h, d_ptr));
+  memcpy(h_handle, &h, sizeof(h));
+  return 0;
+}
+
+int sptk_ipc_open(const unsigned char* h_handle, void** d_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h_handle, sizeof(h));
+  *d_ptr = nullptr;
+  SPTK_CUDA_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int sptk_ipc_close(void* d_ptr) {
+  SPTK_CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
+  return 0;
+}
+
 size_t sptk_core_ws_bytes(const int64_t* h_jr, int n_modes, int rcore, int exact_chunks) {
   size_t cs = 0;
   for (int n = 0; n < n_modes; ++n) cs += (size_t)h_jr[n] * rcore;
   size_t blocks = exact_chunks > 0 ? (size_t)exact_chunks : (size_t)148 * 4;
-  return blocks * cs * sizeof(double) + sizeof(long long) * (blocks + 2) + 1024;
+  size_t b = blocks * cs * sizeof(double) + sizeof(long long) * (blocks + 2) + 1024;
+  if (exact_chunks > 0) {
+    // segment scratch of the whole-GPU exact pass (core.cu: EXACT_SEG samples)
+    size_t tot = 0;
+    for (int n = 0; n < n_modes; ++n) tot += (size_t)h_jr[n];
+    b += (size_t)32768 * (2 * (size_t)n_modes * rcore + tot) * sizeof(double) + 1024;
+  }
+  return b;
 }
 
 int sptk_core_pass(const int32_t* d_rec, int rw, const int32_t* d_visit, const int32_t* d_map, long long n_visit,

@@ -629,7 +629,126 @@ int core_pass(const int* rec, int rw, const int* visit, const int* map, long lon
   return 0;
 }
 
-// Verification mode: chunk boundaries follow np.array_split(psi, n_chunks).
+// Verification mode: chunk boundaries follow np.array_split(psi, n_chunks),
+// each chunk's accumulator is the sample-ordered sum of _loops.py:92-103 and
+// the chunks are merged in chunk order (trainer.py:238-240).  The per-sample
+// terms are independent, only the sums are ordered, so the pass runs in
+// segments of EXACT_SEG samples: phase 1 (every SM, one thread per sample)
+// writes each sample's coefficient row v = resid * prod_{n0 != n} c[n0] and
+// its factor rows a to a scratch table, phase 2 (one thread per (chunk,
+// output)) extends that output's running sum over the segment's samples in
+// order.  Bitwise equal to the one-CTA sequential walk it replaces.
+#define EXACT_SEG 32768
+
+template <typename T>
+__global__ void __launch_bounds__(128) core_exact_terms_kernel(const int* __restrict__ rec, int rw, int vo,
+                                                               const int* __restrict__ visit,
+                                                               const int* __restrict__ map, long long k0, int cnt,
+                                                               const T* __restrict__ fac, const T* __restrict__ cor,
+                                                               ModelDesc md, T* __restrict__ tv, T* __restrict__ ta,
+                                                               T* __restrict__ tc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  const int N = md.n_modes, R = md.rcore, NR = N * R;
+  int aoff[SPTK_MAX_MODES];
+  int tot = 0;
+  for (int n = 0; n < N; ++n) {
+    aoff[n] = tot;
+    tot += md.jr[n];
+  }
+  T* my_a = ta + (size_t)i * tot;
+  T* my_v = tv + (size_t)i * NR;
+  T* my_c = tc + (size_t)i * NR;
+  const long long k = k0 + i;
+  const long long sid = visit ? (long long)__ldg(visit + k) : k;
+  const long long ri = map ? (long long)__ldg(map + sid) : sid;
+  const int* rp = rec + ri * rw;
+  const T x = load_val<T>(rp, vo);
+  for (int n = 0; n < N; ++n) {
+    const int J = md.jr[n];
+    const T* row = fac + md.foff[n] + (long long)__ldg(rp + n) * J;
+    for (int j = 0; j < J; ++j) my_a[aoff[n] + j] = row[j];
+  }
+  for (int n0 = 0; n0 < N; ++n0) {
+    const int J = md.jr[n0];
+    for (int r = 0; r < R; ++r) {
+      T dot = 0;
+      for (int j = 0; j < J; ++j) dot = cadd(dot, cmul(my_a[aoff[n0] + j], __ldg(cor + md.coff[n0] + j * R + r)));
+      my_c[n0 * R + r] = dot;
+    }
+  }
+  T xhat = 0;
+  for (int r = 0; r < R; ++r) {
+    T pr = 1;
+    for (int n0 = 0; n0 < N; ++n0) pr = cmul(pr, my_c[n0 * R + r]);
+    xhat = cadd(xhat, pr);
+  }
+  const T resid = cadd(xhat, -x);
+  for (int n = 0; n < N; ++n)
+    for (int r = 0; r < R; ++r) {
+      T w = 1;
+      for (int n0 = 0; n0 < N; ++n0)
+        if (n0 != n) w = cmul(w, my_c[n0 * R + r]);
+      my_v[n * R + r] = cmul(resid, w);
+    }
+}
+
+// CTA (128 outputs of chunk blockIdx.y): partial[c][o] += the segment's
+// terms of chunk c in sample order.  The term rows are staged through shared
+// memory KT samples at a time (coalesced), so the per-output sums run at
+// shared-memory latency instead of one dependent L2 round trip per term.
+template <typename T>
+__global__ void __launch_bounds__(128) core_exact_sum_kernel(const T* __restrict__ tv, const T* __restrict__ ta,
+                                                             long long k0, int cnt, const long long* __restrict__ lo,
+                                                             int KT, ModelDesc md, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char ex_sm[];
+  const int CS = md.cor_size, c = blockIdx.y;
+  long long a = lo[c], z = lo[c + 1];
+  a = a > k0 ? a : k0;
+  z = z < k0 + cnt ? z : k0 + cnt;
+  if (a >= z) return;
+  const int N = md.n_modes, R = md.rcore, NR = N * R;
+  int tot = 0;
+  for (int q = 0; q < N; ++q) tot += md.jr[q];
+  T* sv = reinterpret_cast<T*>(ex_sm);
+  T* sa = sv + (size_t)KT * NR;
+  const int o = blockIdx.x * 128 + threadIdx.x;
+  const bool mine = o < CS;
+  int n = 0, aoffn = 0;
+  if (mine) {
+    while (n + 1 < N && o >= md.coff[n + 1]) ++n;
+    for (int q = 0; q < n; ++q) aoffn += md.jr[q];
+  }
+  const int rel = mine ? o - md.coff[n] : 0, j = rel / R, r = rel - (rel / R) * R;
+  double acc = mine ? partial[(size_t)c * CS + o] : 0.0;
+  for (long long kb = a; kb < z; kb += KT) {
+    const int nk = (int)(z - kb < KT ? z - kb : KT);
+    const T* gv = tv + (size_t)(kb - k0) * NR;
+    const T* ga = ta + (size_t)(kb - k0) * tot;
+    for (int i = threadIdx.x; i < nk * NR; i += 128) sv[i] = gv[i];
+    for (int i = threadIdx.x; i < nk * tot; i += 128) sa[i] = ga[i];
+    __syncthreads();
+    if (mine) {
+      const T* pv = sv + n * R + r;
+      const T* pa = sa + aoffn + j;
+      // the products do not depend on acc: unrolled, their loads and
+      // multiplies run ahead of the ordered additions
+#pragma unroll 16
+      for (int s2 = 0; s2 < nk; ++s2) acc = cadd<double>(acc, cmul<double>((double)pv[s2 * NR], (double)pa[s2 * tot]));
+    }
+    __syncthreads();
+  }
+  if (mine) partial[(size_t)c * CS + o] = acc;
+}
+
+size_t core_exact_ws_bytes(const ModelDesc& md, int n_chunks) {
+  int tot = 0;
+  for (int n = 0; n < md.n_modes; ++n) tot += md.jr[n];
+  const size_t NR = (size_t)md.n_modes * md.rcore;
+  return (size_t)n_chunks * md.cor_size * sizeof(double) + sizeof(long long) * (n_chunks + 2) + 512 +
+         (size_t)EXACT_SEG * (2 * NR + tot) * sizeof(double) + 768;
+}
+
 template <typename T>
 int core_pass_exact(const int* rec, int rw, const int* visit, const int* map, long long n_visit, int n_chunks,
                     const T* fac, const T* cor, const ModelDesc& md, double* acc, void* ws, size_t ws_bytes,
@@ -638,9 +757,6 @@ int core_pass_exact(const int* rec, int rw, const int* visit, const int* map, lo
   SPTK_REQUIRE(n_chunks >= 1 && n_chunks <= 1024, "core_pass_exact: bad chunk count");
   const bool f64 = sizeof(T) == 8;
   SPTK_REQUIRE(rw == rec_words_t(md.n_modes, f64), "core_pass_exact: record width mismatch");
-  int S;
-  size_t smem;
-  SPTK_REQUIRE(pick_S(md, sizeof(T), &S, &smem), "core_pass_exact: model ranks too large");
   // np.array_split: first (n % k) chunks get one extra element; empty chunks dropped
   long long h_lo[1025];
   long long q = n_visit / n_chunks, rmd = n_visit % n_chunks, pos = 0;
@@ -652,20 +768,42 @@ int core_pass_exact(const int* rec, int rw, const int* visit, const int* map, lo
     pos += len;
   }
   h_lo[nb] = pos;
-  size_t need = (size_t)nb * md.cor_size * sizeof(double) + sizeof(long long) * (nb + 1) + 256;
-  SPTK_REQUIRE(ws_bytes >= need, "core_pass_exact: workspace too small");
-  double* partial = (double*)ws;
-  long long* d_lo = (long long*)((char*)ws + (((size_t)nb * md.cor_size * sizeof(double) + 255) & ~(size_t)255));
+  SPTK_REQUIRE(ws_bytes >= core_exact_ws_bytes(md, nb), "core_pass_exact: workspace too small");
+  int tot = 0;
+  for (int n = 0; n < md.n_modes; ++n) tot += md.jr[n];
+  const size_t NR = (size_t)md.n_modes * md.rcore;
+  char* w = (char*)ws;
+  double* partial = (double*)w;
+  w += ((size_t)nb * md.cor_size * sizeof(double) + 255) & ~(size_t)255;
+  long long* d_lo = (long long*)w;
+  w += (sizeof(long long) * (nb + 2) + 255) & ~(size_t)255;
+  T* tv = (T*)w;
+  w += ((size_t)EXACT_SEG * NR * sizeof(T) + 255) & ~(size_t)255;
+  T* tc = (T*)w;
+  w += ((size_t)EXACT_SEG * NR * sizeof(T) + 255) & ~(size_t)255;
+  T* ta = (T*)w;
   SPTK_CUDA_TRY(cudaMemcpyAsync(d_lo, h_lo, sizeof(long long) * (nb + 1), cudaMemcpyHostToDevice, s));
-  auto kfn = core_pass_kernel<T, true>;
-  SPTK_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kfn<<<(unsigned)nb, 256, smem, s>>>(rec, rw, rec_val_off(md.n_modes, f64), visit, map, n_visit, fac, cor, md, S,
-                                       partial, d_lo);
-  SPTK_CHECK_LAUNCH();
+  SPTK_CUDA_TRY(cudaMemsetAsync(partial, 0, (size_t)nb * md.cor_size * sizeof(double), s));
+  const int vo = rec_val_off(md.n_modes, f64);
+  // staged samples per step of the ordered sums: <= 64, <= 96 KB of terms
+  int KT = (int)((96 * 1024) / ((NR + tot) * sizeof(T)));
+  KT = KT > 1024 ? 1024 : (KT < 1 ? 1 : KT);
+  const size_t ex_smem = (size_t)KT * (NR + tot) * sizeof(T);
+  SPTK_CUDA_TRY(cudaFuncSetAttribute(core_exact_sum_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ex_smem));
+  for (long long k0 = 0; k0 < n_visit; k0 += EXACT_SEG) {
+    const int cnt = (int)(n_visit - k0 < EXACT_SEG ? n_visit - k0 : EXACT_SEG);
+    core_exact_terms_kernel<T><<<(cnt + 127) / 128, 128, 0, s>>>(rec, rw, vo, visit, map, k0, cnt, fac, cor, md, tv,
+                                                                  ta, tc);
+    SPTK_CHECK_LAUNCH();
+    core_exact_sum_kernel<T><<<dim3((unsigned)((md.cor_size + 127) / 128), (unsigned)nb), 128, ex_smem, s>>>(
+        tv, ta, k0, cnt, d_lo, KT, md, partial);
+    SPTK_CHECK_LAUNCH();
+  }
   core_reduce_ordered_kernel<<<(md.cor_size + 255) / 256, 256, 0, s>>>(partial, nb, md.cor_size, acc);
   SPTK_CHECK_LAUNCH();
-  // the host copy of h_lo must outlive the async copy
-  SPTK_CUDA_TRY(cudaStreamSynchronize(s));
+  // (h_lo: a pageable host-to-device cudaMemcpyAsync returns once the source
+  // has been staged, so the next call may overwrite it)
   return 0;
 }
 

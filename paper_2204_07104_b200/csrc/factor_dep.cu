@@ -19,10 +19,10 @@
 //      flags (ld.acquire), updates the sample with the reference's operation
 //      order (lanes over r / j, sums in the reference's index order, no FMA
 //      contraction), writes the rows and publishes its flag (st.release).
-// The critical path is the longest predecessor chain (~ the largest row
-// multiplicity), not the visit length: cfg1's 90K samples form chains of
-// ~130, against the ~2,800 conflict-free prefixes of the one-warp walker
-// (factor_seq_kernel, kept for tiny visit lists).
+// The critical path is the longest predecessor chain, not the visit length:
+// cfg1's 90K samples have a longest chain of 563 (computed on the host for
+// one visit order), against the ~2,800 conflict-free prefixes of the
+// one-warp walker (factor_seq_kernel, kept for tiny visit lists).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -103,16 +103,18 @@ __global__ void __launch_bounds__(128) factor_dep_kernel(const int* __restrict__
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= nv) break;
     const int* rp = rec + (base + (visit ? (long long)__ldg(visit + k) : k)) * rw;
+    // the record is read-only: fetched before the wait
+    const T x = load_val<T>(rp, vo);
+    int rows[SPTK_MAX_MODES];
+    for (int n = 0; n < N; ++n) rows[n] = __ldg(rp + n);
     // wait for the predecessors (all lanes poll the same words)
     for (int n = 0; n < N; ++n) {
       const int p = __ldg(pred + (long long)n * nv + k);
       if (p >= 0)
-        while (ld_acquire(flags + p) == 0) __nanosleep(20);
+        while (ld_acquire(flags + p) == 0) {
+        }
     }
-    const T x = load_val<T>(rp, vo);
-    int rows[SPTK_MAX_MODES];
     for (int n = 0; n < N; ++n) {
-      rows[n] = __ldg(rp + n);
       const int J = md.jr[n];
       const T* row = fac + md.foff[n] + (long long)rows[n] * J;
       for (int j = lane; j < J; j += 32) a_s[aoff[n] + j] = __ldcg(row + j);
@@ -164,10 +166,13 @@ __global__ void __launch_bounds__(128) factor_dep_kernel(const int* __restrict__
       }
       __syncwarp();
     }
-    // publish: every lane's row stores before the flag
-    __threadfence();
+    // publish: the warp's row stores (ordered before lane 0 by the warp
+    // barrier), one gpu-scope fence (cumulative), then the flag
     __syncwarp();
-    if (lane == 0) st_release(flags + k, 1);
+    if (lane == 0) {
+      __threadfence();
+      st_release(flags + k, 1);
+    }
   }
 }
 

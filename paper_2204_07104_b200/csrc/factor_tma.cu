@@ -51,6 +51,41 @@ struct TmaParams {
   int bulk_red;           // hot deltas as one bulk add-reduction per sample (TMA unit) instead of red.add.v4
 };
 
+// DSGD across GPUs, fused into the factor kernel (sptk_factor_pass_dsgd):
+// the rank's visit list holds its blocks round after round, each round padded
+// to whole 128-sample tiles (padding entries -1).  A tile of round r >= 1
+// starts only once the rotated block of round r has landed (*ready >= gen0 +
+// r, written by the sending rank over NVLink); the CTA that finishes the last
+// tile of round r copies the block this rank hands on to its next owner
+// (peer stores) and raises that rank's ready flag (release at system scope).
+// (partition.py:100-117: consecutive rounds move one mode's blocks one rank
+// along the ring.)
+struct DsgdPush {
+  long long row_lo;  // first row of the block
+  long long nrows;   // 0: nothing to send after this round
+  long long mode;
+  float* dst;        // the receiving rank's copy of row row_lo (peer pointer)
+  int* dst_ready;    // the receiving rank's ready flag (peer pointer)
+};
+struct DsgdParams {
+  const long long* rstart;  // [n_rounds + 1] first visit slot of each round (multiples of 128)
+  const long long* rend;    // [n_rounds] end of each round's valid samples
+  const DsgdPush* push;     // [n_rounds]
+  int* done;                // [n_rounds] finished tiles (zeroed by the launcher)
+  int* ready;               // this rank's flag: rounds whose incoming block has landed
+  int n_rounds;
+  int gen0;                 // global round number of this epoch's round 0
+};
+
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <int N, int J, int R>
 struct TmaCfg {
   static constexpr int M = 128;
@@ -121,11 +156,12 @@ template <int N, int J>
 constexpr int tma_min_blocks() {
   return (N == 3 && J == 16) ? SPTK_TMA_MINB_3_16 : 4;
 }
-template <int N, int J, int R, bool HV>
+template <int N, int J, int R, bool HV, bool DS = false>
 __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
     factor_tma_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
                       float* __restrict__ fac, const float* __restrict__ cor, const __grid_constant__ TmaParams<N> p,
-                      const __grid_constant__ TmaMaps<N> maps, unsigned* __restrict__ tile_ctr) {
+                      const __grid_constant__ TmaMaps<N> maps, unsigned* __restrict__ tile_ctr,
+                      const __grid_constant__ DsgdParams dp) {
   constexpr int RW = N <= 3 ? 4 : (N <= 7 ? 8 : 16);
   using C = TmaCfg<N, J, R>;
   extern __shared__ __align__(16) float sm_raw[];
@@ -199,10 +235,22 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
   long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
   if (tid == 0) misc[1] = atomicAdd(tile_ctr, 1u);
   RecReg<N, RW> cur, nxt;
+  // DS: padding entries (-1) are invalid samples that read record 0
+  auto lrec = [&](RecReg<N, RW>& o, int v, long long t) {
+    if (DS)
+      load_rec<N, RW>(o, rec, v < 0 ? 0 : v, tile_valid(n_visit, t) && v >= 0, base, pol_stream);
+    else
+      load_rec<N, RW>(o, rec, v, tile_valid(n_visit, t), base, pol_stream);
+  };
   int v2 = load_vis<HV>(visit, n_visit, t2, pol_stream);
-  load_rec<N, RW>(cur, rec, load_vis<HV>(visit, n_visit, tile, pol_stream), tile_valid(n_visit, tile), base,
-                  pol_stream);
-  load_rec<N, RW>(nxt, rec, load_vis<HV>(visit, n_visit, t1, pol_stream), tile_valid(n_visit, t1), base, pol_stream);
+  lrec(cur, load_vis<HV>(visit, n_visit, tile, pol_stream), tile);
+  lrec(nxt, load_vis<HV>(visit, n_visit, t1, pol_stream), t1);
+  // DS round tracking: the round of this CTA's current tile (tiles only grow)
+  int r_cur = 0, r_waited = 0, r_tiles = 0;
+  auto adv = [&](int r, long long t) {
+    while (r + 1 < dp.n_rounds && t * 128 >= dp.rstart[r + 1]) ++r;
+    return r;
+  };
   int pb = 0, par = 0;
   stage_ids(cur, 0);
   __syncwarp();
@@ -213,6 +261,18 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
   long long t3 = 3 * G + misc[1];
   while (tile * 128 < n_visit) {
     TMA_STAMP(0);
+    if (DS) {
+      // a tile of a later round: its rotated block must have landed
+      r_cur = adv(r_cur, tile);
+      if (r_cur > r_waited) {
+        if (tid == 0) {
+          while (ld_acquire_sys(dp.ready) < dp.gen0 + r_cur) __nanosleep(64);
+          fence_proxy_async_global();
+        }
+        __syncthreads();
+        r_waited = r_cur;
+      }
+    }
     unsigned claim = 0;
     if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
     // late modes (the hot ones by default) are read at the start of their own
@@ -223,9 +283,9 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
     // the next tile's indices, for its early gathers during this tile
     stage_ids(nxt, par ^ 1);
     RecReg<N, RW> nnxt;
-    load_rec<N, RW>(nnxt, rec, v2, tile_valid(n_visit, t2), base, pol_stream);
+    lrec(nnxt, v2, t2);
     v2 = load_vis<HV>(visit, n_visit, t3, pol_stream);
-    const bool full_tile = (tile + 1) * 128 <= n_visit;
+    const bool full_tile = (tile + 1) * 128 <= (DS ? dp.rend[r_cur] : n_visit);
     TMA_STAMP(1);
 #pragma unroll
     for (int n = 0; n < N; ++n) {
@@ -405,6 +465,35 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
     pb ^= spare;
     par ^= 1;
     if (tid == 0) misc[1] = claim;
+    if (DS) {
+      ++r_tiles;
+      if (!(tile * 128 < n_visit) || adv(r_cur, tile) != r_cur) {
+        // this CTA's last tile of round r_cur: its row writes complete and
+        // visible, then count its tiles; the round's last CTA forwards the block
+        tc::bulk_wait_all();
+        fence_proxy_async_global();
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+          const int total = (int)((dp.rstart[r_cur + 1] - dp.rstart[r_cur]) / 128);
+          const int c = atomicAdd(dp.done + r_cur, r_tiles) + r_tiles;
+          __threadfence();
+          misc[2] = (c == total && dp.push[r_cur].nrows > 0) ? 1u : 0u;
+        }
+        __syncthreads();
+        if (misc[2]) {
+          const DsgdPush ps = dp.push[r_cur];
+          const long long nf4 = ps.nrows * J / 4;
+          const float4* src = reinterpret_cast<const float4*>(fac + p.foff[ps.mode] + ps.row_lo * J);
+          float4* dst = reinterpret_cast<float4*>(ps.dst);
+          for (long long e = tid; e < nf4; e += 128) dst[e] = __ldcg(src + e);
+          __threadfence_system();
+          __syncthreads();
+          if (tid == 0) atomicMax_system(ps.dst_ready, dp.gen0 + r_cur + 1);
+        }
+        r_tiles = 0;
+      }
+    }
     // late slots are re-gathered at the top of the next tile; the next c
     // round overwrites TMEM columns this tile's last loads read
     tc::bulk_wait_read();
@@ -466,7 +555,8 @@ void note_factor_kernel(const char* name) { g_last_kernel = name; }
 
 template <int N, int J, int R>
 static int launch_tma(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
-                      const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+                      const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s,
+                      const DsgdParams* dsp = nullptr, int grid = 0) {
   using C = TmaCfg<N, J, R>;
   if (encode_fn()) return 1;
   (void)rw;
@@ -480,6 +570,8 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
   p.atomic_mask = hot_mode_mask(md);
   p.early_mask = ~p.atomic_mask & ((1u << N) - 1u);
   if (const char* e = getenv("SPTK_TMA_EARLY")) p.early_mask = (unsigned)strtoul(e, nullptr, 0) & ((1u << N) - 1u);
+  // DSGD: only the stationary mode 0 may be gathered ahead of a round's wait
+  if (dsp) p.early_mask &= 1u;
   {
     const char* e = getenv("SPTK_TMA_BULKRED");
     p.bulk_red = e ? atoi(e) : 0;
@@ -498,12 +590,14 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
     }
     maps_fac = fac;
   }
-  auto kfn = visit ? factor_tma_kernel<N, J, R, true> : factor_tma_kernel<N, J, R, false>;
+  auto kfn = dsp ? factor_tma_kernel<N, J, R, true, true>
+                 : (visit ? factor_tma_kernel<N, J, R, true> : factor_tma_kernel<N, J, R, false>);
   const size_t smem = (p.early_mask >> (N - 1) & 1u) ? C::SMEM_SPARE : C::SMEM;
   static int per_sm = 0;
   static size_t per_sm_smem = 0;
   if (per_sm_smem != smem) {
-    for (auto f : {factor_tma_kernel<N, J, R, true>, factor_tma_kernel<N, J, R, false>}) {
+    for (auto f : {factor_tma_kernel<N, J, R, true>, factor_tma_kernel<N, J, R, false>,
+                   factor_tma_kernel<N, J, R, true, true>}) {
       SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_SPARE));
       SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
@@ -517,15 +611,24 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
   long long blocks = 148LL * per_sm - (per_sm >= 2 ? slots : 0);
   if (const char* e = getenv("SPTK_TC_GRID")) blocks = atoll(e);
   if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
+  // DSGD: a persistent grid (every CTA resident: a CTA may wait on a round
+  // flag while earlier tiles are still running elsewhere); grid > 0 caps it
+  // (two ranks sharing one GPU in the tests)
+  if (dsp && grid > 0 && blocks > grid) blocks = grid;
   if (blocks < 1) blocks = 1;
   if (blocks > tiles) blocks = tiles;
   unsigned* ctr = nullptr;
   SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tma_tile_ctr));
   ctr += g_tma_ctr_slot.fetch_add(1u) & 63u;
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
-  kfn<<<(unsigned)blocks, 128, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, maps, ctr);
+  DsgdParams dp{};
+  if (dsp) {
+    dp = *dsp;
+    SPTK_CUDA_TRY(cudaMemsetAsync(dp.done, 0, sizeof(int) * dp.n_rounds, s));
+  }
+  kfn<<<(unsigned)blocks, 128, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, maps, ctr, dp);
   SPTK_CHECK_LAUNCH();
-  note_factor_kernel("factor_tma_kernel");
+  note_factor_kernel(dsp ? "factor_tma_kernel<dsgd>" : "factor_tma_kernel");
   return 0;
 }
 
@@ -548,5 +651,36 @@ int try_factor_tma(const int* rec, int rw, const int* visit, long long n_visit, 
 #undef SPTK_TMA_CASE
   return 0;
 }
+
+// One rank's whole epoch of DSGD rounds in one launch (see DsgdParams).
+int factor_pass_dsgd(const int* rec, int rw, const int* visit, long long n_visit, float* fac, const float* cor,
+                     const ModelDesc& md, const float* gam, const float* lam, const long long* rstart,
+                     const long long* rend, const void* push, int* done, int* ready, int n_rounds, int gen0, int grid,
+                     cudaStream_t s) {
+  const int N = md.n_modes, R = md.rcore, J = md.jr[0];
+  for (int n = 0; n < N; ++n)
+    SPTK_REQUIRE(md.jr[n] == J, "factor_pass_dsgd: needs uniform J (got J_%d = %d)", n, md.jr[n]);
+  SPTK_REQUIRE(J == R && rw == rec_words(N), "factor_pass_dsgd: needs J == R and fp32 records");
+  SPTK_REQUIRE(n_visit % 128 == 0, "factor_pass_dsgd: the visit list must be padded to whole tiles");
+  SPTK_REQUIRE(n_rounds >= 1, "factor_pass_dsgd: no rounds");
+  DsgdParams dp;
+  dp.rstart = rstart;
+  dp.rend = rend;
+  dp.push = (const DsgdPush*)push;
+  dp.done = done;
+  dp.ready = ready;
+  dp.n_rounds = n_rounds;
+  dp.gen0 = gen0;
+#define SPTK_DSGD_CASE(NN, JJ)                                                                               \
+  if (N == NN && J == JJ)                                                                                    \
+    return launch_tma<NN, JJ, JJ>(rec, rw, visit, n_visit, 0, fac, cor, md, gam, lam, s, &dp, grid);
+  SPTK_DSGD_CASE(3, 16)
+  SPTK_DSGD_CASE(4, 16)
+  SPTK_DSGD_CASE(3, 8)
+  SPTK_DSGD_CASE(6, 8)
+#undef SPTK_DSGD_CASE
+  SPTK_REQUIRE(false, "factor_pass_dsgd: no fused DSGD kernel for order %d, J = R = %d", N, J);
+}
+size_t dsgd_push_bytes() { return sizeof(DsgdPush); }
 
 }  // namespace sptk

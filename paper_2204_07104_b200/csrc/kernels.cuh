@@ -66,6 +66,11 @@ int try_factor_tc(const int* rec, int rw, const int* visit, long long n_visit, l
 // factor_tma.cu (tcgen05 + TMA row traffic; returns 1 if it handled the launch)
 int try_factor_tma(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
                    const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc);
+int factor_pass_dsgd(const int* rec, int rw, const int* visit, long long n_visit, float* fac, const float* cor,
+                     const ModelDesc& md, const float* gam, const float* lam, const long long* rstart,
+                     const long long* rend, const void* push, int* done, int* ready, int n_rounds, int gen0, int grid,
+                     cudaStream_t s);
+size_t dsgd_push_bytes();
 // name of the factor kernel the last factor_pass dispatched to
 const char* last_factor_kernel();
 void note_factor_kernel(const char* name);

@@ -144,3 +144,52 @@ def predict_device_f64(model, indices: np.ndarray) -> np.ndarray:
     check(_lib.load().sptk_eval_f64(ptr(coo.rec), coo.rw, m, ptr(dm.fac), dm.p_foff, ptr(dm.cor), dm.p_coff,
                                     dm.p_jr, dm.order, dm.rcore, ptr(out), None, stream_ptr()), "sptk_eval_f64")
     return out[:m].cpu().numpy()
+
+
+class SharedBuffer:
+    """Device memory another process (or GPU) can map: cudaMalloc'd by libsptk
+    (sptk_shared_alloc) so its CUDA IPC handle covers exactly this buffer.
+    ``view`` returns zero-copy torch tensors over it.  Freed by ``close``."""
+
+    _TYPESTR = {"float32": "<f4", "int32": "<i4", "float64": "<f8", "int64": "<i8", "uint8": "|u1"}
+
+    def __init__(self, nbytes: int):
+        import ctypes
+
+        p = ctypes.c_void_p()
+        check(_lib.load().sptk_shared_alloc(int(nbytes), ctypes.byref(p)), "sptk_shared_alloc")
+        self.ptr = int(p.value)
+        self.nbytes = int(nbytes)
+
+    def view(self, dtype, numel: int, offset: int = 0):
+        torch = _torch()
+        name = str(dtype).replace("torch.", "")
+
+        class _Cai:
+            pass
+
+        o = _Cai()
+        o.__cuda_array_interface__ = {"shape": (int(numel),), "typestr": self._TYPESTR[name],
+                                      "data": (self.ptr + int(offset), False), "version": 3, "strides": None}
+        return torch.as_tensor(o, device="cuda")
+
+    def ipc_handle(self) -> bytes:
+        import ctypes
+
+        buf = ctypes.create_string_buffer(64)
+        check(_lib.load().sptk_ipc_get(self.ptr, buf), "sptk_ipc_get")
+        return buf.raw
+
+    def close(self) -> None:
+        if self.ptr:
+            check(_lib.load().sptk_shared_free(self.ptr), "sptk_shared_free")
+            self.ptr = 0
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer's SharedBuffer (its ipc_handle()); returns the device address."""
+    import ctypes
+
+    p = ctypes.c_void_p()
+    check(_lib.load().sptk_ipc_open(bytes(handle), ctypes.byref(p)), "sptk_ipc_open")
+    return int(p.value)

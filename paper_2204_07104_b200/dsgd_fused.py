@@ -1,0 +1,228 @@
+"""Multi-GPU DSGD with the ring shift fused into the factor kernel.
+
+The reference runs the rounds of its DSGD schedule on W threads with a
+barrier per round (trainer.py:189-208; partition.py:100-117): rank w holds
+mode-0 block w for good, and between consecutive rounds exactly one mode's
+blocks move one rank along the ring.  On B200s that barrier and the move are
+the problem (NF at 8 GPUs: 64 rounds of ~20 us of work each), so here every
+rank runs its whole epoch of rounds as ONE persistent launch
+(sptk_factor_pass_dsgd):
+
+* the rank's visit list holds its block of every round, round after round,
+  each round padded to whole 128-sample tiles;
+* a tile of round r >= 1 starts once the block rotated in for round r has
+  landed (the rank's ready flag, raised by the sender at system scope);
+* the CTA that finishes the rank's last tile of round r copies the block the
+  rank hands on straight into its next owner's model over NVLink (peer
+  stores into memory mapped with CUDA IPC) and raises that rank's flag.
+
+No host round trip, launch or NCCL call per round.  After the epoch's last
+round the ranks exchange the blocks they hold (one NCCL all-gather) and
+all-reduce the B gradients, as dist.DistRunner does.
+
+``FusedRankRunner`` is transport-agnostic (peer addresses are given); the
+tests run two of them on one GPU (two streams, both grids resident) against
+the oracle.  ``FusedDistRunner`` is the torch.distributed rank (IPC handles
+exchanged with all_gather_object).
+"""
+
+from __future__ import annotations
+
+from dataclasses import replace
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, ptr, stream_ptr
+from .device import SharedBuffer, ipc_open
+from .dist import DistRunner, DsgdPlan
+from .sampler import BLOCK_PERM_MAX, BlockOrders
+from .training import EpochRunner
+
+PUSH_DTYPE = np.dtype([("row_lo", "<i8"), ("nrows", "<i8"), ("mode", "<i8"), ("dst", "<u8"), ("dst_ready", "<u8")])
+TILE = 128
+
+
+def fused_supported(model, config) -> bool:
+    """The fused kernel covers the TMA factor kernel's shapes in throughput mode."""
+    J = int(model.j_ranks[0])
+    return (config.update_mode == "hogwild" and config.precision == "fp32"
+            and all(int(j) == J for j in model.j_ranks) and J == int(model.r_core)
+            and (model.order, J) in ((3, 16), (4, 16), (3, 8), (6, 8)))
+
+
+class FusedState:
+    """Device state of one rank's fused DSGD factor phase (see module doc)."""
+
+    def __init__(self, runner: EpochRunner, plan: DsgdPlan, rank: int):
+        import torch
+
+        self.runner, self.plan, self.rank = runner, plan, rank
+        dev = runner.dm.fac.device
+        R = plan.n_rounds
+        # the rank's block of every round (kept even when empty: its tile is
+        # what forwards the block to the next owner)
+        rounds = []
+        for r in range(R):
+            block = plan.block_of(rank, r)
+            off, cnt = runner.part.block_range(block)
+            rounds.append([(block, off, cnt)] if cnt > 0 else [])
+        self.big = max((c for rnd in rounds for (_, _, c) in rnd), default=0) > BLOCK_PERM_MAX
+        self.orders = BlockOrders(rounds, runner.order, dev, big=self.big, pad=TILE)
+        self.total = self.orders.total
+        self.fvis = [torch.full((self.total,), -1, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.rstart = torch.tensor(self.orders.round_start, dtype=torch.int64, device=dev)
+        self.rend = torch.tensor(self.orders.round_end, dtype=torch.int64, device=dev)
+        self.done = torch.zeros(R, dtype=torch.int32, device=dev)
+        # the model replica other ranks write into, plus this rank's flag
+        dm = runner.dm
+        fac_bytes = dm.fac.numel() * dm.fac.element_size()
+        self.flag_off = (fac_bytes + 255) // 256 * 256
+        self.shared = SharedBuffer(self.flag_off + 256)
+        fac = self.shared.view(dm.fac.dtype, dm.fac.numel())
+        fac.copy_(dm.fac)
+        dm.fac = fac
+        self.ready = self.shared.view("int32", 1, self.flag_off)
+        self.push = None
+        # Hogwild staleness inside a rank: a round's block covers 1/M of every
+        # mode's rows, so a full grid would put M times more concurrent
+        # updates on each hot row than on one GPU.  Measured on one GPU with
+        # the 8-worker NF blocks launched one by one at full occupancy (the
+        # per-rank dynamics of 8-GPU DSGD): test RMSE NaN; with at most
+        # block/16 samples in flight: 0.4832 (the reference's W=8 curve).
+        # So the persistent grid holds at most (largest block)/SPAN samples,
+        # SPAN = 16 (SPTK_DSGD_SPAN).
+        import os
+
+        span = int(os.environ.get("SPTK_DSGD_SPAN", "16"))
+        biggest = max((c for rnd in rounds for (_, _, c) in rnd), default=TILE)
+        self.grid = max(1, biggest // max(span, 1) // TILE) if span > 0 else 0
+
+    # -- peers ---------------------------------------------------------------
+    def peer_addresses(self):
+        """(fac address, ready-flag address) of this rank's shared buffer."""
+        return self.shared.ptr, self.shared.ptr + self.flag_off
+
+    def set_peers(self, fac_addrs, ready_addrs) -> None:
+        """Build the per-round push table from every rank's (mapped) addresses."""
+        import torch
+
+        plan, dm = self.plan, self.runner.dm
+        R = plan.n_rounds
+        tab = np.zeros(R, dtype=PUSH_DTYPE)
+        for r in range(R - 1):
+            mine = [(n, b, dst) for n, b, src, dst in plan.transfers(r, r + 1) if src == self.rank]
+            if len(mine) > 1:
+                raise RuntimeError(f"round {r}: rank {self.rank} would send {len(mine)} blocks")
+            for n, b, dst in mine:
+                lo, hi = plan.rows(n, b)
+                J = int(dm.jr[n])
+                tab[r] = (lo, hi - lo, n, int(fac_addrs[dst]) + 4 * (int(dm.foff[n]) + lo * J),
+                          int(ready_addrs[dst]))
+        if int(_lib.load().sptk_dsgd_push_bytes()) != PUSH_DTYPE.itemsize:
+            raise RuntimeError("DsgdPush layout mismatch between libsptk and dsgd_fused.py")
+        self.push = torch.from_numpy(tab.view(np.uint8).copy()).to(self.runner.dm.fac.device)
+
+    # -- visit orders ----------------------------------------------------------
+    def draw(self, t: int, slot: int, stream) -> None:
+        """This rank's visit list of epoch t into fvis[slot] (padding stays -1)."""
+        r = self.runner
+        if not self.big:
+            self.orders.draw(r.cfg.seed, t, self.fvis[slot], stream=stream)
+        else:
+            self.orders.interleave(r.perm[slot], r.lo if r.batched_fy else -1, self.fvis[slot], stream=stream)
+
+    def launch(self, t: int, gamma_a: float, slot: int) -> None:
+        r, dm = self.runner, self.runner.dm
+        if self.push is None:
+            raise RuntimeError("set_peers() first")
+        r._gam[:] = gamma_a
+        R = self.plan.n_rounds
+        check(r.L.sptk_factor_pass_dsgd(ptr(r.part.rec), r.part.rw, ptr(self.fvis[slot]), self.total, ptr(dm.fac),
+                                        dm.p_foff, ptr(dm.cor), dm.p_coff, dm.p_jr, r.order, dm.rcore, r.p_gam,
+                                        r.p_lam, ptr(self.rstart), ptr(self.rend), ptr(self.push), ptr(self.done),
+                                        ptr(self.ready), R, t * R, int(self.grid), stream_ptr()),
+              "sptk_factor_pass_dsgd")
+
+
+class _FusedMixin:
+    """EpochRunner overrides: visit orders into the padded per-rank list, one
+    fused launch per epoch instead of one launch (and exchange) per round."""
+
+    fused: FusedState
+
+    def draw_jseq(self, t, slot, stream):
+        if not self.fused.big:
+            self.j_epoch[slot] = t  # the block CTAs draw their j-sequences themselves
+            return
+        super().draw_jseq(t, slot, stream)
+
+    def apply_jseq(self, t, slot, stream):
+        if self.fused.big:
+            super().apply_jseq(t, slot, stream)
+        self.fused.draw(t, slot, stream)
+        self.sampled_epoch[slot] = t
+
+    def factor_phase(self, t, gamma_a, slot):
+        if self.factor_events is not None:
+            e0 = self.torch.cuda.Event(enable_timing=True)
+            e0.record()
+        self.fused.launch(t, gamma_a, slot)
+        if self.factor_events is not None:
+            e1 = self.torch.cuda.Event(enable_timing=True)
+            e1.record()
+            self.factor_events.append((e0, e1))
+        self.after_factor_phase()
+        return self.nnz_local
+
+
+class FusedRankRunner(_FusedMixin, EpochRunner):
+    """One rank of the fused DSGD epoch without a process group (tests, the
+    per-rank simulation): peers are given as device addresses with
+    ``set_peers``; the epoch-end block exchange and the B all-reduce are left
+    to the caller."""
+
+    def __init__(self, model, train_set, config, rank: int, world: int, prefetch: bool = True):
+        if config.workers != world:
+            config = replace(config, workers=world)
+        super().__init__(model, train_set, config, prefetch=prefetch, owner_rank=rank)
+        self.rank, self.world = rank, world
+        self.plan = DsgdPlan(model.dims, world)
+        self.fused = FusedState(self, self.plan, rank)
+
+    def set_peers(self, fac_addrs, ready_addrs):
+        self.fused.set_peers(fac_addrs, ready_addrs)
+
+
+class FusedDistRunner(_FusedMixin, DistRunner):
+    """dist.DistRunner with the rounds fused: the ranks map each other's model
+    replicas (CUDA IPC over NVLink/NVSwitch) once, then every epoch is one
+    launch per rank plus the epoch-end all-gather and B all-reduce."""
+
+    def __init__(self, model, train_set, config, group=None):
+        import torch.distributed as td
+
+        super().__init__(model, train_set, config, group)
+        self.fused = FusedState(self, self.plan, self.rank)
+        self.ex.fac = self.dm.fac  # the exchange works on the shared replica
+        mine = (self.fused.shared.ipc_handle(), self.fused.flag_off)
+        allh = [None] * self.world
+        td.all_gather_object(allh, mine, group=group)
+        self._mapped = []
+        facs, readys = [], []
+        for q, (h, foff) in enumerate(allh):
+            if q == self.rank:
+                a = self.fused.shared.ptr
+            else:
+                a = ipc_open(h)
+                self._mapped.append(a)
+            facs.append(a)
+            readys.append(a + foff)
+        self.fused.set_peers(facs, readys)
+        td.barrier(group=group)
+
+    def after_round(self, r):  # no per-round exchange: the kernel forwards blocks itself
+        pass
+
+
+__all__ = ["FusedState", "FusedRankRunner", "FusedDistRunner", "fused_supported"]

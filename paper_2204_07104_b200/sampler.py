@@ -160,12 +160,13 @@ class BlockOrders:
 
     rounds: list of rounds, each a list of (block tuple, off, n)."""
 
-    def __init__(self, rounds, order: int, device, big: bool = False):
+    def __init__(self, rounds, order: int, device, big: bool = False, pad: int = 1):
         import torch
 
         # big=True: blocks above BLOCK_PERM_MAX; only the job table is built
         # and interleave() lays out visit orders drawn elsewhere
         self.big = big
+        self.round_start, self.round_end = [], []
         jobs, coords, base = [], [], 0
         for rnd in rounds:
             first, m = len(jobs), len(rnd)
@@ -177,7 +178,15 @@ class BlockOrders:
                     raise ValueError(f"block of {n} nonzeros exceeds {BLOCK_PERM_MAX}")
                 jobs.append((off, base, n, first, m, slot, nmin, 0))
                 coords.append(tuple(int(c) for c in block))
+            self.round_start.append(base)
+            self.round_end.append(base + sum(n for _, _, n in rnd))
+            # pad > 1: every round starts on a multiple of pad (and takes at
+            # least one pad unit even when empty); the gaps stay untouched
             base += sum(n for _, _, n in rnd)
+            if pad > 1:
+                base = max(base, self.round_start[-1] + pad)
+                base = (base + pad - 1) // pad * pad
+        self.round_start.append(base)
         self.total = base
         self.n_jobs = len(jobs)
         self.order = order

@@ -1,0 +1,94 @@
+"""Fused multi-GPU DSGD (sptk_factor_pass_dsgd, dsgd_fused.py) with two ranks
+sharing one GPU: each rank runs its whole epoch of rounds as one persistent
+launch on its own stream, waits on its ready flag for every rotated block and
+forwards the block it hands on into the other rank's model by device stores.
+
+On blocks whose samples touch pairwise-distinct rows the Hogwild order does
+not matter, so the two ranks' factor phase must equal the reference's
+2-worker DSGD factor phase (trainer.py:189-208, the oracle) at the TF32
+tolerance of the tcgen05 kernel."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _conflict_free(dims, per_block, m, seed):
+    """per_block samples in every DSGD block (m per mode), rows pairwise
+    distinct inside each block."""
+    from paper_2204_07104_b200.schedule import cut_points
+
+    rng = np.random.default_rng(seed)
+    cuts = cut_points(dims, m)
+    idx = []
+    for key in np.ndindex(*(m,) * len(dims)):
+        cols = []
+        for n, b in enumerate(key):
+            lo, hi = cuts[n][b], cuts[n][b + 1]
+            cols.append(lo + rng.permutation(hi - lo)[:per_block])
+        idx.append(np.stack(cols, axis=1))
+    idx = np.concatenate(idx)
+    idx = idx[rng.permutation(len(idx))]
+    return idx, rng.normal(2.0, 1.0, len(idx))
+
+
+@pytest.mark.parametrize("dims,J,per_block", [((3000, 2800, 2600), 16, 700), ((1200, 1100, 1000, 900), 16, 300),
+                                               ((3000, 2800, 2600), 8, 700)])
+def test_two_ranks_one_gpu_match_reference_dsgd(dims, J, per_block):
+    from paper_2204_07104_b200 import ModelConfig, SparseTensorCoo, TrainConfig, init_model
+    from paper_2204_07104_b200.dsgd_fused import FusedRankRunner
+    from paper_2204_07104_b200.training import learning_rate
+
+    W, E = 2, 2
+    order = len(dims)
+    idx, vals = _conflict_free(dims, per_block, W, 5)
+    tensor = SparseTensorCoo(tuple(dims), idx, vals)
+    model = init_model(dims, ModelConfig((J,) * order, J, 1.0, seed=1))
+    cfg = TrainConfig(epochs=E, workers=W, seed=1, alpha_a=0.003, update_mode="hogwild", update_core=False)
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    ranks = []
+    for w in range(W):
+        with torch.cuda.stream(streams[w]):
+            ranks.append(FusedRankRunner(model, tensor, cfg, w, W, prefetch=False))
+    torch.cuda.synchronize()
+    addrs = [rk.fused.peer_addresses() for rk in ranks]
+    for rk in ranks:
+        rk.set_peers([a for a, _ in addrs], [b for _, b in addrs])
+        rk.fused.grid = 64  # both persistent grids resident on the one GPU
+    plan = ranks[0].plan
+    dm0 = ranks[0].dm
+    for t in range(E):
+        ga = learning_rate(cfg.alpha_a, cfg.beta_a, t)
+        for w, rk in enumerate(ranks):
+            with torch.cuda.stream(streams[w]):
+                slot = rk._ensure_samples(t)
+        torch.cuda.synchronize()
+        for w, rk in enumerate(ranks):
+            with torch.cuda.stream(streams[w]):
+                rk.factor_phase(t, ga, slot)
+        torch.cuda.synchronize()
+        # epoch-end exchange: every rank gets the blocks the others hold
+        for q, src in enumerate(ranks):
+            for n, b in enumerate(plan.held_blocks(q, plan.n_rounds - 1)):
+                lo, hi = plan.rows(n, b)
+                a, z = int(dm0.foff[n]) + lo * J, int(dm0.foff[n]) + hi * J
+                for w, dst in enumerate(ranks):
+                    if w != q:
+                        dst.dm.fac[a:z].copy_(src.dm.fac[a:z])
+        torch.cuda.synchronize()
+    got = ranks[0].dm.fac.double().cpu().numpy()
+    assert np.array_equal(got, ranks[1].dm.fac.double().cpu().numpy())
+    fs = [a.copy() for a in model.factors]
+    bs = [b.copy() for b in model.core_factors]
+    O.train(fs, bs, idx, vals, epochs=E, workers=W, seed=1, alpha_a=0.003, update_core=False, evaluate=False,
+            dims=tuple(dims))
+    want, _ = O.pack(fs)
+    init, _ = O.pack(model.factors)
+    assert not np.allclose(want, init)
+    np.testing.assert_allclose(got, want, rtol=5e-3, atol=5e-4 * np.abs(want).max())
+    for rk in ranks:
+        assert rk.L.sptk_last_factor_kernel().decode() == "factor_tma_kernel<dsgd>"
