@@ -245,7 +245,12 @@ def bench_ours(args, cfg):
     if distributed:
         from paper_2204_07104_b200 import dist
 
-        runner = dist.DistRunner(model, tr, tcfg)
+        from paper_2204_07104_b200.dsgd_fused import FusedDistRunner, fused_supported
+
+        if fused_supported(model, tcfg, tr.nnz) and os.environ.get("SPTK_DSGD_FUSED", "1") == "1":
+            runner = FusedDistRunner(model, tr, tcfg)
+        else:
+            runner = dist.DistRunner(model, tr, tcfg)
     elif sim > 1:
         # one rank's share of an M-GPU DSGD epoch (its blocks, their samplers,
         # the core phase): the fused per-rank launch with its pushes aimed at
@@ -261,6 +266,7 @@ def bench_ours(args, cfg):
             fa, ra = runner.fused.peer_addresses()
             runner.set_peers([fa] * sim, [ra] * sim)
             runner.fused.ready.fill_(1 << 30)
+            runner.fused.epoch_flag.fill_(1 << 30)
         else:
             runner = EpochRunner(model, tr, tcfg, owner_rank=0)
     else:

@@ -221,9 +221,11 @@ int sptk_factor_pass_exact_f64(const int32_t* d_rec, int rw, const int32_t* d_vi
  * round r >= 1 start once *d_ready >= gen0 + r (the block rotated in for
  * round r has landed); after its last tile of round r the rank copies the
  * block described by d_push[r] (sptk_dsgd_push_bytes() bytes each: {int64
- * row_lo, int64 nrows, int64 mode, float* dst, int32* dst_ready}; nrows = 0:
- * none) to its next owner's model (peer pointer: NVLink stores) and raises
- * that rank's flag to gen0 + r + 1 (release, system scope).  d_done:
+ * row_lo, int64 nrows, int64 mode, float* dst, int32* dst_ready, int32*
+ * dst_gathered}; nrows = 0: none) to its next owner's model (peer pointer:
+ * NVLink stores) -- once that rank's epoch flag *dst_gathered >= epoch, i.e.
+ * its previous epoch-end exchange has been written -- and raises that rank's
+ * ready flag to gen0 + r + 1 (release, system scope).  d_done:
  * n_rounds ints of scratch.  grid > 0 caps the persistent grid (all CTAs of
  * every rank sharing a GPU must be resident).  Uniform J = R, TMA kernel
  * shapes (order 3/4 at J = 16, 3/6 at J = 8). */
@@ -231,8 +233,11 @@ int sptk_factor_pass_dsgd(const int32_t* d_rec, int rw, const int32_t* d_visit, 
                           const int64_t* h_foff, const float* d_cor, const int64_t* h_coff, const int64_t* h_jr,
                           int n_modes, int rcore, const double* h_gammas, const double* h_lambdas,
                           const long long* d_rstart, const long long* d_rend, const void* d_push, int32_t* d_done,
-                          int32_t* d_ready, int n_rounds, int gen0, int grid, void* stream);
+                          int32_t* d_ready, int n_rounds, int gen0, int epoch, int grid, void* stream);
 size_t sptk_dsgd_push_bytes(void);
+/* *d_flag = max(*d_flag, value) at system scope, in stream order (a rank's
+ * epoch flag after its epoch-end exchange). */
+int sptk_flag_store(int32_t* d_flag, int value, void* stream);
 /* Device memory other processes can map (cudaMalloc'd, zeroed) and its CUDA
  * IPC handle (64 bytes); sptk_ipc_open maps a peer's allocation (peer access
  * enabled lazily: NVLink loads/stores on NVSwitch systems). */

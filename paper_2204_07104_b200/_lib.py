@@ -75,8 +75,9 @@ SIGNATURES = {
                                                   ctypes.c_size_t, _vp]),
     "sptk_factor_pass_dsgd": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _vp, _i64p, _vp, _i64p, _i64p,
                                              ctypes.c_int, ctypes.c_int, _f64p, _f64p, _vp, _vp, _vp, _vp, _vp,
-                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]),
+                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]),
     "sptk_dsgd_push_bytes": (ctypes.c_size_t, []),
+    "sptk_flag_store": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
     "sptk_shared_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(_vp)]),
     "sptk_shared_free": (ctypes.c_int, [_vp]),
     "sptk_ipc_get": (ctypes.c_int, [_vp, ctypes.c_char_p]),

@@ -235,7 +235,7 @@ int sptk_factor_pass_dsgd(const int32_t* d_rec, int rw, const int32_t* d_visit, 
                           const int64_t* h_foff, const float* d_cor, const int64_t* h_coff, const int64_t* h_jr,
                           int n_modes, int rcore, const double* h_gammas, const double* h_lambdas,
                           const long long* d_rstart, const long long* d_rend, const void* d_push, int32_t* d_done,
-                          int32_t* d_ready, int n_rounds, int gen0, int grid, void* stream) {
+                          int32_t* d_ready, int n_rounds, int gen0, int epoch, int grid, void* stream) {
   ModelDesc md;
   if (build_model_desc(&md, h_foff, h_coff, h_jr, n_modes, rcore)) return 2;
   float g[SPTK_MAX_MODES], l[SPTK_MAX_MODES];
@@ -244,10 +244,14 @@ int sptk_factor_pass_dsgd(const int32_t* d_rec, int rw, const int32_t* d_visit, 
     l[n] = (float)h_lambdas[n];
   }
   return factor_pass_dsgd(d_rec, rw, d_visit, n_visit, d_fac, d_cor, md, g, l, d_rstart, d_rend, d_push, d_done,
-                          d_ready, n_rounds, gen0, grid, (cudaStream_t)stream);
+                          d_ready, n_rounds, gen0, epoch, grid, (cudaStream_t)stream);
 }
 
 size_t sptk_dsgd_push_bytes(void) { return dsgd_push_bytes(); }
+
+int sptk_flag_store(int32_t* d_flag, int value, void* stream) {
+  return flag_store(d_flag, value, (cudaStream_t)stream);
+}
 
 int sptk_shared_alloc(size_t bytes, void** d_ptr) {
   *d_ptr = nullptr;

@@ -66,6 +66,7 @@ struct DsgdPush {
   long long mode;
   float* dst;        // the receiving rank's copy of row row_lo (peer pointer)
   int* dst_ready;    // the receiving rank's ready flag (peer pointer)
+  int* dst_gathered; // the receiving rank's epoch flag: its epoch-end exchange of epoch e-1 is written (peer)
 };
 struct DsgdParams {
   const long long* rstart;  // [n_rounds + 1] first visit slot of each round (multiples of 128)
@@ -75,6 +76,7 @@ struct DsgdParams {
   int* ready;               // this rank's flag: rounds whose incoming block has landed
   int n_rounds;
   int gen0;                 // global round number of this epoch's round 0
+  int epoch;                // the receiver's epoch flag must be >= this before a push lands
 };
 
 __device__ __forceinline__ int ld_acquire_sys(const int* p) {
@@ -483,6 +485,11 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
         __syncthreads();
         if (misc[2]) {
           const DsgdPush ps = dp.push[r_cur];
+          // the receiver must be past the previous epoch's block exchange,
+          // which rewrites its replica (else this block would be overwritten)
+          if (tid == 0)
+            while (ld_acquire_sys(ps.dst_gathered) < dp.epoch) __nanosleep(64);
+          __syncthreads();
           const long long nf4 = ps.nrows * J / 4;
           const float4* src = reinterpret_cast<const float4*>(fac + p.foff[ps.mode] + ps.row_lo * J);
           float4* dst = reinterpret_cast<float4*>(ps.dst);
@@ -655,8 +662,8 @@ int try_factor_tma(const int* rec, int rw, const int* visit, long long n_visit, 
 // One rank's whole epoch of DSGD rounds in one launch (see DsgdParams).
 int factor_pass_dsgd(const int* rec, int rw, const int* visit, long long n_visit, float* fac, const float* cor,
                      const ModelDesc& md, const float* gam, const float* lam, const long long* rstart,
-                     const long long* rend, const void* push, int* done, int* ready, int n_rounds, int gen0, int grid,
-                     cudaStream_t s) {
+                     const long long* rend, const void* push, int* done, int* ready, int n_rounds, int gen0, int epoch,
+                     int grid, cudaStream_t s) {
   const int N = md.n_modes, R = md.rcore, J = md.jr[0];
   for (int n = 0; n < N; ++n)
     SPTK_REQUIRE(md.jr[n] == J, "factor_pass_dsgd: needs uniform J (got J_%d = %d)", n, md.jr[n]);
@@ -671,6 +678,7 @@ int factor_pass_dsgd(const int* rec, int rw, const int* visit, long long n_visit
   dp.ready = ready;
   dp.n_rounds = n_rounds;
   dp.gen0 = gen0;
+  dp.epoch = epoch;
 #define SPTK_DSGD_CASE(NN, JJ)                                                                               \
   if (N == NN && J == JJ)                                                                                    \
     return launch_tma<NN, JJ, JJ>(rec, rw, visit, n_visit, 0, fac, cor, md, gam, lam, s, &dp, grid);
@@ -682,5 +690,13 @@ int factor_pass_dsgd(const int* rec, int rw, const int* visit, long long n_visit
   SPTK_REQUIRE(false, "factor_pass_dsgd: no fused DSGD kernel for order %d, J = R = %d", N, J);
 }
 size_t dsgd_push_bytes() { return sizeof(DsgdPush); }
+
+__global__ void flag_store_kernel(int* flag, int value) { atomicMax_system(flag, value); }
+
+int flag_store(int* flag, int value, cudaStream_t s) {
+  flag_store_kernel<<<1, 1, 0, s>>>(flag, value);
+  SPTK_CHECK_LAUNCH();
+  return 0;
+}
 
 }  // namespace sptk

@@ -68,9 +68,10 @@ int try_factor_tma(const int* rec, int rw, const int* visit, long long n_visit, 
                    const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc);
 int factor_pass_dsgd(const int* rec, int rw, const int* visit, long long n_visit, float* fac, const float* cor,
                      const ModelDesc& md, const float* gam, const float* lam, const long long* rstart,
-                     const long long* rend, const void* push, int* done, int* ready, int n_rounds, int gen0, int grid,
-                     cudaStream_t s);
+                     const long long* rend, const void* push, int* done, int* ready, int n_rounds, int gen0, int epoch,
+                     int grid, cudaStream_t s);
 size_t dsgd_push_bytes();
+int flag_store(int* flag, int value, cudaStream_t s);
 // name of the factor kernel the last factor_pass dispatched to
 const char* last_factor_kernel();
 void note_factor_kernel(const char* name);

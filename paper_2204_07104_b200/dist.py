@@ -246,7 +246,16 @@ def train_distributed(model, split, config):
     from .device import DeviceCoo, rmse_mae_device
     from .training import MetricsRow, _RecordView, learning_rate
 
-    runner = DistRunner(model, split.train, config)
+    import os
+
+    from .dsgd_fused import FusedDistRunner, fused_supported
+
+    # throughput mode on the TMA kernel shapes: one fused launch per rank per
+    # epoch (dsgd_fused); otherwise one launch + exchange per round
+    if fused_supported(model, config, split.train.nnz) and os.environ.get("SPTK_DSGD_FUSED", "1") == "1":
+        runner = FusedDistRunner(model, split.train, config)
+    else:
+        runner = DistRunner(model, split.train, config)
     test_coo = DeviceCoo(split.test.indices, split.test.values, f64=runner.f64) if split.test.nnz else None
     train_eval = _RecordView(runner.part)
     rows, wall, pending = [], 0.0, []

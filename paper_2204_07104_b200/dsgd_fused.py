@@ -39,14 +39,21 @@ from .dist import DistRunner, DsgdPlan
 from .sampler import BLOCK_PERM_MAX, BlockOrders
 from .training import EpochRunner
 
-PUSH_DTYPE = np.dtype([("row_lo", "<i8"), ("nrows", "<i8"), ("mode", "<i8"), ("dst", "<u8"), ("dst_ready", "<u8")])
+PUSH_DTYPE = np.dtype([("row_lo", "<i8"), ("nrows", "<i8"), ("mode", "<i8"), ("dst", "<u8"), ("dst_ready", "<u8"),
+                       ("dst_gathered", "<u8")])
 TILE = 128
 
 
-def fused_supported(model, config) -> bool:
-    """The fused kernel covers the TMA factor kernel's shapes in throughput mode."""
+def fused_supported(model, config, nnz: int | None = None) -> bool:
+    """The fused kernel covers the TMA factor kernel's shapes in throughput
+    mode ("auto" resolves by the training-set size, as EpochRunner does)."""
+    from .training import resolve_mode
+
     J = int(model.j_ranks[0])
-    return (config.update_mode == "hogwild" and config.precision == "fp32"
+    mode = config.update_mode
+    if mode == "auto":
+        mode = "hogwild" if nnz is not None and resolve_mode(mode, nnz) == 0 else "exact"
+    return (mode == "hogwild" and config.precision == "fp32"
             and all(int(j) == J for j in model.j_ranks) and J == int(model.r_core)
             and (model.order, J) in ((3, 16), (4, 16), (3, 8), (6, 8)))
 
@@ -82,7 +89,10 @@ class FusedState:
         fac = self.shared.view(dm.fac.dtype, dm.fac.numel())
         fac.copy_(dm.fac)
         dm.fac = fac
+        # flags: [0] ready (rounds landed), [1] epoch (epoch-end exchange of
+        # epoch e-1 written: pushes of epoch e may land)
         self.ready = self.shared.view("int32", 1, self.flag_off)
+        self.epoch_flag = self.shared.view("int32", 1, self.flag_off + 4)
         self.push = None
         # Hogwild staleness inside a rank: a round's block covers 1/M of every
         # mode's rows, so a full grid would put M times more concurrent
@@ -100,11 +110,17 @@ class FusedState:
 
     # -- peers ---------------------------------------------------------------
     def peer_addresses(self):
-        """(fac address, ready-flag address) of this rank's shared buffer."""
+        """(fac address, flags address) of this rank's shared buffer."""
         return self.shared.ptr, self.shared.ptr + self.flag_off
 
+    def mark_exchanged(self, t: int) -> None:
+        """Epoch t's epoch-end exchange is enqueued on the current stream: once
+        it has executed, peers may push epoch t+1's blocks into this replica."""
+        check(self.runner.L.sptk_flag_store(ptr(self.epoch_flag), int(t) + 1, stream_ptr()), "sptk_flag_store")
+
     def set_peers(self, fac_addrs, ready_addrs) -> None:
-        """Build the per-round push table from every rank's (mapped) addresses."""
+        """Build the per-round push table from every rank's (mapped) addresses
+        (ready_addrs: each rank's flags address; its epoch flag follows)."""
         import torch
 
         plan, dm = self.plan, self.runner.dm
@@ -118,7 +134,7 @@ class FusedState:
                 lo, hi = plan.rows(n, b)
                 J = int(dm.jr[n])
                 tab[r] = (lo, hi - lo, n, int(fac_addrs[dst]) + 4 * (int(dm.foff[n]) + lo * J),
-                          int(ready_addrs[dst]))
+                          int(ready_addrs[dst]), int(ready_addrs[dst]) + 4)
         if int(_lib.load().sptk_dsgd_push_bytes()) != PUSH_DTYPE.itemsize:
             raise RuntimeError("DsgdPush layout mismatch between libsptk and dsgd_fused.py")
         self.push = torch.from_numpy(tab.view(np.uint8).copy()).to(self.runner.dm.fac.device)
@@ -141,7 +157,7 @@ class FusedState:
         check(r.L.sptk_factor_pass_dsgd(ptr(r.part.rec), r.part.rw, ptr(self.fvis[slot]), self.total, ptr(dm.fac),
                                         dm.p_foff, ptr(dm.cor), dm.p_coff, dm.p_jr, r.order, dm.rcore, r.p_gam,
                                         r.p_lam, ptr(self.rstart), ptr(self.rend), ptr(self.push), ptr(self.done),
-                                        ptr(self.ready), R, t * R, int(self.grid), stream_ptr()),
+                                        ptr(self.ready), R, t * R, int(t), int(self.grid), stream_ptr()),
               "sptk_factor_pass_dsgd")
 
 
@@ -164,6 +180,7 @@ class _FusedMixin:
         self.sampled_epoch[slot] = t
 
     def factor_phase(self, t, gamma_a, slot):
+        self._fused_t = t
         if self.factor_events is not None:
             e0 = self.torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -192,6 +209,10 @@ class FusedRankRunner(_FusedMixin, EpochRunner):
 
     def set_peers(self, fac_addrs, ready_addrs):
         self.fused.set_peers(fac_addrs, ready_addrs)
+
+    def mark_exchanged(self, t: int) -> None:
+        """Call after the caller's epoch-end exchange of epoch t (stream order)."""
+        self.fused.mark_exchanged(t)
 
 
 class FusedDistRunner(_FusedMixin, DistRunner):
@@ -223,6 +244,12 @@ class FusedDistRunner(_FusedMixin, DistRunner):
 
     def after_round(self, r):  # no per-round exchange: the kernel forwards blocks itself
         pass
+
+    def after_factor_phase(self):
+        # the epoch-end exchange rewrites this replica; peers' next-epoch
+        # pushes wait for the epoch flag raised behind it (stream order)
+        super().after_factor_phase()
+        self.fused.mark_exchanged(self._fused_t)
 
 
 __all__ = ["FusedState", "FusedRankRunner", "FusedDistRunner", "fused_supported"]

@@ -79,6 +79,8 @@ def test_two_ranks_one_gpu_match_reference_dsgd(dims, J, per_block):
                 for w, dst in enumerate(ranks):
                     if w != q:
                         dst.dm.fac[a:z].copy_(src.dm.fac[a:z])
+        for rk in ranks:
+            rk.mark_exchanged(t)
         torch.cuda.synchronize()
     got = ranks[0].dm.fac.double().cpu().numpy()
     assert np.array_equal(got, ranks[1].dm.fac.double().cpu().numpy())
@@ -92,3 +94,69 @@ def test_two_ranks_one_gpu_match_reference_dsgd(dims, J, per_block):
     np.testing.assert_allclose(got, want, rtol=5e-3, atol=5e-4 * np.abs(want).max())
     for rk in ranks:
         assert rk.L.sptk_last_factor_kernel().decode() == "factor_tma_kernel<dsgd>"
+
+
+def _fused_worker(rank, world, port, out, dims, J, per_block):
+    import os
+
+    import torch.distributed as td
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2204_07104_b200 import ModelConfig, SparseTensorCoo, TrainConfig, init_model
+        from paper_2204_07104_b200.dsgd_fused import FusedDistRunner
+        from paper_2204_07104_b200.training import learning_rate
+
+        idx, vals = _conflict_free(dims, per_block, world, 5)
+        model = init_model(dims, ModelConfig((J,) * len(dims), J, 1.0, seed=1))
+        cfg = TrainConfig(epochs=int(os.environ.get("FUSED_EPOCHS", "2")), workers=world, seed=1, alpha_a=0.003,
+                          update_mode="hogwild", update_core=False)
+        runner = FusedDistRunner(model, SparseTensorCoo(tuple(dims), idx, vals), cfg)
+        for t in range(cfg.epochs):
+            runner.epoch(t, learning_rate(cfg.alpha_a, cfg.beta_a, t), learning_rate(cfg.alpha_b, cfg.beta_b, t))
+        torch.cuda.synchronize()
+        np.save(os.path.join(out, f"fac{rank}.npy"), runner.dm.fac.double().cpu().numpy())
+        td.barrier()
+    finally:
+        td.destroy_process_group()
+
+
+def test_two_processes_ipc_match_reference_dsgd(tmp_path):
+    """Two processes (torch.distributed over gloo for the epoch-end exchange)
+    sharing cuda:0, each mapping the other's model with CUDA IPC: the
+    FusedDistRunner path end to end.  (Without MPS the two persistent kernels
+    time-slice the GPU, so the rounds hand over slowly but must still agree.)"""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dims, J, per_block, W = (3000, 2800, 2600), 16, 700, 2
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_fused_worker, args=(w, W, port, str(tmp_path), dims, J, per_block))
+             for w in range(W)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    alive = [p for p in procs if p.is_alive()]
+    for p in alive:
+        p.kill()
+    assert not alive, "fused DSGD processes did not finish"
+    assert all(p.exitcode == 0 for p in procs)
+    got = [np.load(tmp_path / f"fac{w}.npy") for w in range(W)]
+    assert np.array_equal(got[0], got[1])
+    from paper_2204_07104_b200 import ModelConfig, init_model
+
+    idx, vals = _conflict_free(dims, per_block, W, 5)
+    model = init_model(dims, ModelConfig((J,) * len(dims), J, 1.0, seed=1))
+    fs = [a.copy() for a in model.factors]
+    bs = [b.copy() for b in model.core_factors]
+    O.train(fs, bs, idx, vals, epochs=2, workers=W, seed=1, alpha_a=0.003, update_core=False, evaluate=False,
+            dims=tuple(dims))
+    want, _ = O.pack(fs)
+    np.testing.assert_allclose(got[0], want, rtol=5e-3, atol=5e-4 * np.abs(want).max())
