@@ -71,6 +71,9 @@ int sptk_get_tc_mode(void);
  * (e.g. "factor_tma_kernel"); "none" before the first call.  Lets the caller
  * label measurements with the kernel that actually ran. */
 const char* sptk_last_factor_kernel(void);
+/* 1 if the throughput factor pass at uniform J = R = j runs on the CUDA-core
+ * FMA kernel rather than tcgen05 (measured crossover; SPTK_FMA_RANKS). */
+int sptk_fma_rank(int j);
 /* test hook: per-sample dump of the first tcgen05 tile (c, gs, refreshed c). */
 void sptk_debug_tc_buffer(float* d_buf);
 
@@ -88,7 +91,7 @@ int sptk_pcg64_seed(const uint64_t* h_entropy, int n_entropy, uint64_t h_state_o
  * {int64 off, int64 out_base, int32 n, int32 first, int32 m, int32 slot, int32 nmin
  * (the round's smallest block), int32 pad},
  * round-major (first = index of the round's first job, m <= 64 jobs per round);
- * d_coords: n_jobs x order block coordinates; cap >= max n_b, <= 18000 (12 bytes
+ * d_coords: n_jobs x order block coordinates; cap >= max n_b, <= 28000 (8 bytes
  * of shared memory per nonzero); d_js: uint16 scratch for the j-sequences, one
  * entry per record of the jobs (indexed like the records: off_b + p).
  * Replaces the per-block permutation + `visit = ids[perm]` of the round loop. */

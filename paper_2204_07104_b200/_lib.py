@@ -33,6 +33,7 @@ SIGNATURES = {
     "sptk_get_tc_mode": (ctypes.c_int, []),
     "sptk_last_factor_kernel": (ctypes.c_char_p, []),
     "sptk_debug_tc_buffer": (None, [_vp]),
+    "sptk_fma_rank": (ctypes.c_int, [ctypes.c_int]),
     "sptk_pcg64_seed": (ctypes.c_int, [_u64p, ctypes.c_int, _u64p]),
     "sptk_block_job_bytes": (ctypes.c_size_t, []),
     "sptk_block_perm": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _i64, ctypes.c_int,

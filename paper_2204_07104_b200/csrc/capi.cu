@@ -201,6 +201,8 @@ int sptk_factor_pass_f64(const int32_t* d_rec, int rw, const int32_t* d_visit, l
                              (cudaStream_t)stream);
 }
 
+int sptk_fma_rank(int j) { return fma_rank_policy(j); }
+
 size_t sptk_factor_pass_exact_ws_bytes(long long n_visit, int n_modes) {
   return factor_dep_ws_bytes(n_visit, n_modes);
 }

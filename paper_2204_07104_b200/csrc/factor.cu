@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(128, (J <= 4 ? 6 : (N * J <= 24 ? 5 : (J <= 8 
 #define SPTK_NO_HOIST() asm volatile("" ::: "memory")
 
 template <int N, int J, bool HV>
-__global__ void __launch_bounds__(128, (J <= 8 ? 4 : 3))
+__global__ void __launch_bounds__(128, (J <= 4 ? 8 : (J <= 8 ? 4 : 3)))
     factor_fma_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
                       float* __restrict__ fac, const float* __restrict__ cor, TpsParams<N> p, unsigned hot) {
   constexpr int R = J, RW = N <= 3 ? 4 : 8;
@@ -538,7 +538,7 @@ static int launch_fma(const int* rec, const int* visit, long long n_visit, long 
     if ((end - md.foff[n]) / J < (1LL << 18)) hot |= 1u << n;
   }
   if (const char* e = getenv("SPTK_ATOMIC_MASK")) hot = (unsigned)strtoul(e, nullptr, 0);
-  int per_sm = 3;
+  int per_sm = J <= 4 ? 8 : (J <= 8 ? 4 : 3);
   if (const char* e = getenv("SPTK_TC_CTAS")) per_sm = atoi(e);
   long long blocks = 148LL * per_sm;
   const long long need = (n_visit + 127) / 128;
@@ -568,8 +568,33 @@ static int try_fma(const int* rec, int rw, const int* visit, long long n_visit, 
     *rc = launch_fma<3, 8>(rec, visit, n_visit, base, fac, cor, md, gam, lam, s);
     return 1;
   }
+  if (N == 3 && J == 4) {
+    *rc = launch_fma<3, 4>(rec, visit, n_visit, base, fac, cor, md, gam, lam, s);
+    return 1;
+  }
   return 0;
 }
+
+// Ranks whose throughput factor pass runs on the CUDA-core FMA kernel
+// instead of tcgen05 (bit r: J = R = r), from the measured crossover
+// (DESIGN.md section 4); SPTK_FMA_RANKS="4,8" style overrides.
+static bool fma_rank(int J) {
+  static int mask = -1;
+  if (mask < 0) {
+    mask = 0;
+    if (const char* e = getenv("SPTK_FMA_RANKS")) {
+      const char* q = e;
+      while (*q) {
+        const int v = atoi(q);
+        if (v > 0 && v < 31) mask |= 1 << v;
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    }
+  }
+  return J > 0 && J < 31 && (mask >> J & 1);
+}
+int fma_rank_policy(int J) { return (get_tc_mode() == 5 || fma_rank(J)) ? 1 : 0; }
 
 // returns 1 if handled (status in *rc), 0 if no specialisation
 static int try_tps(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
@@ -630,8 +655,9 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
   }
   if (!f64) {
     int rc = 0;
-    if (get_tc_mode() == 5 && try_fma(rec, rw, visit, n_visit, base, (float*)fac, (const float*)cor, md,
-                                      (const float*)h_gammas, (const float*)h_lambdas, s, &rc))
+    if ((get_tc_mode() == 5 || fma_rank(md.jr[0])) &&
+        try_fma(rec, rw, visit, n_visit, base, (float*)fac, (const float*)cor, md, (const float*)h_gammas,
+                (const float*)h_lambdas, s, &rc))
       return rc;
     if (try_factor_tc(rec, rw, visit, n_visit, base, (float*)fac, (const float*)cor, md, (const float*)h_gammas,
                       (const float*)h_lambdas, s, &rc))

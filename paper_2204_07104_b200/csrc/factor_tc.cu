@@ -665,8 +665,11 @@ struct Tc3Cfg {
   static constexpr int OFF_G = OFF_BN + N * J * R;
   static constexpr int OFF_A = OFF_G + N * R * R;        // N slots of 128 x J
   static constexpr int OFF_W = OFF_A + N * M * J;        // 128 x R
-  static constexpr int OFF_X = OFF_W + M * R;            // 2 x 128 partial predictions
-  static constexpr int OFF_BAR = OFF_X + 2 * M;          // mbarrier (2 words), TMEM slot, claim slot
+  // 2 x 128 partial predictions, double-buffered by mode parity: a thread's
+  // partner reads mode n's value after the barrier while this thread may
+  // already write mode n+1's (compute-sanitizer racecheck)
+  static constexpr int OFF_X = OFF_W + M * R;
+  static constexpr int OFF_BAR = OFF_X + 4 * M;          // mbarrier (2 words), TMEM slot, claim slot
   // the last mode's second slot, only allocated when that mode is gathered a
   // tile ahead (a cold mode); a hot last mode (NF) leaves it out, which lets
   // two J = 32 CTAs share an SM
@@ -815,7 +818,7 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 2))
         }
         *reinterpret_cast<float4*>(wt + canon<128>(s, c0 + 4 * q)) = make_float4(w4[0], w4[1], w4[2], w4[3]);
       }
-      px[hf * 128 + s] = part;
+      px[(n & 1) * 256 + hf * 128 + s] = part;
       tc::fence_async_smem();
       tc::fence_before_sync();
       __syncthreads();
@@ -827,7 +830,7 @@ __global__ void __launch_bounds__(256, (J <= 16 ? 3 : 2))
         tc::mma_commit(&mbar);
       }
       if (n >= 1 && n - 1 < N - 1 && (pfm >> (n - 1) & 1u)) issue_mode(nxt, n - 1, 0);
-      const float inter = part + px[(hf ^ 1) * 128 + s];
+      const float inter = part + px[(n & 1) * 256 + (hf ^ 1) * 128 + s];
       tc::mbar_wait(&mbar, phase);
       phase ^= 1;
       tc::fence_after_sync();
@@ -1057,8 +1060,8 @@ struct Tc4Cfg {
   static constexpr int OFF_BN = OFF_BT + N * R * J;  // N x (J rows x R)
   static constexpr int OFF_A = OFF_BN + N * J * R;   // N slots of 128 x J
   static constexpr int OFF_W = OFF_A + (N - 1) * M * J;  // 128 x R: the last mode's A slot (see below)
-  static constexpr int OFF_X = OFF_A + N * M * J;    // 4 x 128 partial predictions
-  static constexpr int FLOATS = OFF_X + 4 * M;
+  static constexpr int OFF_X = OFF_A + N * M * J;    // 4 x 128 partial predictions, x2 by mode parity
+  static constexpr int FLOATS = OFF_X + 8 * M;
   static constexpr int NEED = N * R + J;             // c_0..c_{N-1}, gs
   static constexpr int TCOLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr size_t SMEM = (size_t)FLOATS * 4 + 16;
@@ -1199,7 +1202,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         *reinterpret_cast<float4*>(wt + canon<128>(s, c0 + 4 * q)) = make_float4(w4[0], w4[1], w4[2], w4[3]);
       }
-      px[qq * 128 + s] = part;
+      px[(n & 1) * 512 + qq * 128 + s] = part;
       tc::fence_async_smem();
       tc::fence_before_sync();
       __syncthreads();
@@ -1208,7 +1211,8 @@ __global__ void __launch_bounds__(512, 1)
         issue_gemm<J, R, false>(tbase + tgs, sbase + 4 * C::OFF_W, 0, sbase + 4 * (C::OFF_BN + n * J * R), 0, id_g);
         tc::mma_commit(&mbar);
       }
-      const float inter = ((px[s] + px[128 + s]) + px[256 + s]) + px[384 + s];
+      const float* pp = px + (n & 1) * 512;
+      const float inter = ((pp[s] + pp[128 + s]) + pp[256 + s]) + pp[384 + s];
       float* at = sm + a_off(n);
       float a[Q];
       if (n == N - 1) {

@@ -52,6 +52,8 @@ int factor_pass(const int* rec, int rw, const int* visit, long long n_visit, lon
                 const T* cor, const ModelDesc& md, const T* h_gammas, const T* h_lambdas, int mode,
                 cudaStream_t s);
 
+int fma_rank_policy(int J);
+
 // factor_dep.cu (exact mode across the GPU: predecessor-driven schedule)
 size_t factor_dep_ws_bytes(long long nv, int n_modes);
 template <typename T>

@@ -2001,110 +2001,121 @@ __global__ void __launch_bounds__(32 * BP_JW) block_jgen_kernel(const BlockJob* 
 }
 
 #define BP_T 256
-// Shared memory per nonzero: J (target, later the result), L (steps grouped by
-// target), S (each group sorted by step, descending), V (chain roots): 16-bit;
-// C (group ends): 32-bit -- 12 bytes.
+// Shared memory per nonzero: 8 bytes -- C (group counts, then group starts /
+// ends: 16-bit halves of 32-bit words, so the counting and scatter atomics
+// stay 32-bit), J (target of each step), S (each target's group sorted by
+// step, descending), and one array that holds L (steps grouped by target)
+// until S is built and V (chain roots) after.  16-bit entries: n <= 28000.
+#define BP_CAP 28000
+__device__ __forceinline__ unsigned c16_get(const unsigned* C, int t) { return (C[t >> 1] >> ((t & 1) * 16)) & 0xFFFFu; }
+__device__ __forceinline__ unsigned c16_inc(unsigned* C, int t) {
+  const unsigned sh = (t & 1) * 16;
+  return (atomicAdd(&C[t >> 1], 1u << sh) >> sh) & 0xFFFFu;
+}
 __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restrict__ jobs,
                                                         const uint16_t* __restrict__ js,
                                                         int* __restrict__ visit, int cap) {
   extern __shared__ __align__(16) unsigned char bp_sm[];
-  unsigned* C = reinterpret_cast<unsigned*>(bp_sm);  // [cap] counts -> group ends
-  uint16_t* J = reinterpret_cast<uint16_t*>(C + cap);
-  uint16_t* L = J + cap;
-  uint16_t* S = L + cap;
-  uint16_t* V = S + cap;
+  unsigned* C = reinterpret_cast<unsigned*>(bp_sm);  // [cap/2 + 1] packed 16-bit
+  uint16_t* J = reinterpret_cast<uint16_t*>(C + (cap / 2 + 1));
+  uint16_t* S = J + cap;
+  uint16_t* LV = S + cap;  // L, then V
   __shared__ int sh[33];
   __shared__ int sizes[64];
   const BlockJob jb = jobs[blockIdx.x];
   const int n = jb.n, tid = threadIdx.x;
   if (tid < jb.m && tid < 64) sizes[tid] = jobs[jb.first + tid].n;
-  for (int p = tid; p < n; p += BP_T) {
-    C[p] = 0u;
-    J[p] = js[jb.off + p];
-    V[p] = (uint16_t)p;  // no step above p targets p: p keeps its own value
-  }
+  for (int p = tid; p < (n + 1) / 2; p += BP_T) C[p] = 0u;
+  for (int p = tid; p < n; p += BP_T) J[p] = js[jb.off + p];
   __syncthreads();
-  for (int i = tid; i < n; i += BP_T) atomicAdd(&C[J[i]], 1u);
+  for (int i = tid; i < n; i += BP_T) c16_inc(C, J[i]);
   __syncthreads();
   {
-    const int per = (n + BP_T - 1) / BP_T, a = tid * per, z = min(n, a + per);
+    // exclusive scan of the 16-bit counts, each thread a run of whole words
+    const int words = (n + 1) / 2;
+    const int per = (words + BP_T - 1) / BP_T, a = tid * per, z = min(words, a + per);
     int run = 0;
-    for (int p = a; p < z; ++p) run += (int)C[p];
+    for (int w = a; w < z; ++w) run += (int)(C[w] & 0xFFFFu) + (int)(C[w] >> 16);
     int tot;
     int ex = block_excl_scan(run, sh, &tot);
-    for (int p = a; p < z; ++p) {
-      const int c = (int)C[p];
-      C[p] = (unsigned)ex;
-      ex += c;
+    for (int w = a; w < z; ++w) {
+      const unsigned c0 = C[w] & 0xFFFFu, c1 = C[w] >> 16;
+      C[w] = (unsigned)ex | ((unsigned)(ex + (int)c0) << 16);
+      ex += (int)(c0 + c1);
     }
   }
   __syncthreads();
-  for (int i = tid; i < n; i += BP_T) L[atomicAdd(&C[J[i]], 1u)] = (uint16_t)i;
+  // steps grouped by target (group starts -> group ends)
+  for (int i = tid; i < n; i += BP_T) LV[c16_inc(C, J[i])] = (uint16_t)i;
   __syncthreads();
   // each step's place in its target's group, largest step first (the order
   // Fisher-Yates runs them): rank = number of larger steps in the group
   for (int i = tid; i < n; i += BP_T) {
-    const int t = J[i], s0 = t ? (int)C[t - 1] : 0, s1 = (int)C[t];
+    const int t = J[i], s0 = t ? (int)c16_get(C, t - 1) : 0, s1 = (int)c16_get(C, t);
     int rank = 0;
-    for (int x = s0; x < s1; ++x) rank += (int)L[x] > i;
+    for (int x = s0; x < s1; ++x) rank += (int)LV[x] > i;
     S[s0 + rank] = (uint16_t)i;
   }
+  __syncthreads();
+  // L is dead: V(p) = p (no step above p targets p: p keeps its own value)
+  for (int p = tid; p < n; p += BP_T) LV[p] = (uint16_t)p;
   __syncthreads();
   // every step targeting t is >= t: the smallest step above t (t's parent)
   // is the last of the group, or the second to last after t's own step
   for (int t = tid; t < n; t += BP_T) {
-    const int s0 = t ? (int)C[t - 1] : 0, s1 = (int)C[t];
+    const int s0 = t ? (int)c16_get(C, t - 1) : 0, s1 = (int)c16_get(C, t);
     if (s1 > s0) {
       const int last = S[s1 - 1];
-      if (last > t) V[t] = (uint16_t)last;
-      else if (s1 - s0 >= 2) V[t] = S[s1 - 2];
+      if (last > t) LV[t] = (uint16_t)last;
+      else if (s1 - s0 >= 2) LV[t] = S[s1 - 2];
     }
   }
   __syncthreads();
-  // V(p) = root of p's chain
+  // V(p) = root of p's chain (pointer jumping in place.  racecheck reports
+  // the read of LV[v] against other threads' writes: benign -- every value
+  // LV[q] ever holds is an ancestor of q on q's chain, so a stale or a fresh
+  // read both move p toward the same root, the unique fixed point)
   for (;;) {
     int changed = 0;
     for (int p = tid; p < n; p += BP_T) {
-      const uint16_t v = V[p], w = V[v];
+      const uint16_t v = LV[p], w = LV[v];
       if (w != v) {
-        V[p] = w;
+        LV[p] = w;
         changed = 1;
       }
     }
     if (!__syncthreads_or(changed)) break;
   }
-  // result[i]: the value its target held just before step i (L is free now)
-  for (int x = tid; x < n; x += BP_T) {
-    const int i = S[x], t = J[i], s0 = t ? (int)C[t - 1] : 0;
-    L[i] = x == s0 ? (uint16_t)t : V[S[x - 1]];
-  }
-  __syncthreads();
-  // round-interleaved output: slot(p) = sum_s min(n_s, p) + #{s < slot : n_s > p}
+  // result[i]: the value its target held just before step i, written straight
+  // to its round-interleaved slot:
+  //   slot(p) = sum_s min(n_s, p) + #{s < slot : n_s > p}
   const int m = min(jb.m, 64);
-  for (int p = tid; p < n; p += BP_T) {
+  for (int x = tid; x < n; x += BP_T) {
+    const int i = S[x], t = J[i], s0 = t ? (int)c16_get(C, t - 1) : 0;
+    const int val = x == s0 ? t : (int)LV[S[x - 1]];
     long long pos = jb.out_base;
-    if (p < jb.nmin) {
-      pos += (long long)p * m + jb.slot;  // every block of the round still has entries
+    if (i < jb.nmin) {
+      pos += (long long)i * m + jb.slot;  // every block of the round still has entries
     } else {
-      for (int s = 0; s < m; ++s) {
-        const int ns = sizes[s];
-        pos += ns < p ? ns : p;
-        if (s < jb.slot && ns > p) ++pos;
+      for (int s2 = 0; s2 < m; ++s2) {
+        const int ns = sizes[s2];
+        pos += ns < i ? ns : i;
+        if (s2 < jb.slot && ns > i) ++pos;
       }
     }
-    visit[pos] = (int)(jb.off + L[p]);
+    visit[pos] = (int)(jb.off + val);
   }
 }
 
 int block_perm(const void* d_jobs, const int* d_coords, int n_jobs, int order, unsigned long long seed,
                long long t, int cap, uint16_t* d_js, int* d_visit, cudaStream_t s) {
   SPTK_REQUIRE(n_jobs >= 0 && order >= 1 && order <= SPTK_MAX_MODES, "block_perm: bad arguments");
-  SPTK_REQUIRE(cap >= 1 && cap <= 18000, "block_perm: block capacity must be in [1, 18000]");
+  SPTK_REQUIRE(cap >= 1 && cap <= BP_CAP, "block_perm: block capacity must be in [1, %d]", BP_CAP);
   if (n_jobs == 0) return 0;
   const BlockJob* jobs = (const BlockJob*)d_jobs;
   block_jgen_kernel<<<(n_jobs + BP_JW - 1) / BP_JW, 32 * BP_JW, 0, s>>>(jobs, n_jobs, d_coords, order, seed, t, d_js);
   SPTK_CHECK_LAUNCH();
-  const size_t smem = (size_t)cap * 12 + 16;
+  const size_t smem = (size_t)(cap / 2 + 1) * 4 + (size_t)cap * 6 + 16;
   static size_t configured = 0;
   if (smem > configured) {
     SPTK_CUDA_TRY(cudaFuncSetAttribute(block_fy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

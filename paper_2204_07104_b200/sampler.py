@@ -148,7 +148,7 @@ def u32_stream(entropy, n: int, q0: int = 0):
 
 BLOCK_JOB_DTYPE = np.dtype([("off", "<i8"), ("out_base", "<i8"), ("n", "<i4"), ("first", "<i4"), ("m", "<i4"),
                             ("slot", "<i4"), ("nmin", "<i4"), ("pad", "<i4")])
-BLOCK_PERM_MAX = 18000  # 12 bytes of shared memory per nonzero in one CTA
+BLOCK_PERM_MAX = 28000  # 8 bytes of shared memory per nonzero in one CTA (16-bit entries)
 
 
 class BlockOrders:

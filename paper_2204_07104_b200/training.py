@@ -218,10 +218,12 @@ class EpochRunner:
         self.owner_rank = owner_rank
         self.order = model.order
         self.nnz = train_set.nnz
-        # J = R = 4 in throughput mode: run on a zero-padded rank-8 model (the
-        # smallest tcgen05 tile; exactly equivalent, see DeviceModel)
-        pad = 8 if (not self.f64 and self.mode == 0 and model.r_core == 4
-                    and all(int(j) == 4 for j in model.j_ranks)) else None
+        # J = R = 4 in throughput mode on tcgen05: a zero-padded rank-8 model
+        # (the smallest TF32 tile; exactly equivalent, see DeviceModel) -- only
+        # where a rank-8 tcgen05 kernel exists (orders 3 and 6) and the
+        # measured crossover does not put rank 4 on the FMA kernel
+        pad = 8 if (not self.f64 and self.mode == 0 and model.r_core == 4 and model.order in (3, 6)
+                    and all(int(j) == 4 for j in model.j_ranks) and not _lib.load().sptk_fma_rank(4)) else None
         self.dm = DeviceModel(model, f64=self.f64, pad_rank=pad)
         self.part = DevicePartition(train_set.indices, train_set.values, model.dims, self.m, f64=self.f64,
                                     want_ids=False)

@@ -246,15 +246,59 @@ def test_block_perm_matches_reference(order, sizes_seed):
     np.testing.assert_array_equal(got, _interleave_reference(rounds, perms))
 
 
-def test_block_perm_max_block():
-    """The largest block one CTA takes (18,000 nonzeros: 12 bytes of shared memory each), bit-exact."""
+@pytest.mark.parametrize("big", [18000, 24811, 28000])
+def test_block_perm_max_block(big):
+    """The largest blocks one CTA takes (up to 28,000 nonzeros: 8 bytes of
+    shared memory each; NF at W = 16 has ~24.2K per block), bit-exact."""
     import torch
 
     from paper_2204_07104_b200.sampler import BlockOrders
 
-    rounds = [[((3, 1, 4), 0, 18000), ((2, 7, 1), 18000, 1)]]
+    rounds = [[((3, 1, 4), 0, big), ((2, 7, 1), big, 1)]]
     bo = BlockOrders(rounds, 3, "cuda")
     out = torch.empty(bo.total, dtype=torch.int32, device="cuda")
     bo.draw(7, 0, out)
-    perms = [[O.permutation([7, 1, 0, 3, 1, 4], 18000), O.permutation([7, 1, 0, 2, 7, 1], 1)]]
+    perms = [[O.permutation([7, 1, 0, 3, 1, 4], big), O.permutation([7, 1, 0, 2, 7, 1], 1)]]
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.int64), _interleave_reference(rounds, perms))
+
+
+@pytest.mark.parametrize("pad", [1, 128])
+def test_block_orders_padding_and_interleave(pad):
+    """Padded rounds (the fused DSGD layout: every round on a multiple of 128,
+    empty rounds one padding unit, gaps untouched) and sptk_interleave_rounds
+    (the same layout from per-block orders in the partitioned layout) agree
+    with the host restatement."""
+    import torch
+
+    from paper_2204_07104_b200.sampler import BlockOrders
+
+    rng = np.random.default_rng(4)
+    rounds, off = [], 0
+    for r in range(6):
+        rnd = []
+        for s in range(int(rng.integers(0, 4))):
+            n = int(rng.choice([1, 5, 300, 2000]))
+            rnd.append((tuple(int(x) for x in rng.integers(0, 9, 3)), off, n))
+            off += n
+        rounds.append(rnd)
+    bo = BlockOrders(rounds, 3, "cuda", pad=pad)
+    out = torch.full((max(bo.total, 1),), -1, dtype=torch.int32, device="cuda")
+    bo.draw(99, 1, out)
+    perms = [[O.permutation([99, 1, 1, *block], n) for block, _, n in rnd] for rnd in rounds]
+    want = np.full(bo.total, -1, dtype=np.int64)
+    for r, (rnd, prs) in enumerate(zip(rounds, perms)):
+        seg = _interleave_reference([rnd], [prs])
+        assert bo.round_end[r] - bo.round_start[r] == len(seg)
+        want[bo.round_start[r]: bo.round_start[r] + len(seg)] = seg
+        if pad > 1:
+            assert bo.round_start[r] % pad == 0 and bo.round_start[r + 1] > bo.round_start[r]
+    np.testing.assert_array_equal(out[:bo.total].cpu().numpy().astype(np.int64), want)
+    # the interleave kernel from per-block orders (entries relative to off_b)
+    flat = np.zeros(off, dtype=np.int32)
+    for rnd, prs in zip(rounds, perms):
+        for (block, o, n), pr in zip(rnd, prs):
+            flat[o: o + n] = pr
+    big = BlockOrders(rounds, 3, "cuda", big=True, pad=pad)
+    out2 = torch.full((max(big.total, 1),), -1, dtype=torch.int32, device="cuda")
+    big.interleave(torch.from_numpy(flat).cuda(), -1, out2)
+    np.testing.assert_array_equal(out2[:big.total].cpu().numpy().astype(np.int64), want)
