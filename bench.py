@@ -39,8 +39,13 @@ sys.path.insert(0, ROOT)
 METRIC = "sampled nonzeros/sec per SGD epoch (A+B update) at 1/2/4/8 B200; test RMSE"
 
 CONFIGS = {
+    # workers: the reference's TrainConfig.workers (DSGD blocks per mode).
+    # NF runs its DSGD schedule with 24 blocks per mode on the one GPU: the
+    # fastest of the measured 1/16/24/32/48/64 (14.8/11.9/10.5/10.9/12.5/14.8
+    # ms per epoch; profiles/r02), same test RMSE (0.4784 vs 0.4786 at W=1)
     "nf": dict(workload="netflix-shaped 480189x17770x2182, 99,072,112 nnz, J=R=16",
-               dims=(480189, 17770, 2182), nnz=99_072_112, n_test=1_408_395, J=16, R=16, alpha_a=0.003),
+               dims=(480189, 17770, 2182), nnz=99_072_112, n_test=1_408_395, J=16, R=16, alpha_a=0.003,
+               workers=24),
     "cfg1": dict(workload="synthetic 1Kx1Kx1K, 90K train / 10K test, J=R=8",
                  dims=(1000, 1000, 1000), nnz=90_000, n_test=10_000, J=8, R=8),
     # alpha_a: the reference's default 0.009 diverges on these std-4 synthetic
@@ -60,14 +65,14 @@ def bytes_per_nnz(order, J):
     return 4 * (order + 1) + 8 * order * J
 
 
-def factor_traffic(workload):
+def factor_traffic(workload, workers=1):
     """dram__bytes_read.sum + dram__bytes_write.sum per factor-kernel launch from
     the committed ncu --set full capture of this workload (profiles/), or None."""
     p = os.path.join(ROOT, "profiles", "factor_traffic.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d["bytes_per_launch"] if d.get("workload") == workload else None
+        return d["bytes_per_launch"] if d.get("workload") == workload and d.get("workers", 1) == workers else None
     except Exception:
         return None
 
@@ -238,7 +243,7 @@ def bench_ours(args, cfg):
     scale = default_init_scale(tr.values, order)
     model = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
     # +3: every timed epoch also draws the next epoch's samples (steady state)
-    workers = args.workers if args.workers else (world if world > 1 else 1)
+    workers = args.workers if args.workers else (world if world > 1 else cfg.get("workers", 1))
     tcfg = TrainConfig(epochs=args.warmup + args.steps + 3, seed=1, update_mode=args.mode,
                        workers=workers, alpha_a=cfg.get("alpha_a", 0.009))
     sim = int(os.environ.get("BENCH_DSGD_SIM", "0"))
@@ -356,8 +361,8 @@ def bench_ours(args, cfg):
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         threads = len(os.sched_getaffinity(0))
         sample = cpu_sample_size(cfg)
-        rates, workers, desc = run_cpu_reference(cfg, sample, 1, threads)
-        cpu = {"value": rates[-1], "unit": "nnz/s", "cores": workers, "kind": "port", "sample": desc}
+        rates, cpu_workers, desc = run_cpu_reference(cfg, sample, 1, threads)
+        cpu = {"value": rates[-1], "unit": "nnz/s", "cores": cpu_workers, "kind": "port", "sample": desc}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
@@ -375,7 +380,7 @@ def bench_ours(args, cfg):
                              "model is L2-resident by design"},
             "test_rmse": test_rmse,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": factor_traffic(cfg["workload"]),
+                         "frac": achieved / peak, "traffic": factor_traffic(cfg["workload"], workers),
                          "kernel": kernel,
                          "kernel_ms": f_ms, "kernel_share": f_ms * launches_per_epoch / ms_per_step,
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,

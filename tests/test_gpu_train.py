@@ -100,7 +100,8 @@ def test_cfg1_hogwild_rmse(golden, golden_meta):
     assert gap < 0.01
 
 
-def test_netflix_shaped_hogwild_rmse_curve_within_1pct():
+@pytest.mark.parametrize("workers", [1, 24])
+def test_netflix_shaped_hogwild_rmse_curve_within_1pct(workers):
     """North-star accuracy bar on the bench workload (BASELINE configs[1]): the
     throughput (Hogwild, fp32, tcgen05) path's test RMSE after each of 5
     epochs is within 1% of the reference's (tests/golden/nf99_curve.json, the
@@ -126,9 +127,9 @@ def test_netflix_shaped_hogwild_rmse_curve_within_1pct():
     tr, te, _ = generate_large(dims, ref["nnz"], (16, 16, 16), 16, 0.1, seed=7, n_test=ref["n_test"], predict=pred)
     m = init_model(dims, ModelConfig((16, 16, 16), 16, default_init_scale(tr.values, 3), seed=1))
     rows = train(m, DatasetSplit(tr, te), TrainConfig(epochs=ref["epochs"], seed=1, alpha_a=ref["alpha_a"],
-                                                      update_mode="hogwild"))
+                                                      update_mode="hogwild", workers=workers))
     got = [r.test_rmse for r in rows]
     want = [r["test_rmse"] for r in ref["rows"]]
-    print("NF test RMSE", got, "reference", want)
+    print("NF workers", workers, "test RMSE", got, "reference", want)
     for g, w in zip(got, want):
         assert abs(g - w) <= 0.01 * w
