@@ -647,18 +647,22 @@ __global__ void __launch_bounds__(128) core_exact_terms_kernel(const int* __rest
                                                                const T* __restrict__ fac, const T* __restrict__ cor,
                                                                ModelDesc md, T* __restrict__ tv, T* __restrict__ ta,
                                                                T* __restrict__ tc) {
+  // term tables column-major (column stride EXACT_SEG): a thread's writes of
+  // one column are coalesced with its neighbours', and the ordered sums read
+  // each output's column as one contiguous stream
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cnt) return;
-  const int N = md.n_modes, R = md.rcore, NR = N * R;
+  const int N = md.n_modes, R = md.rcore;
+  constexpr long long S = EXACT_SEG;
   int aoff[SPTK_MAX_MODES];
   int tot = 0;
   for (int n = 0; n < N; ++n) {
     aoff[n] = tot;
     tot += md.jr[n];
   }
-  T* my_a = ta + (size_t)i * tot;
-  T* my_v = tv + (size_t)i * NR;
-  T* my_c = tc + (size_t)i * NR;
+  T* my_a = ta + i;
+  T* my_v = tv + i;
+  T* my_c = tc + i;
   const long long k = k0 + i;
   const long long sid = visit ? (long long)__ldg(visit + k) : k;
   const long long ri = map ? (long long)__ldg(map + sid) : sid;
@@ -667,20 +671,21 @@ __global__ void __launch_bounds__(128) core_exact_terms_kernel(const int* __rest
   for (int n = 0; n < N; ++n) {
     const int J = md.jr[n];
     const T* row = fac + md.foff[n] + (long long)__ldg(rp + n) * J;
-    for (int j = 0; j < J; ++j) my_a[aoff[n] + j] = row[j];
+    for (int j = 0; j < J; ++j) my_a[(aoff[n] + j) * S] = row[j];
   }
   for (int n0 = 0; n0 < N; ++n0) {
     const int J = md.jr[n0];
     for (int r = 0; r < R; ++r) {
       T dot = 0;
-      for (int j = 0; j < J; ++j) dot = cadd(dot, cmul(my_a[aoff[n0] + j], __ldg(cor + md.coff[n0] + j * R + r)));
-      my_c[n0 * R + r] = dot;
+      for (int j = 0; j < J; ++j)
+        dot = cadd(dot, cmul(my_a[(aoff[n0] + j) * S], __ldg(cor + md.coff[n0] + j * R + r)));
+      my_c[(n0 * R + r) * S] = dot;
     }
   }
   T xhat = 0;
   for (int r = 0; r < R; ++r) {
     T pr = 1;
-    for (int n0 = 0; n0 < N; ++n0) pr = cmul(pr, my_c[n0 * R + r]);
+    for (int n0 = 0; n0 < N; ++n0) pr = cmul(pr, my_c[(n0 * R + r) * S]);
     xhat = cadd(xhat, pr);
   }
   const T resid = cadd(xhat, -x);
@@ -688,57 +693,48 @@ __global__ void __launch_bounds__(128) core_exact_terms_kernel(const int* __rest
     for (int r = 0; r < R; ++r) {
       T w = 1;
       for (int n0 = 0; n0 < N; ++n0)
-        if (n0 != n) w = cmul(w, my_c[n0 * R + r]);
-      my_v[n * R + r] = cmul(resid, w);
+        if (n0 != n) w = cmul(w, my_c[(n0 * R + r) * S]);
+      my_v[(n * R + r) * S] = cmul(resid, w);
     }
 }
 
-// CTA (128 outputs of chunk blockIdx.y): partial[c][o] += the segment's
-// terms of chunk c in sample order.  The term rows are staged through shared
-// memory KT samples at a time (coalesced), so the per-output sums run at
-// shared-memory latency instead of one dependent L2 round trip per term.
+// One warp per (chunk blockIdx.y, output o): partial[c][o] += the segment's
+// terms of chunk c in sample order.  The lanes load 32 consecutive samples'
+// factors of the output's two columns (coalesced) and form the 32 products in
+// parallel; the ordered sum then takes them one by one (shuffles issued ahead
+// of the dependent additions).
 template <typename T>
 __global__ void __launch_bounds__(128) core_exact_sum_kernel(const T* __restrict__ tv, const T* __restrict__ ta,
                                                              long long k0, int cnt, const long long* __restrict__ lo,
-                                                             int KT, ModelDesc md, double* __restrict__ partial) {
-  extern __shared__ __align__(16) unsigned char ex_sm[];
-  const int CS = md.cor_size, c = blockIdx.y;
+                                                             ModelDesc md, double* __restrict__ partial) {
+  const int CS = md.cor_size, c = blockIdx.y, lane = threadIdx.x & 31;
+  const int o = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (o >= CS) return;
   long long a = lo[c], z = lo[c + 1];
   a = a > k0 ? a : k0;
   z = z < k0 + cnt ? z : k0 + cnt;
   if (a >= z) return;
-  const int N = md.n_modes, R = md.rcore, NR = N * R;
-  int tot = 0;
-  for (int q = 0; q < N; ++q) tot += md.jr[q];
-  T* sv = reinterpret_cast<T*>(ex_sm);
-  T* sa = sv + (size_t)KT * NR;
-  const int o = blockIdx.x * 128 + threadIdx.x;
-  const bool mine = o < CS;
+  const int N = md.n_modes, R = md.rcore;
   int n = 0, aoffn = 0;
-  if (mine) {
-    while (n + 1 < N && o >= md.coff[n + 1]) ++n;
-    for (int q = 0; q < n; ++q) aoffn += md.jr[q];
+  while (n + 1 < N && o >= md.coff[n + 1]) ++n;
+  for (int q = 0; q < n; ++q) aoffn += md.jr[q];
+  const int rel = o - md.coff[n], j = rel / R, r = rel - (rel / R) * R;
+  const T* pv = tv + (size_t)(n * R + r) * EXACT_SEG;
+  const T* pa = ta + (size_t)(aoffn + j) * EXACT_SEG;
+  double acc = partial[(size_t)c * CS + o];
+  for (long long kb = a; kb < z; kb += 32) {
+    const long long kk = kb + lane;
+    const bool ok = kk < z;
+    const double prod = ok ? cmul<double>((double)pv[kk - k0], (double)pa[kk - k0]) : 0.0;
+    const int nk = (int)(z - kb < 32 ? z - kb : 32);
+    double ps[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) ps[u] = __shfl_sync(0xffffffffu, prod, u);
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+      if (u < nk) acc = cadd<double>(acc, ps[u]);
   }
-  const int rel = mine ? o - md.coff[n] : 0, j = rel / R, r = rel - (rel / R) * R;
-  double acc = mine ? partial[(size_t)c * CS + o] : 0.0;
-  for (long long kb = a; kb < z; kb += KT) {
-    const int nk = (int)(z - kb < KT ? z - kb : KT);
-    const T* gv = tv + (size_t)(kb - k0) * NR;
-    const T* ga = ta + (size_t)(kb - k0) * tot;
-    for (int i = threadIdx.x; i < nk * NR; i += 128) sv[i] = gv[i];
-    for (int i = threadIdx.x; i < nk * tot; i += 128) sa[i] = ga[i];
-    __syncthreads();
-    if (mine) {
-      const T* pv = sv + n * R + r;
-      const T* pa = sa + aoffn + j;
-      // the products do not depend on acc: unrolled, their loads and
-      // multiplies run ahead of the ordered additions
-#pragma unroll 16
-      for (int s2 = 0; s2 < nk; ++s2) acc = cadd<double>(acc, cmul<double>((double)pv[s2 * NR], (double)pa[s2 * tot]));
-    }
-    __syncthreads();
-  }
-  if (mine) partial[(size_t)c * CS + o] = acc;
+  if (lane == 0) partial[(size_t)c * CS + o] = acc;
 }
 
 size_t core_exact_ws_bytes(const ModelDesc& md, int n_chunks) {
@@ -785,19 +781,13 @@ int core_pass_exact(const int* rec, int rw, const int* visit, const int* map, lo
   SPTK_CUDA_TRY(cudaMemcpyAsync(d_lo, h_lo, sizeof(long long) * (nb + 1), cudaMemcpyHostToDevice, s));
   SPTK_CUDA_TRY(cudaMemsetAsync(partial, 0, (size_t)nb * md.cor_size * sizeof(double), s));
   const int vo = rec_val_off(md.n_modes, f64);
-  // staged samples per step of the ordered sums: <= 64, <= 96 KB of terms
-  int KT = (int)((96 * 1024) / ((NR + tot) * sizeof(T)));
-  KT = KT > 1024 ? 1024 : (KT < 1 ? 1 : KT);
-  const size_t ex_smem = (size_t)KT * (NR + tot) * sizeof(T);
-  SPTK_CUDA_TRY(cudaFuncSetAttribute(core_exact_sum_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)ex_smem));
   for (long long k0 = 0; k0 < n_visit; k0 += EXACT_SEG) {
     const int cnt = (int)(n_visit - k0 < EXACT_SEG ? n_visit - k0 : EXACT_SEG);
     core_exact_terms_kernel<T><<<(cnt + 127) / 128, 128, 0, s>>>(rec, rw, vo, visit, map, k0, cnt, fac, cor, md, tv,
                                                                   ta, tc);
     SPTK_CHECK_LAUNCH();
-    core_exact_sum_kernel<T><<<dim3((unsigned)((md.cor_size + 127) / 128), (unsigned)nb), 128, ex_smem, s>>>(
-        tv, ta, k0, cnt, d_lo, KT, md, partial);
+    core_exact_sum_kernel<T><<<dim3((unsigned)((md.cor_size + 3) / 4), (unsigned)nb), 128, 0, s>>>(
+        tv, ta, k0, cnt, d_lo, md, partial);
     SPTK_CHECK_LAUNCH();
   }
   core_reduce_ordered_kernel<<<(md.cor_size + 255) / 256, 256, 0, s>>>(partial, nb, md.cor_size, acc);

@@ -107,12 +107,12 @@ __global__ void __launch_bounds__(128) factor_dep_kernel(const int* __restrict__
     const T x = load_val<T>(rp, vo);
     int rows[SPTK_MAX_MODES];
     for (int n = 0; n < N; ++n) rows[n] = __ldg(rp + n);
-    // wait for the predecessors (all lanes poll the same words)
-    for (int n = 0; n < N; ++n) {
-      const int p = __ldg(pred + (long long)n * nv + k);
-      if (p >= 0)
-        while (ld_acquire(flags + p) == 0) {
-        }
+    // wait for the predecessors: lane n < N polls mode n's (one round trip
+    // per poll for all modes together)
+    {
+      const int p = lane < N ? __ldg(pred + (long long)lane * nv + k) : -1;
+      while (!__all_sync(0xffffffffu, p < 0 || ld_acquire(flags + p) != 0)) {
+      }
     }
     for (int n = 0; n < N; ++n) {
       const int J = md.jr[n];
