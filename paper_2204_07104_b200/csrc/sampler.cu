@@ -1579,6 +1579,63 @@ __global__ void __launch_bounds__(256) lp_exit_kernel(const uint32_t* __restrict
   ex[i] = q < 0 ? INT_MIN : (int)(q - t1);
 }
 
+// Two-stage exits.  Walks of one chunk never cross: a walk entering at a
+// larger offset can only be caught by one entering lower (same draw index,
+// same word, same bound), after which the two are identical.  Pass 1a walks
+// every candidate the first `pre` draws and records its offset there
+// (non-decreasing in the candidate); pass 1b walks the rest of the chunk once
+// per distinct offset (one thread per run of equal offsets) and gives the
+// run's exit to all of its candidates.
+__global__ void __launch_bounds__(256) lp_prewalk_kernel(const uint32_t* __restrict__ v, LpPlan P, int pre_len,
+                                                         const int* __restrict__ lo, int* __restrict__ pre) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)P.nch * P.W) return;
+  const int c = (int)(i / P.W), w = (int)(i % P.W);
+  if (w >= lo[P.nch + c]) return;
+  const long long r = (long long)lo[c] + w;
+  const long long t0 = (long long)c * LP_C, t1 = t0 + LP_C < P.T ? t0 + LP_C : P.T;
+  const long long tm = t0 + pre_len < t1 ? t0 + pre_len : t1;
+  const long long q = lp_walk(v, P.vcap, t0, tm, t0 + r, P.base, P.dir, nullptr);
+  pre[i] = q < 0 ? INT_MIN : (int)(q - tm);
+}
+
+// run starts compacted into a dense list (a lane per run, not per candidate:
+// most candidates of a run would otherwise idle in their warps)
+__global__ void __launch_bounds__(256) lp_runs_list_kernel(LpPlan P, const int* __restrict__ lo,
+                                                           const int* __restrict__ pre, int* __restrict__ nruns,
+                                                           int* __restrict__ runs) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  bool start = false;
+  if (i < (long long)P.nch * P.W) {
+    const int c = (int)(i / P.W), w = (int)(i % P.W);
+    start = w < lo[P.nch + c] && (w == 0 || pre[i - 1] != pre[i]);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, start);
+  int base = 0;
+  if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(nruns, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (start) runs[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (int)i;
+}
+
+__global__ void __launch_bounds__(256) lp_runs_kernel(const uint32_t* __restrict__ v, LpPlan P, int pre_len,
+                                                      const int* __restrict__ lo, const int* __restrict__ pre,
+                                                      const int* __restrict__ nruns, const int* __restrict__ runs,
+                                                      int* __restrict__ ex) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= *nruns) return;
+  const long long i = runs[g];
+  const int c = (int)(i / P.W), w = (int)(i % P.W), width = lo[P.nch + c];
+  const int d = pre[i];
+  const long long t0 = (long long)c * LP_C, t1 = t0 + LP_C < P.T ? t0 + LP_C : P.T;
+  const long long tm = t0 + pre_len < t1 ? t0 + pre_len : t1;
+  int e = INT_MIN;
+  if (d != INT_MIN) {
+    const long long q = lp_walk(v, P.vcap, tm, t1, tm + d, P.base, P.dir, nullptr);
+    e = q < 0 ? INT_MIN : (int)(q - t1);
+  }
+  for (int u = w; u < width && pre[(long long)c * P.W + u] == d; ++u) ex[(long long)c * P.W + u] = e;
+}
+
 __global__ void lp_resolve_kernel(LpPlan P, const int* __restrict__ lo, const int* __restrict__ ex,
                                   int* __restrict__ rc, long long* __restrict__ q_end_out, int* __restrict__ fail) {
   if (threadIdx.x != 0) return;
@@ -1631,7 +1688,7 @@ __global__ void __launch_bounds__(256) lp_emit_kernel(const uint32_t* __restrict
 
 static size_t lp_ws_bytes(long long T) {
   const long long nch = (T + LP_C - 1) / LP_C;
-  return (size_t)nch * 4096 * 4 + (size_t)(nch + 1) * 16 + 8 * 256;
+  return (size_t)nch * 4096 * 4 * 3 + (size_t)(nch + 1) * 16 + 8 * 256;
 }
 
 static double lp_p(long long rng) {  // P(reject) of one Lemire draw with bound rng (inclusive)
@@ -1717,11 +1774,32 @@ static int lemire_walk(const uint32_t* v, long long vcap, long long T, long long
   int* rc = cv.take<int>(nch + 1);
   int* fail = cv.take<int>(1);
   int* ex = cv.take<int>((size_t)nch * W);
+  int* pre = cv.take<int>((size_t)nch * W);
+  int* runs = cv.take<int>((size_t)nch * W);
+  int* nruns = cv.take<int>(1);
   SPTK_REQUIRE(cv.ok(), "sampler workspace too small (lemire walk)");
   lp_plan_kernel<<<1, 1024, 0, s>>>(P, lo);
   SPTK_CHECK_LAUNCH();
-  lp_exit_kernel<<<(unsigned)((nch * W + 255) / 256), 256, 0, s>>>(v, P, lo, ex);
-  SPTK_CHECK_LAUNCH();
+  // prefix length of the two-stage exits (SPTK_LP_PRE; 0 = walk every
+  // candidate through the whole chunk).  NF core batch, per epoch: one stage
+  // 1.09 ms; prefix 512 / 1024 / 2048: 0.62 / 0.69 / 0.84 ms
+  static int pre_len = -1;
+  if (pre_len < 0) {
+    const char* e = getenv("SPTK_LP_PRE");
+    pre_len = e ? atoi(e) : 512;
+  }
+  if (pre_len > 0 && pre_len < LP_C) {
+    lp_prewalk_kernel<<<(unsigned)((nch * W + 255) / 256), 256, 0, s>>>(v, P, pre_len, lo, pre);
+    SPTK_CHECK_LAUNCH();
+    SPTK_CUDA_TRY(cudaMemsetAsync(nruns, 0, sizeof(int), s));
+    lp_runs_list_kernel<<<(unsigned)((nch * W + 255) / 256), 256, 0, s>>>(P, lo, pre, nruns, runs);
+    SPTK_CHECK_LAUNCH();
+    lp_runs_kernel<<<(unsigned)((nch * W + 255) / 256), 256, 0, s>>>(v, P, pre_len, lo, pre, nruns, runs, ex);
+    SPTK_CHECK_LAUNCH();
+  } else {
+    lp_exit_kernel<<<(unsigned)((nch * W + 255) / 256), 256, 0, s>>>(v, P, lo, ex);
+    SPTK_CHECK_LAUNCH();
+  }
   lp_resolve_kernel<<<1, 32, 0, s>>>(P, lo, ex, rc, d_qend, fail);
   SPTK_CHECK_LAUNCH();
   lp_emit_kernel<<<(unsigned)((nch * 32 + 255) / 256), 256, 0, s>>>(v, P, rc, fail, out);
