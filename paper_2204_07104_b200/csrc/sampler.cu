@@ -2078,7 +2078,11 @@ __global__ void __launch_bounds__(32 * BP_JW) block_jgen_kernel(const BlockJob* 
   if ((threadIdx.x & 31) == 0 && jb.n > 0) js[jb.off] = 0;  // virtual step 0 (position 0 keeps what is left)
 }
 
-#define BP_T 256
+// threads per block permutation CTA (NF W=24: 256 / 512 / 1024 -> 1.72 /
+// 1.62 / 2.24 ms per epoch)
+#ifndef BP_T
+#define BP_T 512
+#endif
 // Shared memory per nonzero: 8 bytes -- C (group counts, then group starts /
 // ends: 16-bit halves of 32-bit words, so the counting and scatter atomics
 // stay 32-bit), J (target of each step), S (each target's group sorted by
