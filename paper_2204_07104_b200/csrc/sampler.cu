@@ -1700,6 +1700,8 @@ static double lp_p(long long rng) {  // P(reject) of one Lemire draw with bound 
 // window width for +-4.5 sigma of the offset at the chunk start (both from
 // p/(1-p) and p(1-p) sampled every 16 draws and block-scanned over the
 // chunks), at most P.W, so early chunks walk fewer candidates
+#define LP_PLAN_CACHE 4096
+__device__ int g_lp_plan_cache[LP_PLAN_CACHE];
 __global__ void __launch_bounds__(1024) lp_plan_kernel(LpPlan P, int* __restrict__ lo) {
   __shared__ double sc[1024], sv[1024];
   const int c = threadIdx.x;
@@ -1778,8 +1780,32 @@ static int lemire_walk(const uint32_t* v, long long vcap, long long T, long long
   int* runs = cv.take<int>((size_t)nch * W);
   int* nruns = cv.take<int>(1);
   SPTK_REQUIRE(cv.ok(), "sampler workspace too small (lemire walk)");
-  lp_plan_kernel<<<1, 1024, 0, s>>>(P, lo);
-  SPTK_CHECK_LAUNCH();
+  {
+    // the plan depends only on (T, base, dir, W): computed once, then copied
+    // from a library-owned device cache (the per-thread modulo loop is 80 us)
+    static long long kT = -1, kbase = 0;
+    static int kdir = 0, kW = 0, kdev = -1;
+    int dev = 0;
+    SPTK_CUDA_TRY(cudaGetDevice(&dev));
+    int* cache = nullptr;
+    SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&cache, g_lp_plan_cache));
+    const bool fits = 2 * nch <= LP_PLAN_CACHE;
+    if (fits && kT == T && kbase == base && kdir == dir && kW == W && kdev == dev) {
+      SPTK_CUDA_TRY(cudaMemcpyAsync(lo, cache, sizeof(int) * 2 * nch, cudaMemcpyDeviceToDevice, s));
+    } else {
+      lp_plan_kernel<<<1, 1024, 0, s>>>(P, lo);
+      SPTK_CHECK_LAUNCH();
+      if (fits) {
+        SPTK_CUDA_TRY(cudaMemcpyAsync(cache, lo, sizeof(int) * 2 * nch, cudaMemcpyDeviceToDevice, s));
+        SPTK_CUDA_TRY(cudaStreamSynchronize(s));  // once per parameter set: the cache is complete before use
+        kT = T;
+        kbase = base;
+        kdir = dir;
+        kW = W;
+        kdev = dev;
+      }
+    }
+  }
   // prefix length of the two-stage exits (SPTK_LP_PRE; 0 = walk every
   // candidate through the whole chunk).  NF core batch, per epoch: one stage
   // 1.09 ms; prefix 512 / 1024 / 2048: 0.62 / 0.69 / 0.84 ms
