@@ -349,8 +349,10 @@ def bench_ours(args, cfg):
             torch.cuda.synchronize()
             runs.append(time.perf_counter() - t1)
         el = sorted(runs)[1]
-        h2d = tr.indices.nbytes + tr.values.nbytes + te.indices.nbytes + te.values.nbytes + \
-            sum(a.nbytes for a in m2.factors + m2.core_factors)
+        # what crosses PCIe: fp32 records (packed by the upload threads, 4 words
+        # per nonzero at order <= 3, 8 up to 7) and the fp32 model
+        rw = 4 if order <= 3 else 8
+        h2d = (tr.nnz + te.nnz) * rw * 4 + sum(a.size * 4 for a in m2.factors + m2.core_factors)
         d2h = sum(a.nbytes for a in m2.factors + m2.core_factors) + 32 * k2
         log("e2e done")
         e2e = {"value": cfg["nnz"] * k2 / el, "unit": "nnz/s", "h2d_bytes_per_step": h2d // k2,

@@ -181,6 +181,17 @@ size_t sptk_partition_ws_bytes(long long nnz, int order, long long m);
 int sptk_partition(const int64_t* d_idx, const double* d_vals, long long nnz, int order, const int64_t* h_dims,
                    long long m, int f64_records, int32_t* d_rec, int32_t* d_ids, int32_t* d_pos_of_id,
                    int32_t* d_block_off, void* d_ws, size_t ws_bytes, void* stream);
+/* The fp32 record path of the two calls above with the packing moved to the
+ * host side of the upload: sptk_h2d_pack converts the COO arrays (int64
+ * indices [nnz, order], float64 values; indices < 2^31) into fp32 records
+ * {i_0..i_{N-1}, value} in the upload threads' pinned staging buffers and
+ * DMAs those (16 bytes per nonzero at order <= 3 instead of 8N + 8);
+ * sptk_partition_records then groups device records (source order) by block
+ * exactly like sptk_partition (m == 1: in place, d_rec_out == d_rec_src). */
+int sptk_h2d_pack(int32_t* d_rec, const int64_t* h_idx, const double* h_vals, long long nnz, int order, int threads);
+int sptk_partition_records(const int32_t* d_rec_src, long long nnz, int order, const int64_t* h_dims, long long m,
+                           int32_t* d_rec_out, int32_t* d_ids, int32_t* d_pos_of_id, int32_t* d_block_off, void* d_ws,
+                           size_t ws_bytes, void* stream);
 int sptk_pack_records(const int64_t* d_idx, const double* d_vals, long long nnz, int order, int f64_records,
                       int32_t* d_rec, void* stream);
 

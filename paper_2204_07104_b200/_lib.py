@@ -62,6 +62,9 @@ SIGNATURES = {
     "sptk_partition_ws_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int, _i64]),
     "sptk_partition": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, _i64p, _i64, ctypes.c_int, _vp, _vp,
                                       _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "sptk_h2d_pack": (ctypes.c_int, [_vp, _vp, _vp, _i64, ctypes.c_int, ctypes.c_int]),
+    "sptk_partition_records": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _i64p, _i64, _vp, _vp, _vp, _vp, _vp,
+                                              ctypes.c_size_t, _vp]),
     "sptk_pack_records": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp]),
     "sptk_factor_pass": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _i64, _vp, _i64p, _vp, _i64p, _i64p,
                                         ctypes.c_int, ctypes.c_int, _f64p, _f64p, ctypes.c_int, _vp]),

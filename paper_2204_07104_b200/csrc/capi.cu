@@ -172,6 +172,18 @@ int sptk_partition(const int64_t* d_idx, const double* d_vals, long long nnz, in
                    d_pos_of_id, d_block_off, d_ws, ws_bytes, (cudaStream_t)stream, f64_records);
 }
 
+int sptk_h2d_pack(int32_t* d_rec, const int64_t* h_idx, const double* h_vals, long long nnz, int order,
+                  int threads) {
+  return h2d_pack_records(d_rec, (const long long*)h_idx, h_vals, nnz, order, rec_words(order), threads);
+}
+
+int sptk_partition_records(const int32_t* d_rec_src, long long nnz, int order, const int64_t* h_dims, long long m,
+                           int32_t* d_rec_out, int32_t* d_ids, int32_t* d_pos_of_id, int32_t* d_block_off, void* d_ws,
+                           size_t ws_bytes, void* stream) {
+  return partition_records(d_rec_src, rec_words(order), nnz, order, (const long long*)h_dims, m, d_rec_out, d_ids,
+                           d_pos_of_id, d_block_off, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
 int sptk_pack_records(const int64_t* d_idx, const double* d_vals, long long nnz, int order, int f64_records,
                       int32_t* d_rec, void* stream) {
   return pack_records((const long long*)d_idx, d_vals, nnz, order, d_rec, (cudaStream_t)stream, f64_records);

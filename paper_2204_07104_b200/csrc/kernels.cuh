@@ -42,6 +42,11 @@ int partition(const long long* idx64, const double* vals64, long long nnz, int o
               size_t ws_bytes, cudaStream_t s, int f64);
 int pack_records(const long long* idx64, const double* vals64, long long nnz, int order, int* rec_out,
                  cudaStream_t s, int f64);
+int partition_records(const int* rec_src, int rw, long long nnz, int order, const long long* h_dims, long long m,
+                      int* rec_out, int* ids_out, int* pos_of_id_out, int* block_off_out, void* ws, size_t ws_bytes,
+                      cudaStream_t s);
+int h2d_pack_records(int* d_rec, const long long* h_idx, const double* h_vals, long long nnz, int order, int rw,
+                     int threads);
 size_t radix_ws_bytes(long long n);
 int radix_sort_pairs(unsigned* k0, int* v0, unsigned* k1, int* v1, long long n, int bits, void* ws, size_t ws_bytes,
                      cudaStream_t s, unsigned** kout, int** vout);

@@ -337,6 +337,121 @@ int radix_sort_pairs(unsigned* k0, int* v0, unsigned* k1, int* v1, long long n, 
   return 0;
 }
 
+__global__ void rec_keys_kernel(const int* __restrict__ rec, int rw, long long nnz, int N, MDims md, long long m,
+                                unsigned* __restrict__ keys, int* __restrict__ vals) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; e < nnz; e += stride) {
+    unsigned long long key = 0;
+    for (int n = 0; n < N; ++n) {
+      const long long i = rec[e * rw + n];
+      const long long d = md.d[n];
+      long long lo = 0, hi = m;  // largest b in [0, m-1] with floor(b*d/m) <= i
+      while (hi - lo > 1) {
+        const long long mid = (lo + hi) >> 1;
+        if ((mid * d) / m <= i) lo = mid;
+        else hi = mid;
+      }
+      key = key * (unsigned long long)m + (unsigned long long)lo;
+    }
+    keys[e] = (unsigned)key;
+    vals[e] = (int)e;
+  }
+}
+
+__global__ void rec_gather_kernel(const int* __restrict__ src, int rw, const int* __restrict__ ids, long long nnz,
+                                  int* __restrict__ dst, int* __restrict__ pos_of_id) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nnz; p += stride) {
+    const long long id = ids[p];
+    const int4* s4 = reinterpret_cast<const int4*>(src + id * rw);
+    int4* d4 = reinterpret_cast<int4*>(dst + p * rw);
+    for (int q = 0; q < rw / 4; ++q) d4[q] = s4[q];
+    if (pos_of_id) pos_of_id[id] = (int)p;
+  }
+}
+
+// K1 from records already on the device in source order (sptk_h2d_pack):
+// the same stable block grouping as partition(), keys read from the records'
+// int32 indices; rec_out receives the grouped records (m == 1: rec_src is
+// already the layout -- pass rec_out == rec_src).
+int partition_records(const int* rec_src, int rw, long long nnz, int order, const long long* h_dims, long long m,
+                      int* rec_out, int* ids_out, int* pos_of_id_out, int* block_off_out, void* ws, size_t ws_bytes,
+                      cudaStream_t s) {
+  SPTK_REQUIRE(order >= 2 && order <= SPTK_MAX_MODES, "partition_records: bad order");
+  SPTK_REQUIRE(m >= 1, "partition_records: m must be >= 1");
+  long long nkeys = 1;
+  for (int n = 0; n < order; ++n) {
+    SPTK_REQUIRE(m <= h_dims[n], "partition_records: m=%lld exceeds mode %d dimension %lld", m, n, h_dims[n]);
+    nkeys *= m;
+    SPTK_REQUIRE(nkeys < (1LL << 31), "partition_records: too many blocks");
+  }
+  SPTK_REQUIRE(nnz >= 0 && nnz < (1LL << 31), "partition_records: nnz out of range");
+  SPTK_REQUIRE(ws_bytes >= partition_ws_bytes(nnz, order, m), "partition_records: workspace too small");
+  if (m == 1) {
+    SPTK_REQUIRE(rec_out == rec_src, "partition_records: m == 1 keeps the records in place (rec_out == rec_src)");
+    if (nnz > 0)
+      for (int* o : {ids_out, pos_of_id_out})
+        if (o) {
+          iota_i32_kernel<<<gridn(nnz, 256), 256, 0, s>>>(o, nnz);
+          SPTK_CHECK_LAUNCH();
+        }
+    block_off1_kernel<<<1, 32, 0, s>>>(block_off_out, (int)nnz);
+    SPTK_CHECK_LAUNCH();
+    return 0;
+  }
+  SPTK_REQUIRE(rec_out != rec_src, "partition_records: m > 1 needs a separate output buffer");
+  Carve2 cv{(char*)ws, ws_bytes};
+  unsigned* k0 = cv.take<unsigned>(nnz + 1);
+  unsigned* k1 = cv.take<unsigned>(nnz + 1);
+  int* v0 = cv.take<int>(nnz + 1);
+  int* v1 = cv.take<int>(nnz + 1);
+  long long ntiles = (nnz + RX_TILE - 1) / RX_TILE;
+  if (ntiles < 1) ntiles = 1;
+  int* hist = cv.take<int>(256 * ntiles + 2);
+  int* offs = cv.take<int>(256 * ntiles + 2);
+  int* sws = cv.take<int>(scan_ws_bytes(256 * ntiles + 1) / 4 + 1);
+  int* kcnt = cv.take<int>(nkeys + 2);
+  int* sws2 = cv.take<int>(scan_ws_bytes(nkeys + 1) / 4 + 1);
+  SPTK_REQUIRE(!cv.bad, "partition_records: workspace carve failed");
+  MDims md;
+  for (int n = 0; n < order; ++n) md.d[n] = h_dims[n];
+  if (nnz > 0) {
+    rec_keys_kernel<<<gridn(nnz, 256), 256, 0, s>>>(rec_src, rw, nnz, order, md, m, k0, v0);
+    SPTK_CHECK_LAUNCH();
+    int bits = 0;
+    while ((1LL << bits) < nkeys) ++bits;
+    unsigned* kin = k0;
+    unsigned* kout = k1;
+    int* vin = v0;
+    int* vout = v1;
+    for (int shift = 0; shift < bits; shift += 8) {
+      radix_hist_kernel<<<(unsigned)ntiles, RX_THREADS, 0, s>>>(kin, nnz, shift, (int)ntiles, hist);
+      SPTK_CHECK_LAUNCH();
+      if (exclusive_scan(hist, 256 * ntiles, offs, sws, s)) return 1;
+      radix_scatter_kernel<<<(unsigned)ntiles, RX_THREADS, 0, s>>>(kin, vin, nnz, shift, (int)ntiles, offs, hist,
+                                                                   kout, vout);
+      SPTK_CHECK_LAUNCH();
+      unsigned* tk = kin;
+      kin = kout;
+      kout = tk;
+      int* tv = vin;
+      vin = vout;
+      vout = tv;
+    }
+    SPTK_CUDA_TRY(cudaMemsetAsync(kcnt, 0, sizeof(int) * (nkeys + 1), s));
+    key_count_kernel<<<gridn(nnz, 256), 256, 0, s>>>(kin, nnz, kcnt);
+    SPTK_CHECK_LAUNCH();
+    if (exclusive_scan(kcnt, nkeys, block_off_out, sws2, s)) return 1;
+    if (ids_out) SPTK_CUDA_TRY(cudaMemcpyAsync(ids_out, vin, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
+    rec_gather_kernel<<<gridn(nnz, 256), 256, 0, s>>>(rec_src, rw, vin, nnz, rec_out, pos_of_id_out);
+    SPTK_CHECK_LAUNCH();
+  } else {
+    SPTK_CUDA_TRY(cudaMemsetAsync(block_off_out, 0, sizeof(int) * (nkeys + 1), s));
+  }
+  return 0;
+}
+
 int pack_records(const long long* idx64, const double* vals64, long long nnz, int order, int* rec_out,
                  cudaStream_t s, int f64) {
   if (nnz <= 0) return 0;

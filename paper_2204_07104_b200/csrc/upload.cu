@@ -102,4 +102,65 @@ int h2d(void* dst, const void* src, size_t bytes, int threads) {
   return 0;
 }
 
+// The COO arrays packed into device records on the way: every lane converts
+// its slice of nonzeros (int64 indices, float64 value) into the fp32 record
+// layout {i_0..i_{N-1} (int32), value (fp32)} in its pinned staging buffer and
+// DMAs that -- 16 bytes per nonzero over PCIe instead of 8N + 8 (NF: 1.6 GB
+// instead of 3.2 GB).  Indices must fit int32 (checked by the caller).
+int h2d_pack_records(int* d_rec, const long long* h_idx, const double* h_vals, long long nnz, int order, int rw,
+                     int threads) {
+  if (nnz <= 0) return 0;
+  SPTK_REQUIRE(order >= 1 && order < rw, "h2d_pack_records: bad order %d for %d-word records", order, rw);
+  int T = threads > 0 ? threads : (int)std::thread::hardware_concurrency();
+  if (const char* e = getenv("SPTK_H2D_THREADS")) T = atoi(e);
+  if (T < 1) T = 1;
+  if (T > 32) T = 32;
+  const long long per_piece = (long long)(kPiece / ((size_t)rw * 4));
+  if ((nnz + T - 1) / T < per_piece) T = (int)((nnz + per_piece - 1) / per_piece);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_lanes(T)) return 1;
+  int dev = g_dev;
+  std::vector<int> rc(T, 0);
+  std::vector<std::thread> th;
+  const long long slice = (nnz + T - 1) / T;
+  for (int t = 0; t < T; ++t) {
+    th.emplace_back([&, t]() {
+      cudaSetDevice(dev);
+      Lane& l = g_lanes[t];
+      const long long lo = (long long)t * slice, hi = lo + slice < nnz ? lo + slice : nnz;
+      int b = 0;
+      for (long long a = lo; a < hi; a += per_piece, b ^= 1) {
+        const long long n = hi - a < per_piece ? hi - a : per_piece;
+        if (cudaEventSynchronize(l.ev[b]) != cudaSuccess) {
+          rc[t] = 1;
+          return;
+        }
+        int* out = reinterpret_cast<int*>(l.buf[b]);
+        for (long long k = 0; k < n; ++k) {
+          const long long* ix = h_idx + (a + k) * order;
+          int* r = out + k * rw;
+          for (int q = 0; q < order; ++q) r[q] = (int)ix[q];
+          const float v = (float)h_vals[a + k];
+          memcpy(r + order, &v, 4);
+          for (int q = order + 1; q < rw; ++q) r[q] = 0;
+        }
+        if (cudaMemcpyAsync(d_rec + a * rw, l.buf[b], (size_t)n * rw * 4, cudaMemcpyHostToDevice, l.st) !=
+                cudaSuccess ||
+            cudaEventRecord(l.ev[b], l.st) != cudaSuccess) {
+          rc[t] = 1;
+          return;
+        }
+      }
+      if (cudaStreamSynchronize(l.st) != cudaSuccess) rc[t] = 1;
+    });
+  }
+  for (auto& x : th) x.join();
+  for (int t = 0; t < T; ++t)
+    if (rc[t]) {
+      set_error("h2d_pack_records: CUDA error in upload lane %d: %s", t, cudaGetErrorString(cudaGetLastError()));
+      return 1;
+    }
+  return 0;
+}
+
 }  // namespace sptk

@@ -59,7 +59,15 @@ class DeviceModel:
             out[: m.shape[0], : m.shape[1]] = m
             return out.ravel()
 
-        fac = np.concatenate([padded(a, a.shape[0], int(j)) for a, j in zip(model.factors, self.jr)]).astype(npdt)
+        # packed straight into one host buffer of the device dtype, one upload
+        fac = np.empty(int(self.foff[-1]), dtype=npdt)
+        for n, (a, j) in enumerate(zip(model.factors, self.jr)):
+            dst = fac[int(self.foff[n]): int(self.foff[n + 1])].reshape(a.shape[0], int(j))
+            if a.shape[1] == int(j):
+                np.copyto(dst, a, casting="unsafe")
+            else:
+                dst[:] = 0
+                np.copyto(dst[:, : a.shape[1]], a, casting="unsafe")
         cor = np.concatenate([padded(b, int(j), self.rcore) for b, j in zip(model.core_factors, self.jr)]).astype(npdt)
         self.fac = torch.from_numpy(fac).to(self.device)
         self.cor = torch.from_numpy(cor).to(self.device)
@@ -94,9 +102,15 @@ class DeviceCoo:
         self.f64 = f64
         self.rw = record_words(self.order, f64)
         self.rec = torch.empty(max(self.nnz, 1) * self.rw, dtype=torch.int32, device=dev)
-        if self.nnz:
+        vals = np.ascontiguousarray(values, dtype=np.float64)
+        if self.nnz and not f64 and dev.index in (None, torch.cuda.current_device()):
+            # fp32 records packed by the upload threads (sptk_h2d_pack)
+            torch.cuda.current_stream().synchronize()
+            check(_lib.load().sptk_h2d_pack(ptr(self.rec), idx.ctypes.data, vals.ctypes.data, self.nnz, self.order, 0),
+                  "sptk_h2d_pack")
+        elif self.nnz:
             d_idx = torch.from_numpy(idx).to(dev)
-            d_val = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(dev)
+            d_val = torch.from_numpy(vals).to(dev)
             check(_lib.load().sptk_pack_records(ptr(d_idx), ptr(d_val), self.nnz, self.order,
                                                 1 if f64 else 0, ptr(self.rec), stream_ptr()),
                   "sptk_pack_records")

@@ -200,6 +200,62 @@ class BlockOrders:
         span = max([j[0] + j[2] for j in jobs], default=1)
         self.js = None if big else torch.empty(max(span, 1), dtype=torch.int16, device=device)
 
+    @classmethod
+    def from_arrays(cls, blocks, offs, cnts, order: int, device, big: bool = False, pad: int = 1):
+        """The same table from arrays: blocks [R, M, order], offs / cnts [R, M]
+        (record offset and size of each round's blocks; empty blocks are
+        dropped).  Vectorised: the NF W=24 table (13,824 jobs) in ~2 ms instead
+        of the ~50 ms of the tuple loops."""
+        import torch
+
+        self = cls.__new__(cls)
+        self.big = big
+        cnts = np.asarray(cnts, dtype=np.int64)
+        offs = np.asarray(offs, dtype=np.int64)
+        blocks = np.asarray(blocks, dtype=np.int64)
+        R = cnts.shape[0]
+        mask = cnts > 0
+        m_r = mask.sum(axis=1)
+        if (m_r > 64).any():
+            raise ValueError("at most 64 blocks per round")
+        if not big and cnts.max(initial=0) > BLOCK_PERM_MAX:
+            raise ValueError(f"block of {int(cnts.max())} nonzeros exceeds {BLOCK_PERM_MAX}")
+        sums = np.where(mask, cnts, 0).sum(axis=1)
+        nmin = np.where(mask, cnts, np.iinfo(np.int64).max).min(axis=1, initial=np.iinfo(np.int64).max)
+        nmin = np.where(m_r > 0, nmin, 0)
+        starts = np.zeros(R + 1, dtype=np.int64)
+        if pad > 1:
+            step = np.maximum(sums, pad)
+            step = (step + pad - 1) // pad * pad
+        else:
+            step = sums
+        starts[1:] = np.cumsum(step)
+        self.round_start = starts.tolist()
+        self.round_end = (starts[:-1] + sums).tolist()
+        self.total = int(starts[-1])
+        first = np.concatenate([[0], np.cumsum(m_r)[:-1]])
+        slot = np.cumsum(mask, axis=1) - 1
+        rr, cc = np.nonzero(mask)
+        tab = np.zeros(len(rr), dtype=BLOCK_JOB_DTYPE)
+        tab["off"] = offs[rr, cc]
+        tab["out_base"] = starts[rr]
+        tab["n"] = cnts[rr, cc]
+        tab["first"] = first[rr]
+        tab["m"] = m_r[rr]
+        tab["slot"] = slot[rr, cc]
+        tab["nmin"] = nmin[rr]
+        self.n_jobs = len(rr)
+        self.order = order
+        self.cap = int(cnts.max(initial=1)) if self.n_jobs else 1
+        if int(_lib.load().sptk_block_job_bytes()) != BLOCK_JOB_DTYPE.itemsize:
+            raise RuntimeError("BlockJob layout mismatch between libsptk and sampler.py")
+        self.jobs = torch.from_numpy(tab.view(np.uint8).copy()).to(device)
+        self.coords = torch.from_numpy(np.ascontiguousarray(blocks[rr, cc], dtype=np.int32).reshape(-1, order)).to(
+            device)
+        span = int((offs + cnts)[mask].max(initial=1)) if self.n_jobs else 1
+        self.js = None if big else torch.empty(max(span, 1), dtype=torch.int16, device=device)
+        return self
+
     def draw(self, seed: int, t: int, out, stream=None) -> None:
         """visit orders of epoch t into out[0:total] (int32, device)."""
         check(_lib.load().sptk_block_perm(ptr(self.jobs), ptr(self.coords), self.n_jobs, self.order, int(seed),

@@ -94,15 +94,29 @@ class DevicePartition:
         self.ids = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) if want_ids else None
         self.pos_of_id = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
         self.block_off_dev = torch.empty(nkeys + 1, dtype=torch.int32, device=dev)
-        d_idx = upload(idx)
-        d_val = upload(np.ascontiguousarray(values, dtype=np.float64))
         need = int(L.sptk_partition_ws_bytes(self.nnz, self.order, self.m))
         ws = torch.empty(need, dtype=torch.uint8, device=dev)
         dims_c, pd = i64arr(self.dims)
-        check(L.sptk_partition(ptr(d_idx), ptr(d_val), self.nnz, self.order, pd, self.m, 1 if f64 else 0,
-                               ptr(self.rec), ptr(self.ids), ptr(self.pos_of_id), ptr(self.block_off_dev),
-                               ptr(ws), need, stream_ptr()), "sptk_partition")
-        del d_idx, d_val, ws
+        vals = np.ascontiguousarray(values, dtype=np.float64)
+        if not f64 and self.nnz:
+            # fp32 records packed on the host side of the upload (half the
+            # PCIe bytes), then grouped on the device
+            src = self.rec if self.m == 1 else torch.empty_like(self.rec)
+            torch.cuda.current_stream().synchronize()  # the upload runs on sptk's own streams
+            check(L.sptk_h2d_pack(ptr(src), idx.ctypes.data, vals.ctypes.data, self.nnz, self.order, 0),
+                  "sptk_h2d_pack")
+            check(L.sptk_partition_records(ptr(src), self.nnz, self.order, pd, self.m, ptr(self.rec), ptr(self.ids),
+                                           ptr(self.pos_of_id), ptr(self.block_off_dev), ptr(ws), need,
+                                           stream_ptr()), "sptk_partition_records")
+            del src
+        else:
+            d_idx = upload(idx)
+            d_val = upload(vals)
+            check(L.sptk_partition(ptr(d_idx), ptr(d_val), self.nnz, self.order, pd, self.m, 1 if f64 else 0,
+                                   ptr(self.rec), ptr(self.ids), ptr(self.pos_of_id), ptr(self.block_off_dev),
+                                   ptr(ws), need, stream_ptr()), "sptk_partition")
+            del d_idx, d_val
+        del ws
         self.block_off = self.block_off_dev.cpu().numpy().astype(np.int64)
 
     def block_range(self, block) -> tuple[int, int]:
@@ -135,15 +149,34 @@ def _gray(digits: int, m: int) -> list:
     return seq
 
 
+def gray_offsets(digits: int, m: int) -> np.ndarray:
+    """The reflected base-m Gray code of _gray as an int64 array [m^digits, digits]."""
+    seq = np.zeros((1, 0), dtype=np.int64)
+    for _ in range(digits):
+        parts = []
+        for lead in range(m):
+            tail = seq if lead % 2 == 0 else seq[::-1]
+            parts.append(np.concatenate([np.full((tail.shape[0], 1), lead, dtype=np.int64), tail], axis=1))
+        seq = np.concatenate(parts, axis=0)
+    return seq
+
+
+def round_blocks(order: int, m: int) -> np.ndarray:
+    """round_schedule(order, m).rounds as an int64 array [rounds, m, order]:
+    worker w's block in round r is (w, (w + d_1) % m, ...) (partition.py:100-117)."""
+    offs = gray_offsets(order - 1, m)
+    w = np.arange(m, dtype=np.int64)
+    cols = [np.broadcast_to(w, (offs.shape[0], m))] + [(w[None, :] + offs[:, d: d + 1]) % m
+                                                        for d in range(order - 1)]
+    return np.stack(cols, axis=2)
+
+
 def round_schedule(order: int, m: int) -> RoundSchedule:
     if order < 2:
         raise ValueError("order must be >= 2")
     if m < 1:
         raise ValueError("m must be >= 1")
-    rounds = tuple(
-        tuple((w,) + tuple((w + d) % m for d in offs) for w in range(m))
-        for offs in _gray(order - 1, m)
-    )
+    rounds = tuple(tuple(tuple(b) for b in rnd) for rnd in round_blocks(order, m).tolist())
     return RoundSchedule(order, m, rounds)
 
 

@@ -46,7 +46,7 @@ from ._lib import check, f64arr, i64arr, ptr, stream_ptr
 from .device import DeviceCoo, DeviceModel, eval_sums, rmse_mae_device
 from .sampler import (BLOCK_PERM_MAX, BlockOrders, Workspace, choice, fy_apply, pcg64_state, permutation_j,
                       permutation_j_batch)
-from .schedule import DevicePartition, round_schedule
+from .schedule import DevicePartition, round_blocks, round_schedule
 from .tensor import DatasetSplit, SparseTensorCoo
 from .tucker import TuckerModel
 
@@ -227,20 +227,19 @@ class EpochRunner:
         self.dm = DeviceModel(model, f64=self.f64, pad_rank=pad)
         self.part = DevicePartition(train_set.indices, train_set.values, model.dims, self.m, f64=self.f64,
                                     want_ids=False)
-        self.schedule = round_schedule(model.order, self.m)
-        # host list of (block, offset, count) per round, empty blocks dropped
-        self.rounds = []
-        self.nnz_local = 0
-        for rnd in self.schedule.rounds:
-            items = []
-            for block in rnd:
-                if owner_rank is not None and block[0] != owner_rank:
-                    continue
-                off, cnt = self.part.block_range(block)
-                if cnt > 0:
-                    items.append((block, off, cnt))
-                    self.nnz_local += cnt
-            self.rounds.append(items)
+        # the DSGD rounds as arrays: blocks [R, M, N] (worker w's block in
+        # round r, partition.py:100-117), their record offsets and sizes
+        blocks = round_blocks(model.order, self.m)
+        if owner_rank is not None:
+            blocks = blocks[:, owner_rank: owner_rank + 1]
+        keys = (blocks * (self.m ** np.arange(model.order - 1, -1, -1, dtype=np.int64))).sum(axis=2)
+        self._r_blocks = blocks
+        self._r_off = self.part.block_off[keys]
+        self._r_cnt = self.part.block_off[keys + 1] - self._r_off
+        self._rounds = None
+        self.nnz_local = int(self._r_cnt.sum())
+        per_round = (self._r_cnt > 0).sum(axis=1)
+        max_block = int(self._r_cnt.max(initial=1))
         dev = self.dm.fac.device
         # Flat DSGD (throughput mode, W > 1 workers on one GPU): every block's
         # visit order comes from one shared-memory CTA (sptk_block_perm) and
@@ -249,17 +248,16 @@ class EpochRunner:
         # reference's W parallel workers per round (trainer.py:189-208).
         self.flat = (self.m > 1 and self.mode == 0 and not self.f64 and owner_rank is None
                      and _env_int("SPTK_FLAT", 1) == 1
-                     and all(len(items) <= 64 for items in self.rounds)
-                     and max((c for items in self.rounds for (_, _, c) in items), default=0) <= BLOCK_PERM_MAX)
+                     and int(per_round.max(initial=0)) <= 64 and max_block <= BLOCK_PERM_MAX)
         # Blocks too large for one CTA (NF at W = 16: ~24K nonzeros): their
         # orders come from the batched sampler below and are then interleaved
         # the same way (sptk_interleave_rounds), so the factor phase is still
         # one pass -- per-block launches would put a whole block's samples in
         # flight over its 1/W of the rows (Hogwild contention, divergence).
         self.flat_big = (not self.flat and self.m > 1 and self.mode == 0 and not self.f64 and owner_rank is None
-                         and _env_int("SPTK_FLAT", 1) == 1 and all(len(items) <= 64 for items in self.rounds))
-        self.block_orders = (BlockOrders(self.rounds, self.order, dev) if self.flat else
-                             BlockOrders(self.rounds, self.order, dev, big=True) if self.flat_big else None)
+                         and _env_int("SPTK_FLAT", 1) == 1 and int(per_round.max(initial=0)) <= 64)
+        self.block_orders = (BlockOrders.from_arrays(blocks, self._r_off, self._r_cnt, self.order, dev,
+                                                     big=self.flat_big) if (self.flat or self.flat_big) else None)
         self.fvis = ([torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev) for _ in range(2)]
                      if self.flat_big else None)
         # Sampler state (K2), double-buffered by epoch parity: Fisher-Yates
@@ -275,20 +273,22 @@ class EpochRunner:
         # one preallocated workspace per sampler stage (never regrown while a
         # kernel on another stream may still be using it)
         Lb = _lib.load()
-        max_block = max((c for items in self.rounds for (_, _, c) in items), default=1)
         # This process's blocks lie end to end in the partitioned records
         # (block key order, mode 0 most significant), so their visit orders are
         # applied in ONE Fisher-Yates pass over the concatenation
         # (sptk_fy_globalize): the visit entries are then relative to lo.
-        own = sorted((off, cnt) for items in self.rounds for (_, off, cnt) in items)
-        self.lo = own[0][0] if own else 0
-        self.hi = own[-1][0] + own[-1][1] if own else 0
-        contiguous = all(a[0] + a[1] == b[0] for a, b in zip(own, own[1:]))
+        nz = self._r_cnt > 0
+        order_idx = np.argsort(self._r_off[nz], kind="stable")
+        own_off = self._r_off[nz][order_idx]
+        own_cnt = self._r_cnt[nz][order_idx]
+        self.lo = int(own_off[0]) if own_off.size else 0
+        self.hi = int(own_off[-1] + own_cnt[-1]) if own_off.size else 0
+        contiguous = bool(np.all(own_off[:-1] + own_cnt[:-1] == own_off[1:]))
         # (measured per-rank DSGD epochs, NF: batching pays from 16 blocks up)
         min_fy = _env_int("SPTK_BATCHED_FY_MIN_BLOCKS", 16)
-        self.batched_fy = contiguous and len(own) > 1 and len(own) >= min_fy
+        self.batched_fy = contiguous and own_off.size > 1 and own_off.size >= min_fy
         if self.batched_fy:
-            offs = np.array([o - self.lo for o, _ in own] + [self.hi - self.lo], dtype=np.int32)
+            offs = np.concatenate([own_off - self.lo, [self.hi - self.lo]]).astype(np.int32)
             self.fy_off = torch.from_numpy(offs).to(dev)
         self.ws_j, self.ws_fy, self.ws_psi = Workspace(dev), Workspace(dev), Workspace(dev)
         if self.flat:
@@ -352,6 +352,16 @@ class EpochRunner:
         # sampler stage's previous output instead of drawing it again, to measure
         # what that stage's co-running costs the epoch
         self._skip = set(filter(None, os.environ.get("SPTK_EXP_SKIP", "").split(",")))
+
+    @property
+    def rounds(self):
+        """Host list of (block, offset, count) per round, empty blocks dropped
+        (built on first use: the flat paths work from the arrays)."""
+        if self._rounds is None:
+            self._rounds = [[(tuple(b), o, c) for b, o, c in zip(bl, of, cn) if c > 0]
+                            for bl, of, cn in zip(self._r_blocks.tolist(), self._r_off.tolist(),
+                                                  self._r_cnt.tolist())]
+        return self._rounds
 
     # -- samplers (K2) -----------------------------------------------------
     def draw_core_batch(self, t: int, stream) -> None:
