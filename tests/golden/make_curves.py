@@ -35,6 +35,7 @@ O6 = (10_000,) * 6
 CURVES = {
     "y4_20m": dict(dims=Y4, nnz=20_000_000, n_test=200_000, J=16, alpha_a=0.001, epochs=5),
     "y4_full": dict(dims=Y4, nnz=250_272_286, n_test=2_502_723, J=16, alpha_a=0.001, epochs=5),
+    "o6_100m": dict(dims=O6, nnz=100_000_000, n_test=1_000_000, J=8, alpha_a=0.001, epochs=5),
     "o6_10m": dict(dims=O6, nnz=10_000_000, n_test=100_000, J=8, alpha_a=0.001, epochs=5),
     "nf99_j4": dict(dims=NF, nnz=99_072_112, n_test=1_408_395, J=4, alpha_a=0.003, epochs=5),
     "nf99_j8": dict(dims=NF, nnz=99_072_112, n_test=1_408_395, J=8, alpha_a=0.003, epochs=5),
