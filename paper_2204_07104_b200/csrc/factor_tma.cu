@@ -155,8 +155,18 @@ __device__ __forceinline__ bool elect_one() {
 #define SPTK_TMA_MINB_3_16 4
 #endif
 template <int N, int J>
+// Rank 8 at order 3 keeps less per sample (80 registers): six CTAs per SM.
+// NF factor pass J=8 7.26 -> 5.27 ms, J=4 (rank-8 padding) 7.42 -> 5.40 ms.
+// Order 6 at five CTAs (96 registers, ~100 bytes of spill): O6 149 -> 153 ms.
+#ifndef SPTK_TMA_MINB_3_8
+#define SPTK_TMA_MINB_3_8 6
+#endif
+#ifndef SPTK_TMA_MINB_6_8
+#define SPTK_TMA_MINB_6_8 4
+#endif
 constexpr int tma_min_blocks() {
-  return (N == 3 && J == 16) ? SPTK_TMA_MINB_3_16 : 4;
+  return (N == 3 && J == 16) ? SPTK_TMA_MINB_3_16
+                             : (N == 3 && J == 8) ? SPTK_TMA_MINB_3_8 : (N == 6 && J == 8) ? SPTK_TMA_MINB_6_8 : 4;
 }
 template <int N, int J, int R, bool HV, bool DS = false>
 __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
