@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsptk.so")
+# SPTK_LIB: an alternative in-tree build (experiment variants, e.g.
+# libsptk_<variant>.so next to the default)
+LIB_PATH = os.path.join(_HERE, os.environ.get("SPTK_LIB", "libsptk.so"))
 
 _c_i32p = ctypes.c_void_p
 _vp = ctypes.c_void_p

@@ -101,7 +101,9 @@ struct TmaCfg {
   static constexpr int OFF_BAR = (OFF_G + N * R * R + 1) & ~1;  // NSLOT + 1 mbarriers
   static constexpr int OFF_MISC = OFF_BAR + 2 * (NSLOT + 1);     // TMEM address, tile claim
   static constexpr int OFF_IDX = (OFF_MISC + 4 + 3) & ~3;         // [2][N][128] row indices (16-B aligned)
-  static constexpr int OFF_SPARE = (OFF_IDX + 2 * N * M + 255) & ~255;  // the spare slot, last (1024-B aligned)
+  static constexpr int RWC = N <= 3 ? 4 : (N <= 7 ? 8 : 16);     // record words
+  static constexpr int OFF_RING = OFF_IDX + 2 * N * M;            // [2][128][RWC] records in flight (cp.async)
+  static constexpr int OFF_SPARE = (OFF_RING + 2 * M * RWC + 255) & ~255;  // the spare slot, last (1024-B aligned)
   static constexpr size_t SMEM = (size_t)OFF_SPARE * 4 + 1024;          // + alignment slack
   static constexpr size_t SMEM_SPARE = SMEM + (size_t)SLOT * 4;
   // TMEM columns: the c round writes c_0..c_{N-1} at n*R; afterwards W at 0,
@@ -226,10 +228,6 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
   // of each warp reads four rows with one LDS.128 and issues the warp's eight
   // gather4 / scatter4 operations in a uniform loop.  Past-the-end samples
   // carry row 0 (gathered, never written back).
-  auto stage_ids = [&](const RecReg<N, RW>& rr, int par) {
-#pragma unroll
-    for (int n = 0; n < N; ++n) ids[(par * N + n) * 128 + tid] = rr.valid ? rr.idx[n] : 0;
-  };
   auto gather = [&](int n, int s, int par) {
     if (tid == 0) tc::mbar_expect_tx(&full[s], C::SLOT * 4);
     if (elect_one()) {
@@ -246,17 +244,47 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
   const long long G = gridDim.x;
   long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
   if (tid == 0) misc[1] = atomicAdd(tile_ctr, 1u);
-  RecReg<N, RW> cur, nxt;
+  // Records travel through a two-slot shared-memory ring (cp.async, issued
+  // two tiles ahead) instead of registers: a thread keeps only its current and
+  // next sample's value and validity; row indices are staged into ids[].
+  // 127 -> 120 registers; NF W=20 factor pass 7.38 -> 7.20 ms (five CTAs per
+  // SM at this size still spill ~56 bytes and ran slower: 7.58 ms).  The
+  // cp.async here carries no L2 cache-hint operand: with one (evict_first
+  // policy) the B200 raised "illegal instruction" on it.
+  int* ring = reinterpret_cast<int*>(sm + C::OFF_RING);
   // DS: padding entries (-1) are invalid samples that read record 0
-  auto lrec = [&](RecReg<N, RW>& o, int v, long long t) {
-    if (DS)
-      load_rec<N, RW>(o, rec, v < 0 ? 0 : v, tile_valid(n_visit, t) && v >= 0, base, pol_stream);
-    else
-      load_rec<N, RW>(o, rec, v, tile_valid(n_visit, t), base, pol_stream);
+  auto fetch = [&](int q, int v, long long t) -> bool {
+    bool ok = tile_valid(n_visit, t);
+    if (DS) {
+      ok = ok && v >= 0;
+      v = v < 0 ? 0 : v;
+    }
+    const int* src = rec + (base + (long long)v) * RW;
+    const uint32_t dst = tc::smem_u32(ring + (q * 128 + tid) * RW);
+    tc::cp_async16_nohint(dst, src, 16u);
+    if (RW >= 8) tc::cp_async16_nohint(dst + 16, src + 4, 16u);
+    tc::cp_async_commit();
+    return ok;
+  };
+  auto stage = [&](int q, bool ok, int par) -> float {
+    const int4* r = reinterpret_cast<const int4*>(ring + (q * 128 + tid) * RW);
+    int wv[8];
+    const int4 w0 = r[0];
+    wv[0] = w0.x, wv[1] = w0.y, wv[2] = w0.z, wv[3] = w0.w;
+    if (RW >= 8) {
+      const int4 w1 = r[1];
+      wv[4] = w1.x, wv[5] = w1.y, wv[6] = w1.z, wv[7] = w1.w;
+    }
+#pragma unroll
+    for (int n = 0; n < N; ++n) ids[(par * N + n) * 128 + tid] = ok ? wv[n] : 0;
+    return __int_as_float(wv[N]);
   };
   int v2 = load_vis<HV>(visit, n_visit, t2, pol_stream);
-  lrec(cur, load_vis<HV>(visit, n_visit, tile, pol_stream), tile);
-  lrec(nxt, load_vis<HV>(visit, n_visit, t1, pol_stream), t1);
+  bool ok_cur = fetch(0, load_vis<HV>(visit, n_visit, tile, pol_stream), tile);
+  bool ok_nxt = fetch(1, load_vis<HV>(visit, n_visit, t1, pol_stream), t1);
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  float x_cur = stage(0, ok_cur, 0), x_nxt = 0.f;
+  int rs = 1;  // ring slot of the next tile's record
   // DS round tracking: the round of this CTA's current tile (tiles only grow)
   int r_cur = 0, r_waited = 0, r_tiles = 0;
   auto adv = [&](int r, long long t) {
@@ -264,7 +292,6 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
     return r;
   };
   int pb = 0, par = 0;
-  stage_ids(cur, 0);
   __syncwarp();
 #pragma unroll
   for (int n = 0; n < N; ++n)
@@ -292,11 +319,13 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
 #pragma unroll
     for (int n = 0; n < N; ++n)
       if (!(early >> n & 1u)) gather(n, slot_of(n, pb), par);
-    // the next tile's indices, for its early gathers during this tile
-    stage_ids(nxt, par ^ 1);
-    RecReg<N, RW> nnxt;
-    lrec(nnxt, v2, t2);
+    // the record of the tile after next into the free ring slot; the next
+    // tile's (issued a tile ago) has landed: its indices for its early gathers
+    // during this tile
+    const bool ok_nn = fetch(rs ^ 1, v2, t2);
     v2 = load_vis<HV>(visit, n_visit, t3, pol_stream);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    x_nxt = stage(rs, ok_nxt, par ^ 1);
     const bool full_tile = (tile + 1) * 128 <= (DS ? dp.rend[r_cur] : n_visit);
     TMA_STAMP(1);
 #pragma unroll
@@ -394,7 +423,7 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
       for (int j = 0; j < J; ++j) inter = fmaf(a[j], g[j], inter);
       // a' = a - gamma (-x gs + lambda a + inter gs) = keep a + step gs
       const float gm = p.gam[n], lm = p.lam[n];
-      const float keep = 1.f - gm * lm, step = gm * (cur.x - inter), shrink = -gm * lm;
+      const float keep = 1.f - gm * lm, step = gm * (x_cur - inter), shrink = -gm * lm;
       const bool red = p.atomic_mask >> n & 1u;
       if (red || !full_tile) {
         // own row in natural order (it stays inside the row's swizzle span):
@@ -415,7 +444,7 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
           __syncwarp();
           constexpr int CH = J / 4, RPI = 32 / CH;
           const int cq = lane % CH, crow = lane / CH, wbase = tid & ~31;
-          const int me = cur.valid ? cur.idx[n] : -1;
+          const int me = ok_cur ? ids[(par * N + n) * 128 + tid] : -1;
           int row[CH];
           float4 v[CH];
 #pragma unroll
@@ -429,8 +458,8 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
         } else {
           // one bulk add-reduction (delta) or store (new row) per sample
           tc::fence_async_smem();
-          if (cur.valid) {
-            float* dst = fac + p.foff[n] + (long long)cur.idx[n] * J;
+          if (ok_cur) {
+            float* dst = fac + p.foff[n] + (long long)ids[(par * N + n) * 128 + tid] * J;
             const uint32_t src = slot_addr(slot_of(n, pb)) + tid * C::ROWB;
             if (red)
               tc::bulk_red_add(dst, src, C::ROWB);
@@ -469,8 +498,10 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
         for (int r = 0; r < R; ++r) c[n][r] = fmaf(step, h[r], keep * c[n][r]);
       }
     }
-    cur = nxt;
-    nxt = nnxt;
+    x_cur = x_nxt;
+    ok_cur = ok_nxt;
+    ok_nxt = ok_nn;
+    rs ^= 1;
     tile = t1;
     t1 = t2;
     t2 = t3;
@@ -520,6 +551,7 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
     t3 = 3 * G + misc[1];
     ++ntile;
   }
+  tc::cp_async_wait_all();
   tc::bulk_wait_all();
   tc::fence_before_sync();
   __syncthreads();
