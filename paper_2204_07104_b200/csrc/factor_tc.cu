@@ -983,7 +983,14 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
     p.prefetch = e ? atoi(e) : 1;
     // experiment hook (wrong results): drop the hot modes' row writes to
     // measure what their L2 contention costs
-    if (getenv("SPTK_DEBUG_DROP_HOT")) p.atomic_mask |= 0x80000000u;
+    if (getenv("SPTK_DEBUG_DROP_HOT")) {
+      static bool warned = false;
+      if (!warned) {
+        fprintf(stderr, "[sptk] SPTK_DEBUG_DROP_HOT: hot-mode row updates are dropped (timing experiment)\n");
+        warned = true;
+      }
+      p.atomic_mask |= 0x80000000u;
+    }
     const char* d = getenv("SPTK_TC_DEFER_WB");
     p.defer_wb = d ? atoi(d) : 0;
   }

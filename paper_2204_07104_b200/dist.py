@@ -193,6 +193,25 @@ class DsgdExchange:
                 v = self.rows_view(n, plan.held_blocks(q, r_last)[n])
                 v.copy_(g[q, self.pad_off[n]: self.pad_off[n] + v.numel()])
 
+    def allreduce_ordered(self, t) -> None:
+        """t <- t_0 + t_1 + ... + t_{W-1} added in rank order, on every rank:
+        the reference's merge of the chunk accumulators (trainer.py:238-240,
+        total = acc_0 + acc_1 + ...), so exact mode stays bitwise for any W
+        (an all-reduce may group the sums differently)."""
+        td = self.td
+        if self.nccl or t.device.type == "cpu":
+            parts = [self.torch.empty_like(t) for _ in range(self.world)]
+            td.all_gather(parts, t, group=self.group)
+        else:
+            h = t.cpu()
+            parts = [self.torch.empty_like(h) for _ in range(self.world)]
+            td.all_gather(parts, h, group=self.group)
+            parts = [p_.to(t.device) for p_ in parts]
+        total = parts[0].clone()
+        for q in range(1, self.world):
+            total += parts[q]
+        t.copy_(total)
+
     def allreduce(self, t) -> None:
         if self.nccl or t.device.type == "cpu":
             self.td.all_reduce(t, group=self.group)
@@ -234,7 +253,10 @@ class DistRunner(EpochRunner):
         return ids, hi - lo, (1 if self.mode == 1 else 0)
 
     def reduce_core_acc(self):
-        self.ex.allreduce(self.acc)
+        if self.mode == 1:
+            self.ex.allreduce_ordered(self.acc)  # exact: the reference's chunk order
+        else:
+            self.ex.allreduce(self.acc)
 
 
 def train_distributed(model, split, config):

@@ -352,6 +352,9 @@ class EpochRunner:
         # sampler stage's previous output instead of drawing it again, to measure
         # what that stage's co-running costs the epoch
         self._skip = set(filter(None, os.environ.get("SPTK_EXP_SKIP", "").split(",")))
+        if self._skip:
+            warnings.warn(f"SPTK_EXP_SKIP={sorted(self._skip)}: sampler stages re-use stale samples "
+                          "(timing experiment; results are not the reference's)", stacklevel=2)
 
     @property
     def rounds(self):
