@@ -53,10 +53,11 @@ CONFIGS = {
     # tensors; 0.003 (NF) and 0.001 (Y4, and J = R >= 32) are the largest
     # rates at which the reference's own train() converges (oracle runs on
     # 2M-4M prefixes of the same tensors; at 0.003 Y4 goes to NaN).
-    # workers: Y4 16 (44.2 ms vs 62.5 at W=1), O6 8 (149 ms vs 230), same test RMSE
+    # workers: Y4 12 (W = 1/10/12/16/24: 62.5/44.0/41.6/42.4/49.5 ms), O6 8
+    # (W = 1/6/8/10: 230/132/129/139 ms), same test RMSE
     "y4": dict(workload="yahoo-shaped 1000990x624961x3075x133, 250,272,286 nnz, J=R=16",
                dims=(1_000_990, 624_961, 3_075, 133), nnz=250_272_286, n_test=2_502_723, J=16, R=16,
-               alpha_a=0.001, workers=16),
+               alpha_a=0.001, workers=12),
     "o6": dict(workload="6-order 10K^6, 1e9 nnz, J=R=8",
                dims=(10_000,) * 6, nnz=1_000_000_000, n_test=1_000_000, J=8, R=8, alpha_a=0.001, workers=8),
 }

@@ -48,6 +48,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -110,9 +115,14 @@ __global__ void __launch_bounds__(128) factor_dep_kernel(const int* __restrict__
     // wait for the predecessors: lane n < N polls mode n's (one round trip
     // per poll for all modes together)
     {
+      // relaxed polls (an acquire load invalidates the SM's L1 on every poll:
+      // ncu showed 38% of the stall samples on that CCTL.IVALL), then one
+      // acquire once every predecessor is seen done
       const int p = lane < N ? __ldg(pred + (long long)lane * nv + k) : -1;
-      while (!__all_sync(0xffffffffu, p < 0 || ld_acquire(flags + p) != 0)) {
+      while (!__all_sync(0xffffffffu, p < 0 || ld_relaxed(flags + p) != 0)) {
       }
+      if (p >= 0) (void)ld_acquire(flags + p);
+      __syncwarp();
     }
     for (int n = 0; n < N; ++n) {
       const int J = md.jr[n];

@@ -84,6 +84,11 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed_sys(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -305,7 +310,8 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
       r_cur = adv(r_cur, tile);
       if (r_cur > r_waited) {
         if (tid == 0) {
-          while (ld_acquire_sys(dp.ready) < dp.gen0 + r_cur) __nanosleep(64);
+          while (ld_relaxed_sys(dp.ready) < dp.gen0 + r_cur) __nanosleep(64);
+          (void)ld_acquire_sys(dp.ready);
           fence_proxy_async_global();
         }
         __syncthreads();
@@ -529,7 +535,8 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
           // the receiver must be past the previous epoch's block exchange,
           // which rewrites its replica (else this block would be overwritten)
           if (tid == 0)
-            while (ld_acquire_sys(ps.dst_gathered) < dp.epoch) __nanosleep(64);
+            while (ld_relaxed_sys(ps.dst_gathered) < dp.epoch) __nanosleep(64);
+          if (tid == 0) (void)ld_acquire_sys(ps.dst_gathered);
           __syncthreads();
           const long long nf4 = ps.nrows * J / 4;
           const float4* src = reinterpret_cast<const float4*>(fac + p.foff[ps.mode] + ps.row_lo * J);
