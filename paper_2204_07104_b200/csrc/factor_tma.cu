@@ -164,12 +164,13 @@ __device__ __forceinline__ bool elect_one() {
 template <int N, int J>
 // Rank 8 at order 3 keeps less per sample (80 registers): six CTAs per SM.
 // NF factor pass J=8 7.26 -> 5.27 ms, J=4 (rank-8 padding) 7.42 -> 5.40 ms.
-// Order 6 at five CTAs (96 registers, ~100 bytes of spill): O6 149 -> 153 ms.
+// Order 6 at five CTAs (96 registers): with the record ring ~40 bytes of
+// spill, O6 epoch 129.7 -> 121.0 ms (before the ring: ~100 bytes, 149 -> 153).
 #ifndef SPTK_TMA_MINB_3_8
 #define SPTK_TMA_MINB_3_8 6
 #endif
 #ifndef SPTK_TMA_MINB_6_8
-#define SPTK_TMA_MINB_6_8 4
+#define SPTK_TMA_MINB_6_8 5
 #endif
 constexpr int tma_min_blocks() {
   return (N == 3 && J == 16) ? SPTK_TMA_MINB_3_16
