@@ -570,6 +570,340 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
 }
 #undef TMA_STAMP
 
+// ---------------------------------------------------------------------------
+// v7: the v6 pipeline for J = R = 32 with two threads per sample.  256 threads
+// own one 128-sample tile: warp w reads TMEM lane quadrant w % 4 (samples
+// 32 (w % 4) .. +31) and owns column half h = w / 4 of every J- and R-vector,
+// so a thread keeps c_n for 16 columns (48 registers, as v6 at J = 16).  Rows
+// arrive by TMA gather4 into 128-byte-swizzled operand tiles; W_n goes to
+// TMEM (each half its 16 columns) as the MMA's A operand; inter = a . gs is
+// the current prediction sum_r W_n[r] c_n[r], whose halves are exchanged
+// across the barrier that already precedes the MMA (as in v3).  The two warps
+// of a lane quadrant meet at a named barrier before a cold mode's rows are
+// scattered back (each wrote half of every row).  Records come through the
+// shared-memory ring (warps 0-3 fetch and stage them).
+// ---------------------------------------------------------------------------
+template <int N, int J, int R>
+struct Tma2Cfg {
+  static constexpr int M = 128, H = J / 2;
+  static constexpr int ROWB = J * 4;
+  static constexpr int SLOT = M * J;
+  static constexpr int RWC = N <= 3 ? 4 : (N <= 7 ? 8 : 16);
+  static constexpr int OFF_A = 0;                               // N slots, 1024-B aligned
+  static constexpr int OFF_BT = OFF_A + N * SLOT;
+  static constexpr int OFF_BN = OFF_BT + N * R * J;
+  static constexpr int OFF_G = OFF_BN + N * J * R;
+  static constexpr int OFF_BAR = (OFF_G + N * R * R + 1) & ~1;  // N + 1 mbarriers
+  static constexpr int OFF_MISC = OFF_BAR + 2 * (N + 1);
+  static constexpr int OFF_IDX = (OFF_MISC + 4 + 3) & ~3;       // [2][N][128]
+  static constexpr int OFF_X = OFF_IDX + 2 * N * M;             // [2][128] values
+  static constexpr int OFF_PX = OFF_X + 2 * M;                  // [2 parity][2 halves][128]
+  static constexpr int OFF_RING = (OFF_PX + 4 * M + 3) & ~3;    // [2][128][RWC]
+  static constexpr int FLOATS = OFF_RING + 2 * M * RWC;
+  static constexpr size_t SMEM = (size_t)FLOATS * 4 + 1024;
+  static constexpr int COL_W = 0, COL_G = R, COL_H = R + J;
+  static constexpr int NEED = (N * R > 2 * R + J) ? N * R : 2 * R + J;
+  static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : 256;
+};
+
+template <int N, int J, int R, bool HV>
+__global__ void __launch_bounds__(256, 2)
+    factor_tma2_kernel(const int* __restrict__ rec, const int* __restrict__ visit, long long n_visit, long long base,
+                       float* __restrict__ fac, const float* __restrict__ cor, const __grid_constant__ TmaParams<N> p,
+                       const __grid_constant__ TmaMaps<N> maps, unsigned* __restrict__ tile_ctr) {
+  static_assert(J == R && J == 32, "v7 is the J = R = 32 kernel");
+  constexpr int RW = N <= 3 ? 4 : (N <= 7 ? 8 : 16);
+  using C = Tma2Cfg<N, J, R>;
+  constexpr int H = C::H;
+  extern __shared__ __align__(16) float sm_raw[];
+  float* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u) / 4;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* mbar = full + N;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::OFF_MISC);
+  int* ids = reinterpret_cast<int*>(sm + C::OFF_IDX);
+  float* xs = sm + C::OFF_X;
+  float* px = sm + C::OFF_PX;
+  int* ring = reinterpret_cast<int*>(sm + C::OFF_RING);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int qd = warp & 3, hf = warp >> 2, smp = 32 * qd + (tid & 31), c0 = hf * H;
+
+  for (int e = tid; e < N * J * R; e += 256) {
+    const int n = e / (J * R), rem = e - n * (J * R), j = rem / R, r = rem - j * R;
+    const float b = __ldg(cor + e);
+    sm[C::OFF_BT + n * R * J + canon<R>(r, j)] = b;
+    sm[C::OFF_BN + n * J * R + canon<J>(j, r)] = b;
+  }
+  for (int e = tid; e < N * R * R; e += 256) {
+    const int n = e / (R * R), rem = e - n * (R * R), r = rem / R, r2 = rem - r * R;
+    float g = 0.f;
+    for (int j = 0; j < J; ++j) g = fmaf(__ldg(cor + n * J * R + j * R + r), __ldg(cor + n * J * R + j * R + r2), g);
+    sm[C::OFF_G + n * R * R + canon<R>(r, r2)] = g;
+  }
+  if (tid == 0) {
+    for (int q = 0; q <= N; ++q) tc::mbar_init(&full[q], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&misc[0], C::TCOLS);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = misc[0];
+  const uint32_t tlane = tbase + ((uint32_t)(qd * 32) << 16);
+  const uint32_t sbase = tc::smem_u32(sm);
+  const uint32_t id_c = tc::idesc_tf32(128, R), id_g = tc::idesc_tf32(128, J), id_h = tc::idesc_tf32(128, R);
+  const uint64_t pol_stream = tc::policy_evict_first();
+  uint32_t mphase = 0, fphase = 0;
+  const unsigned early = p.early_mask;
+  auto slot_addr = [&](int q) { return sbase + 4u * (uint32_t)(C::OFF_A + q * C::SLOT); };
+
+  // warps 0-3 gather their quadrant's 32 rows (8 gather4 by one lane)
+  auto gather = [&](int n, int par) {
+    if (tid == 0) tc::mbar_expect_tx(&full[n], C::SLOT * 4);
+    if (hf == 0 && elect_one()) {
+      const int4* id4 = reinterpret_cast<const int4*>(ids + (par * N + n) * 128 + qd * 32);
+      const uint32_t dst = slot_addr(n) + qd * 32 * C::ROWB, bar = tc::smem_u32(&full[n]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int4 r = id4[k];
+        tc::tma_gather4(dst + 4 * k * C::ROWB, &maps.m[n], r.x, r.y, r.z, r.w, bar);
+      }
+    }
+  };
+  // records: warps 0-3 fetch (cp.async) and stage them (indices, value)
+  auto fetch = [&](int q, int v, long long t) {
+    if (hf == 0) {
+      const int* src = rec + (base + (long long)v) * RW;
+      const uint32_t dst = tc::smem_u32(ring + (q * 128 + smp) * RW);
+      tc::cp_async16_nohint(dst, src, 16u);
+      if (RW >= 8) tc::cp_async16_nohint(dst + 16, src + 4, 16u);
+      tc::cp_async_commit();
+    }
+    (void)t;
+  };
+  auto stage = [&](int q, long long t, int par) {
+    if (hf == 0) {
+      const bool ok = tile_valid(n_visit, t) ;
+      const int4* rr = reinterpret_cast<const int4*>(ring + (q * 128 + smp) * RW);
+      int wv[8];
+      const int4 w0 = rr[0];
+      wv[0] = w0.x, wv[1] = w0.y, wv[2] = w0.z, wv[3] = w0.w;
+      if (RW >= 8) {
+        const int4 w1 = rr[1];
+        wv[4] = w1.x, wv[5] = w1.y, wv[6] = w1.z, wv[7] = w1.w;
+      }
+#pragma unroll
+      for (int n = 0; n < N; ++n) ids[(par * N + n) * 128 + smp] = ok ? wv[n] : 0;
+      xs[par * 128 + smp] = __int_as_float(wv[N]);
+    }
+  };
+  // valid(t) for this thread's sample (threads of both halves)
+  auto valid_of = [&](long long t) { return t * 128 + smp < n_visit; };
+
+  const long long G = gridDim.x;
+  long long tile = blockIdx.x, t1 = tile + G, t2 = tile + 2 * G;
+  if (tid == 0) misc[1] = atomicAdd(tile_ctr, 1u);
+  int v2 = 0;
+  {
+    // sample smp of a tile (both halves compute the same visit entries;
+    // only warps 0-3 use them)
+    const long long k0 = tile * 128 + smp, k1 = t1 * 128 + smp, k2 = t2 * 128 + smp;
+    auto vis = [&](long long k) -> int {
+      k = k < n_visit ? k : n_visit - 1;
+      return HV ? tc::ld_stream_s32(visit + k, pol_stream) : (int)k;
+    };
+    fetch(0, vis(k0), tile);
+    fetch(1, vis(k1), t1);
+    v2 = vis(k2);
+  }
+  if (hf == 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
+  stage(0, tile, 0);
+  int rs = 1;
+  int par = 0;
+  __syncthreads();
+#pragma unroll
+  for (int n = 0; n < N; ++n)
+    if (early >> n & 1u) gather(n, 0);
+  long long t3 = 3 * G + misc[1];
+  __syncthreads();
+  while (tile * 128 < n_visit) {
+    unsigned claim = 0;
+    if (tid == 0) claim = atomicAdd(tile_ctr, 1u);
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+      if (!(early >> n & 1u)) gather(n, par);
+    fetch(rs ^ 1, v2, t2);
+    {
+      long long k3 = t3 * 128 + smp;
+      k3 = k3 < n_visit ? k3 : n_visit - 1;
+      v2 = HV ? tc::ld_stream_s32(visit + k3, pol_stream) : (int)k3;
+    }
+    if (hf == 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    stage(rs, t1, par ^ 1);
+    const bool full_tile = (tile + 1) * 128 <= n_visit;
+    const bool ok = valid_of(tile);
+    const float x = xs[par * 128 + smp];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      tc::mbar_wait(&full[n], (fphase >> n) & 1u);
+      fphase ^= 1u << n;
+    }
+    if (tid == 0) {
+      tc::fence_after_sync();
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const uint32_t a = slot_addr(n);
+        const uint32_t b = sbase + 4u * (C::OFF_BT + n * R * J);
+#pragma unroll
+        for (int kk = 0; kk < J / 8; ++kk)
+          tc::mma_tf32(tbase + n * R, tc::smem_desc_sw<C::ROWB>(a + 32 * kk),
+                       tc::smem_desc(b + kk * 2 * (R * 16), R * 16, 128), id_c, kk > 0 ? 1u : 0u);
+      }
+      tc::mma_commit(mbar);
+    }
+    tc::mbar_wait(mbar, mphase);
+    mphase ^= 1;
+    tc::fence_after_sync();
+    float c[N][H];
+#pragma unroll
+    for (int n = 0; n < N; ++n) tc::tmem_ldh<H>(tlane + n * R + c0, c[n]);
+
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      float part = 0.f;
+      {
+        float w[H];
+#pragma unroll
+        for (int r = 0; r < H; ++r) {
+          float v = 0.f;
+          bool first = true;
+#pragma unroll
+          for (int n0 = 0; n0 < N; ++n0)
+            if (n0 != n) {
+              v = first ? c[n0][r] : v * c[n0][r];
+              first = false;
+            }
+          w[r] = v;
+          part = fmaf(v, c[n][r], part);
+        }
+        tc::tmem_st16(tlane + C::COL_W + c0, w);
+      }
+      px[((n & 1) * 2 + hf) * 128 + smp] = part;
+      tc::tmem_wait_st();
+      tc::bulk_wait_read();
+      tc::fence_before_sync();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t bn = sbase + 4u * (C::OFF_BN + n * J * R);
+#pragma unroll
+        for (int kk = 0; kk < R / 8; ++kk)
+          tc::mma_tf32_ts(tbase + C::COL_G, tbase + C::COL_W + 8 * kk,
+                          tc::smem_desc(bn + kk * 2 * (J * 16), J * 16, 128), id_g, kk > 0 ? 1u : 0u);
+        if (n < N - 1) {
+          const uint32_t gg = sbase + 4u * (C::OFF_G + n * R * R);
+#pragma unroll
+          for (int kk = 0; kk < R / 8; ++kk)
+            tc::mma_tf32_ts(tbase + C::COL_H, tbase + C::COL_W + 8 * kk,
+                            tc::smem_desc(gg + kk * 2 * (R * 16), R * 16, 128), id_h, kk > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(mbar);
+      }
+      if (n >= 1 && (early >> (n - 1) & 1u)) gather(n - 1, par ^ 1);
+      const float inter = part + px[((n & 1) * 2 + (hf ^ 1)) * 128 + smp];
+      tc::mbar_wait(mbar, mphase);
+      mphase ^= 1;
+      tc::fence_after_sync();
+      float g[H];
+      tc::tmem_ldh<H>(tlane + C::COL_G + c0, g);
+      float* slot = sm + C::OFF_A + n * C::SLOT;
+      float a[H];
+#pragma unroll
+      for (int q = 0; q < H / 4; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(slot + swz<J>(smp, c0 / 4 + q));
+        a[4 * q] = v.x;
+        a[4 * q + 1] = v.y;
+        a[4 * q + 2] = v.z;
+        a[4 * q + 3] = v.w;
+      }
+      const float gm = p.gam[n], lm = p.lam[n];
+      const float keep = 1.f - gm * lm, step = gm * (x - inter), shrink = -gm * lm;
+      const bool red = p.atomic_mask >> n & 1u;
+      if (red) {
+        // hot mode: this thread's half of the delta, four add-reductions
+        if (ok) {
+          float* dst = fac + p.foff[n] + (long long)ids[(par * N + n) * 128 + smp] * J + c0;
+#pragma unroll
+          for (int q = 0; q < H / 4; ++q)
+            tc::red_add_v4(dst + 4 * q, make_float4(fmaf(step, g[4 * q], shrink * a[4 * q]),
+                                                     fmaf(step, g[4 * q + 1], shrink * a[4 * q + 1]),
+                                                     fmaf(step, g[4 * q + 2], shrink * a[4 * q + 2]),
+                                                     fmaf(step, g[4 * q + 3], shrink * a[4 * q + 3])));
+        }
+      } else {
+        // cold mode: the new half-row in place (swizzled), the quadrant's two
+        // warps meet, then one lane scatters the 32 rows (or, in a partial
+        // tile, each valid sample's row goes out as one bulk store)
+#pragma unroll
+        for (int q = 0; q < H / 4; ++q) {
+          float v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = fmaf(step, g[4 * q + u], keep * a[4 * q + u]);
+          *reinterpret_cast<float4*>(slot + swz<J>(smp, c0 / 4 + q)) = make_float4(v[0], v[1], v[2], v[3]);
+        }
+        tc::fence_async_smem();
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + qd) : "memory");
+        if (hf == 0) {
+          if (full_tile) {
+            if (elect_one()) {
+              const int4* id4 = reinterpret_cast<const int4*>(ids + (par * N + n) * 128 + qd * 32);
+              const uint32_t src = slot_addr(n) + qd * 32 * C::ROWB;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int4 r = id4[k];
+                tc::tma_scatter4(&maps.m[n], r.x, r.y, r.z, r.w, src + 4 * k * C::ROWB);
+              }
+              tc::bulk_commit();
+            }
+          } else if (ok) {
+            // swizzled row -> natural order is a permutation of its 16-byte
+            // chunks: one 16-byte bulk store per chunk
+            float* dst = fac + p.foff[n] + (long long)ids[(par * N + n) * 128 + smp] * J;
+#pragma unroll
+            for (int q = 0; q < J / 4; ++q)
+              tc::bulk_store(dst + 4 * q, slot_addr(n) + 4u * (uint32_t)swz<J>(smp, q), 16);
+            tc::bulk_commit();
+          }
+        }
+      }
+      if (n < N - 1) {
+        float h[H];
+        tc::tmem_ldh<H>(tlane + C::COL_H + c0, h);
+#pragma unroll
+        for (int r = 0; r < H; ++r) c[n][r] = fmaf(step, h[r], keep * c[n][r]);
+      }
+    }
+    tile = t1;
+    t1 = t2;
+    t2 = t3;
+    par ^= 1;
+    rs ^= 1;
+    if (tid == 0) misc[1] = claim;
+    tc::bulk_wait_read();
+    tc::fence_before_sync();
+    __syncthreads();
+    t3 = 3 * G + misc[1];
+  }
+  tc::cp_async_wait_all();
+  tc::bulk_wait_all();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tbase, C::TCOLS);
+  }
+}
+
 // ---------------------------------------------------------------- host side --
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -695,6 +1029,62 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
   return 0;
 }
 
+template <int N, int J, int R>
+static int launch_tma2(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
+                       const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s) {
+  using C = Tma2Cfg<N, J, R>;
+  if (encode_fn()) return 1;
+  (void)rw;
+  TmaParams<N> p;
+  for (int n = 0; n < N; ++n) {
+    p.foff[n] = md.foff[n];
+    p.gam[n] = gam[n];
+    p.lam[n] = lam[n];
+  }
+  p.dbg = nullptr;
+  p.atomic_mask = hot_mode_mask(md);
+  p.early_mask = ~p.atomic_mask & ((1u << N) - 1u) & ~(1u << (N - 1));  // no spare slot: the last mode is late
+  p.bulk_red = 0;
+  static TmaMaps<N> maps;
+  static const float* maps_fac = nullptr;
+  static long long maps_foff[N];
+  bool same = maps_fac == fac;
+  for (int n = 0; n < N && same; ++n) same = maps_foff[n] == md.foff[n];
+  if (!same) {
+    for (int n = 0; n < N; ++n) {
+      const long long end = n + 1 < N ? md.foff[n + 1] : md.fac_size;
+      if (encode_row_map(&maps.m[n], fac + md.foff[n], (end - md.foff[n]) / J, J)) return 1;
+      maps_foff[n] = md.foff[n];
+    }
+    maps_fac = fac;
+  }
+  auto kfn = visit ? factor_tma2_kernel<N, J, R, true> : factor_tma2_kernel<N, J, R, false>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    for (auto f : {factor_tma2_kernel<N, J, R, true>, factor_tma2_kernel<N, J, R, false>}) {
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SPTK_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    SPTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, C::SMEM));
+    if (per_sm < 1) per_sm = 1;
+    if (getenv("SPTK_DEBUG")) fprintf(stderr, "[sptk] tma2 kernel smem=%zu -> %d CTAs/SM\n", C::SMEM, per_sm);
+  }
+  const long long tiles = (n_visit + 127) / 128;
+  long long blocks = 148LL * per_sm;
+  if (const char* e = getenv("SPTK_TC_GRID")) blocks = atoll(e);
+  if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
+  if (blocks < 1) blocks = 1;
+  if (blocks > tiles) blocks = tiles;
+  unsigned* ctr = nullptr;
+  SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tma_tile_ctr));
+  ctr += g_tma_ctr_slot.fetch_add(1u) & 63u;
+  SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+  kfn<<<(unsigned)blocks, 256, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, maps, ctr);
+  SPTK_CHECK_LAUNCH();
+  note_factor_kernel("factor_tma2_kernel");
+  return 0;
+}
+
 // returns 1 if handled (uniform J = R in {8, 16}; N = 3, 4 at J = 16; N = 3, 6 at J = 8)
 int try_factor_tma(const int* rec, int rw, const int* visit, long long n_visit, long long base, float* fac,
                    const float* cor, const ModelDesc& md, const float* gam, const float* lam, cudaStream_t s, int* rc) {
@@ -702,6 +1092,15 @@ int try_factor_tma(const int* rec, int rw, const int* visit, long long n_visit, 
   for (int n = 0; n < N; ++n)
     if (md.jr[n] != J) return 0;
   if (J != R || rw != rec_words(N)) return 0;
+  static int tma2 = -1;
+  if (tma2 < 0) {
+    const char* e = getenv("SPTK_TMA2");
+    tma2 = e ? atoi(e) : 0;
+  }
+  if (tma2 && N == 3 && J == 32) {
+    *rc = launch_tma2<3, 32, 32>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);
+    return 1;
+  }
 #define SPTK_TMA_CASE(NN, JJ)                                                                    \
   if (N == NN && J == JJ) {                                                                      \
     *rc = launch_tma<NN, JJ, JJ>(rec, rw, visit, n_visit, base, fac, cor, md, gam, lam, s);      \
