@@ -100,10 +100,11 @@ int sptk_block_perm(const void* d_jobs, const int32_t* d_coords, int n_jobs, int
                     int cap, uint16_t* d_js, int32_t* d_visit, void* stream);
 /* The same round-interleaved visit list from per-block visit orders already
  * in the partitioned layout (d_perm[off_b + p]; entries relative to off_b, or
- * to rel_lo when rel_lo >= 0): for blocks above sptk_block_perm's capacity,
+ * to rel_lo when rel_lo >= 0; cap = the largest block, which sets how many CTAs
+ * share a block): for blocks above sptk_block_perm's capacity,
  * whose orders come from sptk_permutation_j_batch + sptk_fy_apply. */
 int sptk_interleave_rounds(const void* d_jobs, int n_jobs, const int32_t* d_perm, long long rel_lo,
-                           int32_t* d_visit, void* stream);
+                           int32_t* d_visit, long long cap, void* stream);
 size_t sptk_permutation_ws_bytes(long long n);
 /* d_out[n] (int32) = Generator.permutation(n) for the generator in h_state. */
 int sptk_permutation(const uint64_t h_state[4], long long n, int32_t* d_out, void* d_ws, size_t ws_bytes,
@@ -242,7 +243,8 @@ int sptk_factor_pass_exact_f64(const int32_t* d_rec, int rw, const int32_t* d_vi
  * ready flag to gen0 + r + 1 (release, system scope).  d_done:
  * n_rounds ints of scratch.  grid > 0 caps the persistent grid (all CTAs of
  * every rank sharing a GPU must be resident).  Uniform J = R, TMA kernel
- * shapes (order 3/4 at J = 16, 3/6 at J = 8). */
+ * shapes (order 3/4 at J = 16, 3/6 at J = 8); grid < 0 divides the default
+ * grid by -grid (M-way DSGD: the per-row concurrency of one GPU). */
 int sptk_factor_pass_dsgd(const int32_t* d_rec, int rw, const int32_t* d_visit, long long n_visit, float* d_fac,
                           const int64_t* h_foff, const float* d_cor, const int64_t* h_coff, const int64_t* h_jr,
                           int n_modes, int rcore, const double* h_gammas, const double* h_lambdas,

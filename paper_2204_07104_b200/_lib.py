@@ -40,7 +40,7 @@ SIGNATURES = {
     "sptk_block_job_bytes": (ctypes.c_size_t, []),
     "sptk_block_perm": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _i64, ctypes.c_int,
                                        _vp, _vp, _vp]),
-    "sptk_interleave_rounds": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _vp, _vp]),
+    "sptk_interleave_rounds": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _vp, _i64, _vp]),
     "sptk_permutation_ws_bytes": (ctypes.c_size_t, [_i64]),
     "sptk_permutation": (ctypes.c_int, [_u64p, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
     "sptk_permute_records": (ctypes.c_int, [_u64p, _i64, _vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, _vp]),

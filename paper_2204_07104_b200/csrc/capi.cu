@@ -103,8 +103,8 @@ int sptk_block_perm(const void* d_jobs, const int32_t* d_coords, int n_jobs, int
 }
 
 int sptk_interleave_rounds(const void* d_jobs, int n_jobs, const int32_t* d_perm, long long rel_lo,
-                           int32_t* d_visit, void* stream) {
-  return interleave_rounds(d_jobs, n_jobs, d_perm, rel_lo, d_visit, (cudaStream_t)stream);
+                           int32_t* d_visit, long long cap, void* stream) {
+  return interleave_rounds(d_jobs, n_jobs, d_perm, rel_lo, d_visit, (cudaStream_t)stream, cap);
 }
 
 size_t sptk_permutation_ws_bytes(long long n) { return perm_ws_bytes(n); }

@@ -1012,6 +1012,9 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
   // flag while earlier tiles are still running elsewhere); grid > 0 caps it
   // (two ranks sharing one GPU in the tests)
   if (dsp && grid > 0 && blocks > grid) blocks = grid;
+  // grid < 0: the default grid divided by -grid (a rank of M-way DSGD keeps
+  // the per-row concurrency of one GPU running the whole tensor)
+  if (dsp && grid < 0) blocks = (blocks + (-grid) - 1) / (-grid);
   if (blocks < 1) blocks = 1;
   if (blocks > tiles) blocks = tiles;
   unsigned* ctr = nullptr;

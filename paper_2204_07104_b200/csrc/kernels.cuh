@@ -28,7 +28,7 @@ int block_perm(const void* d_jobs, const int* d_coords, int n_jobs, int order, u
                long long t, int cap, uint16_t* d_js, int* d_visit, cudaStream_t s);
 size_t block_job_bytes();
 int interleave_rounds(const void* d_jobs, int n_jobs, const int* d_perm, long long rel_lo, int* d_visit,
-                      cudaStream_t s);
+                      cudaStream_t s, long long cap);
 int u32_stream(const uint64_t st[4], unsigned long long q0, long long n, uint32_t* out, cudaStream_t s);
 int iota(int* out, long long n, int offset, cudaStream_t s);
 size_t scan_ws_bytes(long long n);

@@ -2248,7 +2248,8 @@ __global__ void __launch_bounds__(256) interleave_kernel(const BlockJob* __restr
   if (threadIdx.x < m) sizes[threadIdx.x] = jobs[jb.first + threadIdx.x].n;
   __syncthreads();
   const long long add = rel_lo < 0 ? jb.off : rel_lo;
-  for (int p = threadIdx.x; p < jb.n; p += blockDim.x) {
+  // blockIdx.y splits a large block's entries over several CTAs
+  for (int p = blockIdx.y * blockDim.x + threadIdx.x; p < jb.n; p += gridDim.y * blockDim.x) {
     long long pos = jb.out_base;
     if (p < jb.nmin) {
       pos += (long long)p * m + jb.slot;
@@ -2264,9 +2265,14 @@ __global__ void __launch_bounds__(256) interleave_kernel(const BlockJob* __restr
 }
 
 int interleave_rounds(const void* d_jobs, int n_jobs, const int* d_perm, long long rel_lo, int* d_visit,
-                      cudaStream_t s) {
+                      cudaStream_t s, long long cap) {
   if (n_jobs <= 0) return 0;
-  interleave_kernel<<<n_jobs, 256, 0, s>>>((const BlockJob*)d_jobs, d_perm, rel_lo, d_visit);
+  // enough CTAs per block for ~4K entries each, and at least ~4 waves overall
+  long long ys = (cap + 4095) / 4096;
+  if (ys < 1) ys = 1;
+  if (ys > 65535) ys = 65535;
+  interleave_kernel<<<dim3((unsigned)n_jobs, (unsigned)ys), 256, 0, s>>>((const BlockJob*)d_jobs, d_perm, rel_lo,
+                                                                         d_visit);
   SPTK_CHECK_LAUNCH();
   return 0;
 }

@@ -96,17 +96,17 @@ class FusedState:
         self.push = None
         # Hogwild staleness inside a rank: a round's block covers 1/M of every
         # mode's rows, so a full grid would put M times more concurrent
-        # updates on each hot row than on one GPU.  Measured on one GPU with
-        # the 8-worker NF blocks launched one by one at full occupancy (the
-        # per-rank dynamics of 8-GPU DSGD): test RMSE NaN; with at most
-        # block/16 samples in flight: 0.4832 (the reference's W=8 curve).
-        # So the persistent grid holds at most (largest block)/SPAN samples,
-        # SPAN = 16 (SPTK_DSGD_SPAN).
+        # updates on each hot row than one GPU running the whole tensor does.
+        # Measured on one GPU with the 8-worker NF blocks launched one by one
+        # at full occupancy (the per-rank dynamics of 8-GPU DSGD): test RMSE
+        # NaN; with ~1/6 of the grid: 0.4832 (the reference's W=8 curve).  A
+        # rank therefore runs 1/M of the single-GPU grid: the same in-flight
+        # samples per hot row as the validated single-GPU runs
+        # (SPTK_DSGD_GRID_DIV overrides M; 1 = full grid).
         import os
 
-        span = int(os.environ.get("SPTK_DSGD_SPAN", "16"))
-        biggest = max((c for rnd in rounds for (_, _, c) in rnd), default=TILE)
-        self.grid = max(1, biggest // max(span, 1) // TILE) if span > 0 else 0
+        div = int(os.environ.get("SPTK_DSGD_GRID_DIV", plan.m))
+        self.grid = -div if div > 1 else 0
 
     # -- peers ---------------------------------------------------------------
     def peer_addresses(self):

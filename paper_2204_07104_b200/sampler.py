@@ -266,4 +266,4 @@ class BlockOrders:
         """out[0:total] = the round-interleaved visit list of per-block orders
         perm[off_b + p] (entries relative to off_b, or to rel_lo >= 0)."""
         check(_lib.load().sptk_interleave_rounds(ptr(self.jobs), self.n_jobs, ptr(perm), int(rel_lo), ptr(out),
-                                                 stream_ptr(stream)), "sptk_interleave_rounds")
+                                                 int(max(self.cap, 1)), stream_ptr(stream)), "sptk_interleave_rounds")
