@@ -1,9 +1,9 @@
 #!/bin/bash
-# Final round record: full GPU suite + smoke, headline bench (e2e + cpu leg), reference arm,
-# timeline, launch list, ncu --set full of the factor kernel, every config's line.
-O=gpurun_out/final2; mkdir -p $O
+# Final round record (record ring + W=20): full GPU suite + smoke, headline bench (e2e + cpu leg),
+# reference arm, timeline, launch list, ncu --set full of the factor kernel, every config's line.
+O=gpurun_out/round; mkdir -p $O
 nvidia-smi > $O/nvsmi.txt 2>&1
-timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rxXf > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+timeout 2700 python -m pytest tests -m gpu -q -p no:cacheprovider -rxXf > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/ref.json 2> $O/ref.err
@@ -19,6 +19,6 @@ done
 timeout 900 python bench.py --config y4 --no-cpu-baseline --no-e2e --steps 5 > $O/y4.json 2> $O/y4.err
 timeout 900 python bench.py --config cfg1 --no-cpu-baseline --no-e2e --steps 5 > $O/cfg1.json 2> $O/cfg1.err
 timeout 1500 python bench.py --config o6 --no-cpu-baseline --no-e2e --steps 3 > $O/o6.json 2> $O/o6.err
-for m in 2 4 8; do
+for m in 4 8; do
   BENCH_DSGD_SIM=$m timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 10 > $O/sim$m.json 2> $O/sim$m.err
 done
