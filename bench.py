@@ -40,14 +40,13 @@ METRIC = "sampled nonzeros/sec per SGD epoch (A+B update) at 1/2/4/8 B200; test 
 
 CONFIGS = {
     # workers: the reference's TrainConfig.workers (DSGD blocks per mode).
-    # NF runs its DSGD schedule with 24 blocks per mode on the one GPU: its
-    # ~7,200-entry block permutations fit beside three factor CTAs per SM and
-    # run hidden under the factor pass (9.47 ms; W = 22 / 26: 9.8-9.9 / 9.6-9.7;
-    # with four factor CTAs per SM the best was W = 20 at 9.62; W=1: 14.8;
-    # profiles/r02), same test RMSE (0.4783 vs 0.4786 at W=1)
+    # NF runs its DSGD schedule with 20 blocks per mode on the one GPU: the
+    # fastest of the measured W = 12/16/18/20/24/28/32 (18.8/10.3/10.2/9.7/
+    # 9.9/10.0/10.4 ms per epoch, W=1: 14.8; profiles/r02), same test RMSE
+    # (0.4784 vs 0.4786 at W=1)
     "nf": dict(workload="netflix-shaped 480189x17770x2182, 99,072,112 nnz, J=R=16",
                dims=(480189, 17770, 2182), nnz=99_072_112, n_test=1_408_395, J=16, R=16, alpha_a=0.003,
-               workers=24),
+               workers=20),
     "cfg1": dict(workload="synthetic 1Kx1Kx1K, 90K train / 10K test, J=R=8",
                  dims=(1000, 1000, 1000), nnz=90_000, n_test=10_000, J=8, R=8),
     # alpha_a: the reference's default 0.009 diverges on these std-4 synthetic

@@ -1003,11 +1003,7 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
   }
   const long long tiles = (n_visit + 127) / 128;
   // persistent grid minus the CTA slots left to the side-stream samplers
-  // one CTA slot per SM left to the side-stream samplers: the factor pass
-  // runs 3 CTAs per SM and the block permutations of the next epoch run
-  // beside it instead of after it (NF W=24: 9.47 vs 9.63 ms per epoch with
-  // 16 free slots at W=20)
-  int slots = 148;
+  int slots = (N == 3 && J >= 16) ? 16 : 148;
   if (const char* e = getenv("SPTK_SAMPLER_SLOTS")) slots = atoi(e);
   long long blocks = 148LL * per_sm - (per_sm >= 2 ? slots : 0);
   if (const char* e = getenv("SPTK_TC_GRID")) blocks = atoll(e);

@@ -2091,9 +2091,7 @@ __device__ __forceinline__ Pcg64 block_seed(const BlockJob& jb, const int* __res
 }
 
 // j-sequences: one warp per block, into the block's slice of js (record order)
-#ifndef BP_JW
 #define BP_JW 8
-#endif
 __global__ void __launch_bounds__(32 * BP_JW) block_jgen_kernel(const BlockJob* __restrict__ jobs, int n_jobs,
                                                                  const int* __restrict__ coords, int order,
                                                                  unsigned long long seed, long long t,
@@ -2106,12 +2104,10 @@ __global__ void __launch_bounds__(32 * BP_JW) block_jgen_kernel(const BlockJob* 
   if ((threadIdx.x & 31) == 0 && jb.n > 0) js[jb.off] = 0;  // virtual step 0 (position 0 keeps what is left)
 }
 
-// threads per block permutation CTA.  Alone (NF W=24): 256 / 512 / 1024 ->
-// 1.72 / 1.62 / 2.24 ms per epoch; 256 is what fits beside three factor CTAs
-// on an SM (registers), where the permutations run hidden under the factor
-// pass (NF W=24 epoch 9.63 -> 9.47 ms)
+// threads per block permutation CTA (NF W=24: 256 / 512 / 1024 -> 1.72 /
+// 1.62 / 2.24 ms per epoch)
 #ifndef BP_T
-#define BP_T 256
+#define BP_T 512
 #endif
 // Shared memory per nonzero: 8 bytes -- C (group counts, then group starts /
 // ends: 16-bit halves of 32-bit words, so the counting and scatter atomics

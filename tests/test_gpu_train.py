@@ -99,7 +99,7 @@ def test_cfg1_hogwild_rmse(golden, golden_meta):
     assert gap < 0.01
 
 
-@pytest.mark.parametrize("workers", [1, 24])
+@pytest.mark.parametrize("workers", [1, 20])
 def test_netflix_shaped_hogwild_rmse_curve_within_1pct(workers):
     """North-star accuracy bar on the bench workload (BASELINE configs[1]): the
     throughput (Hogwild, fp32, tcgen05) path's test RMSE after each of 5
