@@ -23,6 +23,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <atomic>
+
 namespace sptk {
 
 template <int N>
@@ -38,6 +40,8 @@ struct TcParams {
 
 static float* g_tc_debug = nullptr;
 __device__ unsigned g_tile_ctr[64];
+// rotating pool index, shared by every host thread that launches
+static std::atomic<unsigned> g_tc_ctr_slot{0};
 
 template <int N, int J, int R, bool SPLIT>
 struct TcCfg {
@@ -955,10 +959,9 @@ static int launch_tc3(const int* rec, int rw, const int* visit, long long n_visi
   if (blocks < 1) blocks = 1;
   if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
   if (blocks > tiles) blocks = tiles;
-  static unsigned slot = 0;
   unsigned* ctr = nullptr;
   SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tile_ctr));
-  ctr += (slot++ & 63u);
+  ctr += g_tc_ctr_slot.fetch_add(1u) & 63u;
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
   kfn<<<(unsigned)blocks, 256, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
   note_factor_kernel("factor_tc3_kernel");
@@ -1029,10 +1032,9 @@ static int launch_tc2(const int* rec, int rw, const int* visit, long long n_visi
   if (blocks > tiles) blocks = tiles;
   // per-launch tile counter from a small rotating pool (launches on one stream
   // are ordered; the pool only guards against back-to-back reuse)
-  static unsigned slot = 0;
   unsigned* ctr = nullptr;
   SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tile_ctr));
-  ctr += (slot++ & 63u);
+  ctr += g_tc_ctr_slot.fetch_add(1u) & 63u;
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
   kfn<<<(unsigned)blocks, 128, smem, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
   note_factor_kernel("factor_tc2_kernel");
@@ -1323,10 +1325,9 @@ static int launch_tc4(const int* rec, int rw, const int* visit, long long n_visi
   long long blocks = 148;
   if (blocks > hogwild_cta_cap(n_visit, 128)) blocks = hogwild_cta_cap(n_visit, 128);
   if (blocks > tiles) blocks = tiles;
-  static unsigned slot = 0;
   unsigned* ctr = nullptr;
   SPTK_CUDA_TRY(cudaGetSymbolAddress((void**)&ctr, g_tile_ctr));
-  ctr += (slot++ & 63u);
+  ctr += g_tc_ctr_slot.fetch_add(1u) & 63u;
   SPTK_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
   kfn<<<(unsigned)blocks, 512, C::SMEM, s>>>(rec, visit, n_visit, base, fac, cor, p, ctr);
   note_factor_kernel("factor_tc4_kernel");
