@@ -2115,7 +2115,6 @@ __global__ void __launch_bounds__(32 * BP_JW) block_jgen_kernel(const BlockJob* 
 // step, descending), and one array that holds L (steps grouped by target)
 // until S is built and V (chain roots) after.  16-bit entries: n <= 28000.
 #define BP_CAP 28000
-__device__ __forceinline__ unsigned c16_get(const unsigned* C, int t) { return (C[t >> 1] >> ((t & 1) * 16)) & 0xFFFFu; }
 __device__ __forceinline__ unsigned c16_inc(unsigned* C, int t) {
   const unsigned sh = (t & 1) * 16;
   return (atomicAdd(&C[t >> 1], 1u << sh) >> sh) & 0xFFFFu;
@@ -2124,20 +2123,44 @@ __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restri
                                                         const uint16_t* __restrict__ js,
                                                         int* __restrict__ visit, int cap) {
   extern __shared__ __align__(16) unsigned char bp_sm[];
-  unsigned* C = reinterpret_cast<unsigned*>(bp_sm);  // [cap/2 + 1] packed 16-bit
+  // a zero word, then C: once the counts are group ends, Cu[t] reads C's
+  // 16-bit half t directly and Cu[-1] = 0 is group 0's start
+  unsigned* C = reinterpret_cast<unsigned*>(bp_sm) + 1;  // [cap/2 + 1] packed 16-bit
+  const uint16_t* Cu = reinterpret_cast<const uint16_t*>(C);
   uint16_t* J = reinterpret_cast<uint16_t*>(C + (cap / 2 + 1));
   uint16_t* S = J + cap;
   uint16_t* LV = S + cap;  // L, then V
   __shared__ int sh[33];
-  __shared__ int sizes[64];
+  // the round's block sizes (slot order), ascending (with prefix sums), and
+  // the sizes of the slots before this one, ascending: the interleaved slot
+  // of entries past the round's smallest block by two binary searches
+  __shared__ int sizes[64], srt[64], low[64];
+  __shared__ long long pre[65];
   const BlockJob jb = jobs[blockIdx.x];
-  const int n = jb.n, tid = threadIdx.x;
-  if (tid < jb.m && tid < 64) sizes[tid] = jobs[jb.first + tid].n;
+  const int n = jb.n, tid = threadIdx.x, m = min(jb.m, 64);
+  if (tid < m) sizes[tid] = jobs[jb.first + tid].n;
+  if (tid == 0) reinterpret_cast<unsigned*>(bp_sm)[0] = 0u;
   for (int p = tid; p < (n + 1) / 2; p += BP_T) C[p] = 0u;
   for (int p = tid; p < n; p += BP_T) J[p] = js[jb.off + p];
   __syncthreads();
+  if (tid < m) {
+    const int v = sizes[tid];
+    int r = 0, rl = 0;
+    for (int s2 = 0; s2 < m; ++s2) {
+      const int w = sizes[s2];
+      r += w < v || (w == v && s2 < tid);
+      rl += s2 < jb.slot && (w < v || (w == v && s2 < tid));
+    }
+    srt[r] = v;
+    if (tid < jb.slot) low[rl] = v;
+  }
   for (int i = tid; i < n; i += BP_T) c16_inc(C, J[i]);
   __syncthreads();
+  if (tid == 0) {
+    long long a = 0;
+    pre[0] = 0;
+    for (int s2 = 0; s2 < m; ++s2) pre[s2 + 1] = a += srt[s2];
+  }
   {
     // exclusive scan of the 16-bit counts, each thread a run of whole words
     const int words = (n + 1) / 2;
@@ -2157,9 +2180,11 @@ __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restri
   for (int i = tid; i < n; i += BP_T) LV[c16_inc(C, J[i])] = (uint16_t)i;
   __syncthreads();
   // each step's place in its target's group, largest step first (the order
-  // Fisher-Yates runs them): rank = number of larger steps in the group
-  for (int i = tid; i < n; i += BP_T) {
-    const int t = J[i], s0 = t ? (int)c16_get(C, t - 1) : 0, s1 = (int)c16_get(C, t);
+  // Fisher-Yates runs them): rank = number of larger steps in the group.
+  // Walked in L order, so the lanes of a warp mostly share a group (the same
+  // trip count, broadcast reads)
+  for (int x0 = tid; x0 < n; x0 += BP_T) {
+    const int i = LV[x0], t = J[i], s0 = Cu[t - 1], s1 = Cu[t];
     int rank = 0;
     for (int x = s0; x < s1; ++x) rank += (int)LV[x] > i;
     S[s0 + rank] = (uint16_t)i;
@@ -2171,7 +2196,7 @@ __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restri
   // every step targeting t is >= t: the smallest step above t (t's parent)
   // is the last of the group, or the second to last after t's own step
   for (int t = tid; t < n; t += BP_T) {
-    const int s0 = t ? (int)c16_get(C, t - 1) : 0, s1 = (int)c16_get(C, t);
+    const int s0 = Cu[t - 1], s1 = Cu[t];
     if (s1 > s0) {
       const int last = S[s1 - 1];
       if (last > t) LV[t] = (uint16_t)last;
@@ -2197,19 +2222,22 @@ __global__ void __launch_bounds__(BP_T) block_fy_kernel(const BlockJob* __restri
   // result[i]: the value its target held just before step i, written straight
   // to its round-interleaved slot:
   //   slot(p) = sum_s min(n_s, p) + #{s < slot : n_s > p}
-  const int m = min(jb.m, 64);
   for (int x = tid; x < n; x += BP_T) {
-    const int i = S[x], t = J[i], s0 = t ? (int)c16_get(C, t - 1) : 0;
+    const int i = S[x], t = J[i], s0 = Cu[t - 1];
     const int val = x == s0 ? t : (int)LV[S[x - 1]];
     long long pos = jb.out_base;
     if (i < jb.nmin) {
       pos += (long long)i * m + jb.slot;  // every block of the round still has entries
     } else {
-      for (int s2 = 0; s2 < m; ++s2) {
-        const int ns = sizes[s2];
-        pos += ns < i ? ns : i;
-        if (s2 < jb.slot && ns > i) ++pos;
+      // k sizes below i: sum_s min(n_s, i) = pre[k] + i (m - k); then the
+      // earlier slots whose blocks are longer than i
+      int k = 0, q = 0;
+#pragma unroll
+      for (int st = 64; st; st >>= 1) {
+        if (k + st <= m && srt[k + st - 1] < i) k += st;
+        if (q + st <= jb.slot && low[q + st - 1] <= i) q += st;
       }
+      pos += pre[k] + (long long)i * (m - k) + (jb.slot - q);
     }
     visit[pos] = (int)(jb.off + val);
   }
