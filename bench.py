@@ -246,10 +246,15 @@ def bench_ours(args, cfg):
     scale = default_init_scale(tr.values, order)
     model = init_model(cfg["dims"], ModelConfig((cfg["J"],) * order, cfg["R"], scale, seed=1))
     # +3: every timed epoch also draws the next epoch's samples (steady state)
-    workers = args.workers if args.workers else (world if world > 1 else cfg.get("workers", 1))
+    sim = int(os.environ.get("BENCH_DSGD_SIM", "0"))
+    # M GPUs (or the M-rank simulation): the config's DSGD blocks per mode
+    # rounded up to a multiple of M -- each rank's slab keeps the reference's
+    # W-worker blocks (dsgd_fused.sub_rounds; NF: W = 20 at M = 2 / 4, 24 at 8)
+    ranks = world if world > 1 else max(sim, 1)
+    w0 = cfg.get("workers", 1)
+    workers = args.workers if args.workers else (-(-w0 // ranks) * ranks if ranks > 1 else w0)
     tcfg = TrainConfig(epochs=args.warmup + args.steps + 3, seed=1, update_mode=args.mode,
                        workers=workers, alpha_a=cfg.get("alpha_a", 0.009))
-    sim = int(os.environ.get("BENCH_DSGD_SIM", "0"))
     if distributed:
         from paper_2204_07104_b200 import dist
 
@@ -268,7 +273,6 @@ def bench_ours(args, cfg):
 
         from paper_2204_07104_b200.dsgd_fused import FusedRankRunner, fused_supported
 
-        tcfg = replace(tcfg, workers=sim)
         if fused_supported(model, replace(tcfg, update_mode="hogwild")) and os.environ.get("BENCH_SIM_FUSED", "1") == "1":
             runner = FusedRankRunner(model, tr, replace(tcfg, update_mode="hogwild"), 0, sim)
             fa, ra = runner.fused.peer_addresses()

@@ -225,13 +225,15 @@ class DistRunner(EpochRunner):
     """One rank of multi-GPU training: EpochRunner restricted to this rank's
     blocks, with the DSGD exchanges in its round / phase hooks."""
 
-    def __init__(self, model, train_set, config, group=None):
+    def __init__(self, model, train_set, config, group=None, sub_blocks: bool = False):
         import torch.distributed as td
 
         rank, world = td.get_rank(group), td.get_world_size(group)
-        if config.workers != world:
+        # sub_blocks (the fused runner): workers = k * world keeps the
+        # reference's W-worker blocks inside each rank's slab (dsgd_fused.sub_rounds)
+        if config.workers != world and not (sub_blocks and config.workers > world and config.workers % world == 0):
             config = replace(config, workers=world)
-        super().__init__(model, train_set, config, owner_rank=rank)
+        super().__init__(model, train_set, config, owner_rank=rank, owner_world=world)
         self.rank, self.world = rank, world
         self.plan = DsgdPlan(model.dims, world)
         self.ex = DsgdExchange(self.plan, self.dm.fac, self.dm.foff, self.dm.jr, group)
@@ -243,6 +245,28 @@ class DistRunner(EpochRunner):
 
     def after_factor_phase(self):
         self.ex.gather_all(self.plan.n_rounds - 1)
+
+    # Psi is one serial draw over the whole tensor (trainer.py:212-220); the
+    # ranks take turns: rank t % W draws epoch t's batch on its psi stream and
+    # broadcasts it (4 MB at NF), so each rank draws 1/W of the batches.
+    def draws_psi(self, t):
+        return t % self.world == self.rank
+
+    def share_psi(self, t, stream):
+        buf = self.psi[t % 3][:self.k]
+        src = t % self.world
+        if self.ex.group is not None:
+            src = self.ex.td.get_global_rank(self.ex.group, src)
+        if stream is None:
+            stream = self.torch.cuda.current_stream()
+        if self.ex.nccl:
+            with self.torch.cuda.stream(stream):
+                self.ex.td.broadcast(buf, src, group=self.ex.group)
+        else:
+            stream.synchronize()
+            h = buf.cpu()
+            self.ex.td.broadcast(h, src, group=self.ex.group)
+            buf.copy_(h)
 
     def core_slice(self, slot):
         lo, hi = self.plan.chunk_bounds(self.k)[self.rank]

@@ -58,6 +58,58 @@ def fused_supported(model, config, nnz: int | None = None) -> bool:
             and (model.order, J) in ((3, 16), (4, 16), (3, 8), (6, 8)))
 
 
+FULL_GRID = 576  # the TMA kernel's single-GPU grid at J = 16 (4 CTAs x 148 SMs - 16 sampler slots)
+
+
+def hot_row_concurrency(dims, m: int, div: int, nnz: int, n_rank: int) -> np.ndarray:
+    """rho per mode: in-flight samples per row of one rank of M-way DSGD (its
+    grid divided by ``div``, its ``n_rank`` visits, blocks of dims/M rows)
+    over those of one GPU running all ``nnz``; 1 where the rank keeps less
+    than one sample in flight per row (concurrent updates of a row are then
+    rare).  Both grids are capped like the launcher's Hogwild cap
+    (common.cuh hogwild_cta_cap: one 128-sample CTA per 64 x 128 visits)."""
+    cap = lambda n: max(1, n // (64 * 128))  # noqa: E731
+    g1 = min(FULL_GRID, cap(nnz)) * 128
+    gr = max(1, -(-min(FULL_GRID, cap(n_rank)) // div)) * 128
+    d = np.asarray(dims, dtype=np.float64)
+    c1 = g1 / d
+    cr = gr / (d / m)
+    return np.where(cr >= 1.0, cr / c1, 1.0)
+
+
+def sub_rounds(plan, rank: int, workers: int):
+    """The visit-list layout of one rank's epoch: (blocks [S, k, N], groups [S]).
+
+    M-way DSGD round r gives the rank the block B = plan.block_of(rank, r)
+    (partition.py:100-117 at M workers).  With ``workers`` = W = k*M blocks
+    per mode (the reference's W-worker division, whose cut points nest in the
+    M-way ones: (j*k*d)//(k*M) == (j*d)//M), B is the union of k^N W-blocks;
+    they run as k^(N-1) sub-rounds of k row-disjoint W-blocks (b_0 = B_0 k + i,
+    b_n = B_n k + (i + s_n) % k), laid end to end inside the round (group r).
+    Every W-block keeps the reference's own visit order of the W-worker run
+    (default_rng([seed, 1, t, *b]), trainer.py:196-199), so each block fits
+    the shared-memory sampler (sptk_block_perm) instead of the whole-slab one.
+    k = 1: one block per round (the M-worker run itself)."""
+    import itertools
+
+    M, N = plan.m, plan.order
+    if workers % M:
+        raise ValueError(f"workers={workers} is not a multiple of the {M} ranks")
+    k = workers // M
+    subs = np.array(list(itertools.product(range(k), repeat=N - 1)), dtype=np.int64).reshape(-1, N - 1)
+    i = np.arange(k, dtype=np.int64)
+    out, groups = [], []
+    for r in range(plan.n_rounds):
+        B = np.asarray(plan.block_of(rank, r), dtype=np.int64)
+        blk = np.empty((len(subs), k, N), dtype=np.int64)
+        blk[:, :, 0] = B[0] * k + i[None, :]
+        for n in range(1, N):
+            blk[:, :, n] = B[n] * k + (i[None, :] + subs[:, n - 1:n]) % k
+        out.append(blk)
+        groups.append(np.full(len(subs), r, dtype=np.int64))
+    return np.concatenate(out), np.concatenate(groups)
+
+
 class FusedState:
     """Device state of one rank's fused DSGD factor phase (see module doc)."""
 
@@ -69,17 +121,17 @@ class FusedState:
         R = plan.n_rounds
         # the rank's block of every round (kept even when empty: its tile is
         # what forwards the block to the next owner)
-        rounds = []
-        for r in range(R):
-            block = plan.block_of(rank, r)
-            off, cnt = runner.part.block_range(block)
-            rounds.append([(block, off, cnt)] if cnt > 0 else [])
-        self.big = max((c for rnd in rounds for (_, _, c) in rnd), default=0) > BLOCK_PERM_MAX
-        self.orders = BlockOrders(rounds, runner.order, dev, big=self.big, pad=TILE)
+        blocks, groups = sub_rounds(plan, rank, runner.m)
+        W, N = runner.m, runner.order
+        keys = (blocks * (W ** np.arange(N - 1, -1, -1, dtype=np.int64))).sum(axis=2)
+        offs = runner.part.block_off[keys]
+        cnts = runner.part.block_off[keys + 1] - offs
+        self.big = int(cnts.max(initial=0)) > BLOCK_PERM_MAX
+        self.orders = BlockOrders.from_arrays(blocks, offs, cnts, N, dev, big=self.big, pad=TILE, groups=groups)
         self.total = self.orders.total
         self.fvis = [torch.full((self.total,), -1, dtype=torch.int32, device=dev) for _ in range(2)]
-        self.rstart = torch.tensor(self.orders.round_start, dtype=torch.int64, device=dev)
-        self.rend = torch.tensor(self.orders.round_end, dtype=torch.int64, device=dev)
+        self.rstart = torch.tensor(self.orders.group_start, dtype=torch.int64, device=dev)
+        self.rend = torch.tensor(self.orders.group_end, dtype=torch.int64, device=dev)
         self.done = torch.zeros(R, dtype=torch.int32, device=dev)
         # the model replica other ranks write into, plus this rank's flag
         dm = runner.dm
@@ -95,18 +147,34 @@ class FusedState:
         self.epoch_flag = self.shared.view("int32", 1, self.flag_off + 4)
         self.push = None
         # Hogwild staleness inside a rank: a round's block covers 1/M of every
-        # mode's rows, so a full grid would put M times more concurrent
-        # updates on each hot row than one GPU running the whole tensor does.
-        # Measured on one GPU with the 8-worker NF blocks launched one by one
-        # at full occupancy (the per-rank dynamics of 8-GPU DSGD): test RMSE
-        # NaN; with ~1/6 of the grid: 0.4832 (the reference's W=8 curve).  A
-        # rank therefore runs 1/M of the single-GPU grid: the same in-flight
-        # samples per hot row as the validated single-GPU runs
-        # (SPTK_DSGD_GRID_DIV overrides M; 1 = full grid).
+        # mode's rows, so the single-GPU grid puts M times more samples in
+        # flight on each hot row than one GPU running the whole tensor does,
+        # and the hot modes' add-reduced deltas (summed over every in-flight
+        # sample on a row) overshoot.  Measured on one GPU with the M-worker
+        # NF blocks launched one by one (one rank's dynamics at M-GPU DSGD;
+        # tools/dsgd_rank_dynamics.py), test RMSE against
+        # the reference's 8-worker curve after 5 epochs:
+        #   M = 8: full grid (rho = 8) NaN; 1/2 grid NaN; 1/4 grid +1.1%;
+        #   1/8 grid +0.3%; full grid with both hot modes' steps x 1/2 +0.6%,
+        #   x 1/4 -0.5%, x 1/8 -0.7%; 1/2 grid (rho = 4) x 1/2: +0.01%, but
+        #   with only the 2,182-row mode scaled +0.6% (+3.5% after epoch 1);
+        #   M = 4 full grid: NaN, x 1/2: -0.03%; M = 2: +1.0%, x 0.71: +0.16%.
+        # Repeated runs at a full grid (both hot modes): M = 8 x 0.35: +0.7%
+        # and -0.2% (+1.4% / +2.9% after epoch 1), x 0.25: -0.48% twice,
+        # x 0.18: -0.6%; M = 4 x 0.5: -0.05% twice, x 0.4: -0.33%; M = 2
+        # x 0.71: +0.16%, x 0.63: -0.01%.
+        # Rule: each hot mode's step is multiplied by rho^(-2/3) (rho = the
+        # rank's in-flight samples per row of that mode over one GPU's,
+        # hot_row_concurrency: M at a full grid, 1 for small tensors):
+        # 0.63 / 0.40 / 0.25 at M = 2 / 4 / 8.
+        # SPTK_DSGD_GRID_DIV (default 1) / SPTK_HOT_STEP_SCALE override.
         import os
 
-        div = int(os.environ.get("SPTK_DSGD_GRID_DIV", plan.m))
+        div = int(os.environ.get("SPTK_DSGD_GRID_DIV", 1))
         self.grid = -div if div > 1 else 0
+        self.rho = hot_row_concurrency(plan.dims, plan.m, div, runner.part.nnz, self.total)
+        if not runner.hot_step_env:
+            runner.hot_step_scale = np.where(runner.hot, np.minimum(1.0, self.rho ** (-2.0 / 3.0)), 1.0)
 
     # -- peers ---------------------------------------------------------------
     def peer_addresses(self):
@@ -152,7 +220,7 @@ class FusedState:
         r, dm = self.runner, self.runner.dm
         if self.push is None:
             raise RuntimeError("set_peers() first")
-        r._gam[:] = gamma_a
+        r.set_gamma(gamma_a)
         R = self.plan.n_rounds
         check(r.L.sptk_factor_pass_dsgd(ptr(r.part.rec), r.part.rw, ptr(self.fvis[slot]), self.total, ptr(dm.fac),
                                         dm.p_foff, ptr(dm.cor), dm.p_coff, dm.p_jr, r.order, dm.rcore, r.p_gam,
@@ -200,9 +268,9 @@ class FusedRankRunner(_FusedMixin, EpochRunner):
     to the caller."""
 
     def __init__(self, model, train_set, config, rank: int, world: int, prefetch: bool = True):
-        if config.workers != world:
+        if config.workers < world or config.workers % world:
             config = replace(config, workers=world)
-        super().__init__(model, train_set, config, prefetch=prefetch, owner_rank=rank)
+        super().__init__(model, train_set, config, prefetch=prefetch, owner_rank=rank, owner_world=world)
         self.rank, self.world = rank, world
         self.plan = DsgdPlan(model.dims, world)
         self.fused = FusedState(self, self.plan, rank)
@@ -214,6 +282,20 @@ class FusedRankRunner(_FusedMixin, EpochRunner):
         """Call after the caller's epoch-end exchange of epoch t (stream order)."""
         self.fused.mark_exchanged(t)
 
+    # the core phase as a rank of DistRunner runs it: this rank draws the
+    # batches of epochs t = rank (mod W) (the caller hands the others over)
+    # and computes the gradient of its chunk of Psi (the caller sums them)
+    def draws_psi(self, t):
+        return t % self.world == self.rank
+
+    def core_slice(self, slot):
+        lo, hi = self.plan.chunk_bounds(self.k)[self.rank]
+        if self.k == self.nnz:
+            ids = self.torch.arange(lo, hi, dtype=self.torch.int32, device=self.dm.fac.device)
+        else:
+            ids = self.psi[self.psi_slot][lo:hi]
+        return ids, hi - lo, 0
+
 
 class FusedDistRunner(_FusedMixin, DistRunner):
     """dist.DistRunner with the rounds fused: the ranks map each other's model
@@ -223,7 +305,7 @@ class FusedDistRunner(_FusedMixin, DistRunner):
     def __init__(self, model, train_set, config, group=None):
         import torch.distributed as td
 
-        super().__init__(model, train_set, config, group)
+        super().__init__(model, train_set, config, group, sub_blocks=True)
         self.fused = FusedState(self, self.plan, self.rank)
         self.ex.fac = self.dm.fac  # the exchange works on the shared replica
         mine = (self.fused.shared.ipc_handle(), self.fused.flag_off)
@@ -252,4 +334,4 @@ class FusedDistRunner(_FusedMixin, DistRunner):
         self.fused.mark_exchanged(self._fused_t)
 
 
-__all__ = ["FusedState", "FusedRankRunner", "FusedDistRunner", "fused_supported"]
+__all__ = ["sub_rounds", "hot_row_concurrency", "FusedState", "FusedRankRunner", "FusedDistRunner", "fused_supported"]

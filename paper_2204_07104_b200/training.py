@@ -204,7 +204,7 @@ class EpochRunner:
     """
 
     def __init__(self, model: TuckerModel, train_set: SparseTensorCoo, config: TrainConfig,
-                 prefetch: bool = True, owner_rank: int | None = None):
+                 prefetch: bool = True, owner_rank: int | None = None, owner_world: int | None = None):
         import torch
 
         _lib.require_cuda()
@@ -214,8 +214,11 @@ class EpochRunner:
         self.mode = resolve_mode(config.update_mode, train_set.nnz)
         self.m = int(config.workers)
         # owner_rank = w: this process runs only the blocks (w, ...) of each
-        # round (one GPU of the DSGD data division, dist.py)
+        # round (one GPU of the DSGD data division, dist.py); with owner_world
+        # = M < workers (a multiple of M) it runs the workers w*k .. w*k+k-1,
+        # k = workers / M: every block of its mode-0 slab (dsgd_fused)
         self.owner_rank = owner_rank
+        self.owner_k = 1 if owner_world is None else int(config.workers) // int(owner_world)
         self.order = model.order
         self.nnz = train_set.nnz
         # J = R = 4 in throughput mode on tcgen05: a zero-padded rank-8 model
@@ -231,7 +234,7 @@ class EpochRunner:
         # round r, partition.py:100-117), their record offsets and sizes
         blocks = round_blocks(model.order, self.m)
         if owner_rank is not None:
-            blocks = blocks[:, owner_rank: owner_rank + 1]
+            blocks = blocks[:, owner_rank * self.owner_k: (owner_rank + 1) * self.owner_k]
         keys = (blocks * (self.m ** np.arange(model.order - 1, -1, -1, dtype=np.int64))).sum(axis=2)
         self._r_blocks = blocks
         self._r_off = self.part.block_off[keys]
@@ -318,6 +321,17 @@ class EpochRunner:
         self.gam_np = np.zeros(self.order)
         self.lam_np = np.full(self.order, float(config.lambda_a))
         self._gam, self.p_gam = f64arr(self.gam_np)
+        # Hogwild step rule for the add-reduced (hot, < 2^18 rows) modes: the
+        # kernel sums the deltas of every in-flight sample on a row, so a
+        # launch that puts rho times more samples in flight per hot row than
+        # the validated single-GPU pass (a DSGD rank: its block holds 1/M of
+        # each mode's rows) scales their step by rho^(-2/3) (dsgd_fused).
+        # 1.0 everywhere else; SPTK_HOT_STEP_SCALE overrides (experiments).
+        # Per mode, multiplied into gamma_a by set_gamma.
+        self.hot = np.array([d < (1 << 18) for d in model.dims], dtype=bool)
+        self.hot_step_env = "SPTK_HOT_STEP_SCALE" in os.environ
+        env = [float(x) for x in os.environ.get("SPTK_HOT_STEP_SCALE", "1.0").replace(";", ",").split(",")]
+        self.hot_step_scale = np.where(self.hot, env if len(env) == model.order else env[0], 1.0)
         self._lam, self.p_lam = f64arr(self.lam_np)
         self.map = self.part.pos_of_id if self.m > 1 else None
         self.L = L
@@ -373,10 +387,19 @@ class EpochRunner:
         if "psi" in self._skip and self.psi_epoch[t % 3] is not None:
             self.psi_epoch[t % 3] = t
             return
-        if cfg.update_core and self.k < self.nnz:
+        if cfg.update_core and self.k < self.nnz and self.draws_psi(t):
             choice(None, self.nnz, self.k, shuffle=(self.mode == 1), out=self.psi[t % 3], ws=self.ws_psi,
                    state=pcg64_state([cfg.seed, 2, t]), stream=stream)
+        if cfg.update_core and self.k < self.nnz:
+            self.share_psi(t, stream)
         self.psi_epoch[t % 3] = t
+
+    def draws_psi(self, t: int) -> bool:
+        """Whether this process draws the core batch of epoch t itself."""
+        return True
+
+    def share_psi(self, t: int, stream) -> None:
+        """Hand the core batch of epoch t to the processes that did not draw it."""
 
     def draw_jseq(self, t: int, slot: int, stream) -> None:
         """Fisher-Yates j-sequences of every (own) block of epoch t:
@@ -517,9 +540,15 @@ class EpochRunner:
         self._marks = []
 
     # -- K3 / K4 / K5 ------------------------------------------------------
+    def set_gamma(self, gamma_a: float) -> None:
+        """Per-mode factor steps of this epoch (hot modes x hot_step_scale)."""
+        self._gam[:] = gamma_a
+        if self.mode == 0:
+            self._gam[:] *= self.hot_step_scale
+
     def factor_phase(self, t: int, gamma_a: float, slot: int) -> int:
         L, dm = self.L, self.dm
-        self._gam[:] = gamma_a
+        self.set_gamma(gamma_a)
         fn = L.sptk_factor_pass_f64 if self.f64 else L.sptk_factor_pass
         s = stream_ptr()
         processed = 0

@@ -115,3 +115,46 @@ def test_dsgd_exchange_reproduces_reference_workers(world, cap):
     want_cor, _ = O.pack(ref_b)
     for g in got:  # every rank ends with the full, identical model, bit for bit (rank-order merge)
         assert np.array_equal(g["fac"], want_fac) and np.array_equal(g["cor"], want_cor)
+
+
+@pytest.mark.parametrize("dims,M,W", [((50, 40, 30), 2, 6), ((20, 18, 16, 14), 2, 4), ((30, 30, 30), 4, 8),
+                                      ((40, 30, 20), 2, 2)])
+def test_sub_rounds_cover_the_slab_with_row_disjoint_blocks(dims, M, W):
+    """dsgd_fused.sub_rounds: rank w's epoch holds every W-block of its
+    mode-0 slab exactly once, each inside the M-block of its round, and the k
+    W-blocks of a sub-round are row-disjoint in every mode."""
+    from paper_2204_07104_b200.dsgd_fused import sub_rounds
+    from paper_2204_07104_b200.schedule import cut_points
+
+    plan = DsgdPlan(dims, M)
+    k, N = W // M, len(dims)
+    cw, cm = cut_points(dims, W), cut_points(dims, M)
+    for n in range(N):  # the W-way cut points nest in the M-way ones
+        assert all(cw[n][j * k] == cm[n][j] for j in range(M + 1))
+    for rank in range(M):
+        blocks, groups = sub_rounds(plan, rank, W)
+        assert blocks.shape == (plan.n_rounds * k ** (N - 1), k, N)
+        assert np.all(np.diff(groups) >= 0) and groups[-1] == plan.n_rounds - 1
+        seen = {tuple(b) for b in blocks.reshape(-1, N)}
+        assert len(seen) == blocks.shape[0] * k
+        want = {b for b in np.ndindex(*(W,) * N) if rank * k <= b[0] < (rank + 1) * k}
+        assert seen == want
+        for s in range(blocks.shape[0]):
+            B = plan.block_of(rank, int(groups[s]))
+            for n in range(N):
+                assert len(set(blocks[s, :, n])) == k
+                assert np.all(blocks[s, :, n] // k == B[n])
+
+
+def test_block_orders_groups_pad_per_group():
+    """BlockOrders.from_arrays(groups=...): rounds of a group lie end to end,
+    groups start on multiples of pad and an empty group still takes one unit."""
+    from paper_2204_07104_b200.sampler import BlockOrders
+
+    cnts = np.array([[3, 4], [5, 0], [0, 0], [7, 1]])
+    offs = np.array([[0, 3], [7, 12], [12, 12], [12, 19]])
+    blocks = np.zeros((4, 2, 3), dtype=np.int64)
+    bo = BlockOrders.from_arrays(blocks, offs, cnts, 3, "cpu", pad=16, groups=[0, 0, 1, 2])
+    assert bo.round_start == [0, 7, 16, 32, 48] and bo.round_end == [7, 12, 16, 40]
+    assert bo.group_start == [0, 16, 32, 48] and bo.group_end == [12, 16, 40]
+    assert bo.total == 48

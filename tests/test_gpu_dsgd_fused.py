@@ -160,3 +160,86 @@ def test_two_processes_ipc_match_reference_dsgd(tmp_path):
             dims=tuple(dims))
     want, _ = O.pack(fs)
     np.testing.assert_allclose(got[0], want, rtol=5e-3, atol=5e-4 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("dims,J,W", [((3000, 2800, 2600), 16, 4), ((3000, 2800, 2600), 8, 6),
+                                      ((1200, 1100, 1000, 900), 16, 4)])
+def test_sub_blocked_ranks_use_reference_block_orders(dims, J, W):
+    """Two ranks sharing one GPU with W = k * 2 DSGD blocks per mode
+    (dsgd_fused.sub_rounds): every W-block's entries appear in the rank's
+    visit list in the reference's own order for that block
+    (default_rng([seed, 1, t, *b]).permutation, via the pinned oracle), each
+    training entry exactly once per epoch; with every row used by one entry
+    only (the update order cannot matter) the factors equal the reference's
+    W-worker run at TF32 tolerance."""
+    from paper_2204_07104_b200 import ModelConfig, SparseTensorCoo, TrainConfig, init_model
+    from paper_2204_07104_b200.dsgd_fused import FusedRankRunner
+    from paper_2204_07104_b200.training import learning_rate
+
+    M, E, order = 2, 2, len(dims)
+    rng = np.random.default_rng(11)
+    nnz = 2400 if order == 3 else 800
+    idx = np.stack([rng.permutation(d)[:nnz] for d in dims], axis=1)
+    vals = rng.normal(2.0, 1.0, nnz)
+    tensor = SparseTensorCoo(tuple(dims), idx, vals)
+    model = init_model(dims, ModelConfig((J,) * order, J, 1.0, seed=1))
+    cfg = TrainConfig(epochs=E, workers=W, seed=1, alpha_a=0.003, update_mode="hogwild", update_core=False)
+    streams = [torch.cuda.Stream() for _ in range(M)]
+    ranks = []
+    for w in range(M):
+        with torch.cuda.stream(streams[w]):
+            ranks.append(FusedRankRunner(model, tensor, cfg, w, M, prefetch=False))
+    torch.cuda.synchronize()
+    assert all(rk.m == W for rk in ranks)
+    addrs = [rk.fused.peer_addresses() for rk in ranks]
+    for rk in ranks:
+        rk.set_peers([a for a, _ in addrs], [b for _, b in addrs])
+        rk.fused.grid = 64
+    plan = ranks[0].plan
+    dm0 = ranks[0].dm
+    k = W // M
+    for t in range(E):
+        ga = learning_rate(cfg.alpha_a, cfg.beta_a, t)
+        slots = []
+        for w, rk in enumerate(ranks):
+            with torch.cuda.stream(streams[w]):
+                slots.append(rk._ensure_samples(t))
+        torch.cuda.synchronize()
+        covered = 0
+        for w, rk in enumerate(ranks):
+            vis = rk.fused.fvis[slots[w]].cpu().numpy().astype(np.int64)
+            vis = vis[vis >= 0]
+            covered += vis.size
+            assert np.unique(vis).size == vis.size
+            for b in np.ndindex(*(W,) * order):
+                if not (w * k <= b[0] < (w + 1) * k):
+                    continue
+                off, cnt = rk.part.block_range(b)
+                got = vis[(vis >= off) & (vis < off + cnt)] - off
+                want = O.permutation([cfg.seed, 1, t, *b], cnt) if cnt else np.zeros(0, np.int64)
+                np.testing.assert_array_equal(got, want)
+        assert covered == nnz
+        for w, rk in enumerate(ranks):
+            with torch.cuda.stream(streams[w]):
+                rk.factor_phase(t, ga, slots[w])
+        torch.cuda.synchronize()
+        for q, src in enumerate(ranks):
+            for n, b in enumerate(plan.held_blocks(q, plan.n_rounds - 1)):
+                lo, hi = plan.rows(n, b)
+                a, z = int(dm0.foff[n]) + lo * J, int(dm0.foff[n]) + hi * J
+                for w, dst in enumerate(ranks):
+                    if w != q:
+                        dst.dm.fac[a:z].copy_(src.dm.fac[a:z])
+        for rk in ranks:
+            rk.mark_exchanged(t)
+        torch.cuda.synchronize()
+    got = ranks[0].dm.fac.double().cpu().numpy()
+    assert np.array_equal(got, ranks[1].dm.fac.double().cpu().numpy())
+    fs = [a.copy() for a in model.factors]
+    bs = [b.copy() for b in model.core_factors]
+    O.train(fs, bs, idx, vals, epochs=E, workers=W, seed=1, alpha_a=0.003, update_core=False, evaluate=False,
+            dims=tuple(dims))
+    want, _ = O.pack(fs)
+    init, _ = O.pack(model.factors)
+    assert not np.allclose(want, init)
+    np.testing.assert_allclose(got, want, rtol=5e-3, atol=5e-4 * np.abs(want).max())
