@@ -253,7 +253,7 @@ class DistRunner(EpochRunner):
         return t % self.world == self.rank
 
     def share_psi(self, t, stream):
-        buf = self.psi[t % 3][:self.k]
+        buf = self.psi[t % self.P][:self.k]
         src = t % self.world
         if self.ex.group is not None:
             src = self.ex.td.get_global_rank(self.ex.group, src)

@@ -272,7 +272,11 @@ class EpochRunner:
         self.k = min(self.nnz, int(config.core_batch_cap))
         # core batches run two epochs ahead (the Floyd/Lemire draw is a serial
         # single-CTA walk): three slots
-        self.psi = [torch.empty(max(self.k, 1), dtype=torch.int32, device=dev) for _ in range(3)]
+        # (P slots; M processes: M + 2, so that each process can draw its
+        # share of the batches -- epochs = rank mod M -- up to M epochs ahead)
+        self.P = 3 if owner_world is None else max(3, int(owner_world) + 2)
+        self.psi = [torch.zeros(max(self.k, 1), dtype=torch.int32, device=dev) for _ in range(self.P)]
+        self.psi_drawn = set()
         # one preallocated workspace per sampler stage (never regrown while a
         # kernel on another stream may still be using it)
         Lb = _lib.load()
@@ -355,10 +359,10 @@ class EpochRunner:
         self.side_j, self.side, self.side2 = mk(prio[0]), mk(prio[1]), mk(prio[2])
         ev2 = lambda: [torch.cuda.Event(), torch.cuda.Event()]  # noqa: E731
         self.j_ready, self.j_free, self.perm_ready, self.done = ev2(), ev2(), ev2(), ev2()
-        self.psi_ready = [torch.cuda.Event() for _ in range(3)]
+        self.psi_ready = [torch.cuda.Event() for _ in range(self.P)]
         self.j_epoch = [None, None]
         self.sampled_epoch = [None, None]
-        self.psi_epoch = [None, None, None]
+        self.psi_epoch = [None] * self.P
         self.psi_slot = 0
         self.timeline = None  # set to [] to record per-epoch stream timelines (synchronises)
         self._marks = []
@@ -382,17 +386,25 @@ class EpochRunner:
 
     # -- samplers (K2) -----------------------------------------------------
     def draw_core_batch(self, t: int, stream) -> None:
-        """Core batch Psi of epoch t (trainer.py:212-220) into psi[t % 3]."""
+        """Core batch Psi of epoch t (trainer.py:212-220) into psi[t % P]:
+        drawn here unless drawn ahead (draw_psi), then shared (share_psi)."""
         cfg = self.cfg
-        if "psi" in self._skip and self.psi_epoch[t % 3] is not None:
-            self.psi_epoch[t % 3] = t
+        if "psi" in self._skip and self.psi_epoch[t % self.P] is not None:
+            self.psi_epoch[t % self.P] = t
             return
-        if cfg.update_core and self.k < self.nnz and self.draws_psi(t):
-            choice(None, self.nnz, self.k, shuffle=(self.mode == 1), out=self.psi[t % 3], ws=self.ws_psi,
-                   state=pcg64_state([cfg.seed, 2, t]), stream=stream)
+        self.draw_psi(t, stream)
         if cfg.update_core and self.k < self.nnz:
             self.share_psi(t, stream)
-        self.psi_epoch[t % 3] = t
+        self.psi_drawn.discard(t)
+        self.psi_epoch[t % self.P] = t
+
+    def draw_psi(self, t: int, stream) -> None:
+        """This process's draw of epoch t's core batch (if it draws it)."""
+        cfg = self.cfg
+        if cfg.update_core and self.k < self.nnz and self.draws_psi(t) and t not in self.psi_drawn:
+            choice(None, self.nnz, self.k, shuffle=(self.mode == 1), out=self.psi[t % self.P], ws=self.ws_psi,
+                   state=pcg64_state([cfg.seed, 2, t]), stream=stream)
+            self.psi_drawn.add(t)
 
     def draws_psi(self, t: int) -> bool:
         """Whether this process draws the core batch of epoch t itself."""
@@ -448,7 +460,7 @@ class EpochRunner:
 
     def draw_samples(self, t: int, slot: int, stream) -> None:
         """Visit orders of every block and the core batch of epoch t, in order on one stream."""
-        if self.psi_epoch[t % 3] != t:
+        if self.psi_epoch[t % self.P] != t:
             self.draw_core_batch(t, stream)
         self.draw_jseq(t, slot, stream)
         self.apply_jseq(t, slot, stream)
@@ -458,10 +470,11 @@ class EpochRunner:
         slot, o = t % 2, 1 - t % 2
         main = torch.cuda.current_stream()
         E = self.cfg.epochs
-        self.psi_slot = t % 3
+        P = self.P
+        self.psi_slot = t % P
         if self.sampled_epoch[slot] != t:
-            if self.psi_epoch[t % 3] == t:
-                main.wait_event(self.psi_ready[t % 3])
+            if self.psi_epoch[t % P] == t:
+                main.wait_event(self.psi_ready[t % P])
             self.draw_samples(t, slot, main)
             self.j_free[slot].record(main)
             if self.prefetch:  # the side stages reuse the same workspaces
@@ -471,18 +484,24 @@ class EpochRunner:
                     st.wait_event(ev)
         else:
             main.wait_event(self.perm_ready[slot])
-            main.wait_event(self.psi_ready[t % 3])
+            main.wait_event(self.psi_ready[t % P])
         if not self.prefetch:
             return slot
-        for e in (t + 1, t + 2):
-            if e < E and self.psi_epoch[e % 3] != e:
-                # psi[e % 3] was last read by epoch e - 3 (its `done` parity slot
-                # still holds that epoch's event)
-                self.side2.wait_event(self.done[(e - 3) % 2])
-                self._mark(f"psi{e - t}_start", self.side2)
+        # core batches: epoch t+1's is completed (drawn if not yet, shared)
+        # and later ones this process draws are drawn ahead, up to t+P-1
+        for e in range(t + 1, min(t + P, E)):
+            if self.psi_epoch[e % P] == e or (e > t + 1 and (e in self.psi_drawn or not self.draws_psi(e))):
+                continue
+            # psi[e % P] was last read by epoch e - P (its `done` parity slot
+            # holds that epoch's event or a later one)
+            self.side2.wait_event(self.done[(e - P) % 2])
+            self._mark(f"psi{e - t}_start", self.side2)
+            if e == t + 1:
                 self.draw_core_batch(e, self.side2)
-                self._mark(f"psi{e - t}_end", self.side2)
-                self.psi_ready[e % 3].record(self.side2)
+                self.psi_ready[e % P].record(self.side2)
+            else:
+                self.draw_psi(e, self.side2)
+            self._mark(f"psi{e - t}_end", self.side2)
         if t + 1 < E and self.sampled_epoch[o] != t + 1:
             if self.j_epoch[o] != t + 1:
                 self.side_j.wait_event(self.j_free[o])
