@@ -519,12 +519,23 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
       ++r_tiles;
       if (!(tile * 128 < n_visit) || adv(r_cur, tile) != r_cur) {
         // this CTA's last tile of round r_cur: its row writes complete and
-        // visible, then count its tiles; the round's last CTA forwards the block
-        tc::bulk_wait_all();
-        fence_proxy_async_global();
-        __threadfence();
+        // visible, then count its tiles; the round's last CTA forwards the
+        // block.  Add-reduced (hot) rows need no drain here: the barrier orders
+        // every thread's red.adds before thread 0's gpu-scope fence, which is
+        // cumulative over them (the cooperative-groups grid barrier pattern;
+        // a fence by every thread cost ~1 membar stall per issued instruction
+        // at 8-way DSGD, where a CTA crosses a round every ~2.6 tiles).  A
+        // pushed block written by bulk stores (a cold mode) is drained first.
+        {
+          const int pm = (int)dp.push[r_cur].mode;
+          if (dp.push[r_cur].nrows > 0 && (!(p.atomic_mask >> pm & 1u) || p.bulk_red)) {
+            tc::bulk_wait_all();
+            fence_proxy_async_global();
+          }
+        }
         __syncthreads();
         if (tid == 0) {
+          __threadfence();
           const int total = (int)((dp.rstart[r_cur + 1] - dp.rstart[r_cur]) / 128);
           const int c = atomicAdd(dp.done + r_cur, r_tiles) + r_tiles;
           __threadfence();
@@ -542,7 +553,16 @@ __global__ void __launch_bounds__(128, tma_min_blocks<N, J>())
           const long long nf4 = ps.nrows * J / 4;
           const float4* src = reinterpret_cast<const float4*>(fac + p.foff[ps.mode] + ps.row_lo * J);
           float4* dst = reinterpret_cast<float4*>(ps.dst);
-          for (long long e = tid; e < nf4; e += 128) dst[e] = __ldcg(src + e);
+          // eight loads in flight per thread (the receiver waits on this copy)
+          long long e = tid;
+          for (; e + 7 * 128 < nf4; e += 8 * 128) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + e + u * 128);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dst[e + u * 128] = v[u];
+          }
+          for (; e < nf4; e += 128) dst[e] = __ldcg(src + e);
           __threadfence_system();
           __syncthreads();
           if (tid == 0) atomicMax_system(ps.dst_ready, dp.gen0 + r_cur + 1);

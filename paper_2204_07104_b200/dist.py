@@ -289,6 +289,7 @@ def train_distributed(model, split, config):
     and ends with the identical model."""
     import torch
 
+    from . import counting
     from .device import DeviceCoo, rmse_mae_device
     from .training import MetricsRow, _RecordView, learning_rate
 
@@ -312,6 +313,10 @@ def train_distributed(model, split, config):
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
         runner.epoch(t, ga, gb)
+        if counting.counter.enabled:
+            lo, hi = runner.plan.chunk_bounds(runner.k)[runner.rank]
+            counting.counter.add(counting.epoch_multiplies(model.j_ranks, model.r_core, runner.nnz_local,
+                                                           hi - lo if config.update_core else 0))
         ev1.record()
         pending.append((ev0, ev1))
         if (t + 1) % config.eval_every == 0 or t == config.epochs - 1:

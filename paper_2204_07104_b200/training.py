@@ -41,7 +41,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib
+from . import _lib, counting
 from ._lib import check, f64arr, i64arr, ptr, stream_ptr
 from .device import DeviceCoo, DeviceModel, eval_sums, rmse_mae_device
 from .sampler import (BLOCK_PERM_MAX, BlockOrders, Workspace, choice, fy_apply, pcg64_state, permutation_j,
@@ -695,6 +695,9 @@ def train(model: TuckerModel, split: DatasetSplit, config: TrainConfig) -> list[
         runner.epoch(t, ga, gb)
         ev1.record()
         pending.append((ev0, ev1))
+        if counting.counter.enabled:
+            counting.counter.add(counting.epoch_multiplies(model.j_ranks, model.r_core, runner.nnz_local,
+                                                           runner.k if config.update_core else 0))
         if (t + 1) % config.eval_every == 0 or t == config.epochs - 1:
             ev1.synchronize()
             for a, b in pending:
