@@ -1,7 +1,8 @@
 """One rank's Hogwild dynamics at M-GPU DSGD, on one GPU: the NF tensor with
 M workers, every block launched on its own (SPTK_FLAT=0) at the grid a rank
 would run, under the hot-mode step rules being compared.  Prints the per-epoch
-test RMSE against the reference's M-worker curve (tests/golden/nf99_curve.json).
+test RMSE against the reference's M-worker curve (tests/golden/nf99_curve.json,
+or CURVE=curve_y4_full.json ...).
 usage: python tools/dsgd_rank_dynamics.py "NAME:ENV=V,ENV=V" ..."""
 import json
 import os
@@ -15,8 +16,11 @@ from paper_2204_07104_b200 import DatasetSplit, ModelConfig, TrainConfig, defaul
 from paper_2204_07104_b200.device import predict_device_f64  # noqa
 from paper_2204_07104_b200.synthetic import generate_large  # noqa
 
-ref = json.load(open(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "nf99_curve.json")))
+# CURVE=<file in tests/golden> picks the workload (default: the NF curve)
+ref = json.load(open(os.path.join(os.path.dirname(__file__), "..", "tests", "golden",
+                                  os.environ.get("CURVE", "nf99_curve.json"))))
 dims, J = tuple(ref["dims"]), ref["J"]
+N = len(dims)
 want = [r["test_rmse"] for r in ref["rows"]]
 
 
@@ -27,9 +31,9 @@ def pred(model, idx):
     return out
 
 
-tr, te, _ = generate_large(dims, ref["nnz"], (J,) * 3, J, 0.1, seed=7, n_test=ref["n_test"], predict=pred)
+tr, te, _ = generate_large(dims, ref["nnz"], (J,) * N, J, 0.1, seed=7, n_test=ref["n_test"], predict=pred)
 ds = DatasetSplit(tr, te)
-m0 = init_model(dims, ModelConfig((J,) * 3, J, default_init_scale(tr.values, 3), seed=1))
+m0 = init_model(dims, ModelConfig((J,) * N, J, default_init_scale(tr.values, N), seed=1))
 print("reference", ref["workers"], "workers:", want, flush=True)
 for spec in sys.argv[1:]:
     name, _, envs = spec.partition(":")
@@ -41,7 +45,7 @@ for spec in sys.argv[1:]:
             workers = int(v)
         else:
             os.environ[k] = v
-    m = init_model(dims, ModelConfig((J,) * 3, J, default_init_scale(tr.values, 3), seed=1))
+    m = init_model(dims, ModelConfig((J,) * N, J, default_init_scale(tr.values, N), seed=1))
     t0 = time.time()
     rows = train(m, ds, TrainConfig(epochs=ref["epochs"], seed=1, alpha_a=ref["alpha_a"], workers=workers,
                                     update_mode="hogwild"))
