@@ -1,5 +1,5 @@
 #!/bin/bash
-# Final round record (record ring + W=20): full GPU suite + smoke, headline bench (e2e + cpu leg),
+# Final round record: full GPU suite + smoke, headline bench (e2e + cpu leg),
 # reference arm, timeline, launch list, ncu --set full of the factor kernel, every config's line.
 O=gpurun_out/round; mkdir -p $O
 nvidia-smi > $O/nvsmi.txt 2>&1
@@ -19,6 +19,7 @@ done
 timeout 900 python bench.py --config y4 --no-cpu-baseline --no-e2e --steps 5 > $O/y4.json 2> $O/y4.err
 timeout 900 python bench.py --config cfg1 --no-cpu-baseline --no-e2e --steps 5 > $O/cfg1.json 2> $O/cfg1.err
 timeout 1500 python bench.py --config o6 --no-cpu-baseline --no-e2e --steps 3 > $O/o6.json 2> $O/o6.err
-for m in 4 8; do
-  BENCH_DSGD_SIM=$m timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 10 > $O/sim$m.json 2> $O/sim$m.err
+for m in 2 4 8; do
+  BENCH_DSGD_SIM=$m timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 16 > $O/sim$m.json 2> $O/sim$m.err
 done
+BENCH_DSGD_SIM=8 timeout 900 python bench.py --config y4 --no-cpu-baseline --no-e2e --steps 6 > $O/sim8_y4.json 2> $O/sim8_y4.err
