@@ -158,3 +158,17 @@ def test_block_orders_groups_pad_per_group():
     assert bo.round_start == [0, 7, 16, 32, 48] and bo.round_end == [7, 12, 16, 40]
     assert bo.group_start == [0, 16, 32, 48] and bo.group_end == [12, 16, 40]
     assert bo.total == 48
+
+
+def test_hot_row_concurrency_rule():
+    """dsgd_fused.hot_row_concurrency: rho = M for every mode a full-grid rank
+    keeps at least one sample in flight per row of (NF: the two small modes;
+    the 480K-row mode too at M = 8), 1 for small tensors (the launcher's
+    Hogwild cap keeps one CTA in flight); with a grid divided by M, rho = 1."""
+    from paper_2204_07104_b200.dsgd_fused import hot_row_concurrency
+
+    nf, n = (480189, 17770, 2182), 99_072_112
+    np.testing.assert_allclose(hot_row_concurrency(nf, 2, 1, n, n // 2), [1.0, 2.0, 2.0])
+    np.testing.assert_allclose(hot_row_concurrency(nf, 8, 1, n, n // 8), [8.0, 8.0, 8.0])
+    np.testing.assert_allclose(hot_row_concurrency(nf, 8, 8, n, n // 8), [1.0, 1.0, 1.0], rtol=0.01)
+    np.testing.assert_allclose(hot_row_concurrency((3000, 2800, 2600), 2, 1, 2400, 1300), [1.0, 1.0, 1.0])
