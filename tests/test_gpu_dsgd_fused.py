@@ -243,3 +243,67 @@ def test_sub_blocked_ranks_use_reference_block_orders(dims, J, W):
     init, _ = O.pack(model.factors)
     assert not np.allclose(want, init)
     np.testing.assert_allclose(got, want, rtol=5e-3, atol=5e-4 * np.abs(want).max())
+
+
+def _train_worker(rank, world, port, out, W, cap):
+    import os
+
+    import torch.distributed as td
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2204_07104_b200 import DatasetSplit, ModelConfig, SparseTensorCoo, TrainConfig, init_model, train
+
+        idx, vals, dims = _rows_once()
+        model = init_model(dims, ModelConfig((16,) * 3, 16, 1.0, seed=1))
+        t = SparseTensorCoo(dims, idx, vals)
+        rows = train(model, DatasetSplit(t, SparseTensorCoo(dims, idx[:300], vals[:300])),
+                     TrainConfig(epochs=2, workers=W, seed=1, alpha_a=0.003, update_mode="hogwild",
+                                 core_batch_cap=cap))
+        np.savez(os.path.join(out, f"r{rank}.npz"), *model.factors, *model.core_factors,
+                 rmse=np.array([r.test_rmse for r in rows]))
+        td.barrier()
+    finally:
+        td.destroy_process_group()
+
+
+def _rows_once():
+    rng = np.random.default_rng(13)
+    dims, nnz = (3000, 2800, 2600), 2400
+    idx = np.stack([rng.permutation(d)[:nnz] for d in dims], axis=1)
+    return idx, rng.normal(2.0, 1.0, nnz), dims
+
+
+def test_two_processes_public_train_sub_blocked_with_core_batches(tmp_path):
+    """The public train() over two processes (gloo; FusedDistRunner through
+    dist.train_distributed) with W = 4 blocks per mode (two per rank's slab)
+    and a core batch smaller than the tensor (drawn by one rank per epoch and
+    broadcast): both ranks end with the same model, equal to the reference's
+    4-worker run at TF32 tolerance (every row used by one entry only, so the
+    Hogwild order cannot matter)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    W, cap = 4, 1000
+    mp.get_context("spawn")
+    mp.spawn(_train_worker, args=(2, port, str(tmp_path), W, cap), nprocs=2, join=True)
+    got = [np.load(tmp_path / f"r{r}.npz") for r in range(2)]
+    idx, vals, dims = _rows_once()
+    from paper_2204_07104_b200 import ModelConfig, init_model
+
+    model = init_model(dims, ModelConfig((16,) * 3, 16, 1.0, seed=1))
+    fs = [a.copy() for a in model.factors]
+    bs = [b.copy() for b in model.core_factors]
+    rows = O.train(fs, bs, idx, vals, idx[:300], vals[:300], epochs=2, workers=W, seed=1, alpha_a=0.003,
+                   core_batch_cap=cap, dims=tuple(dims))
+    for i in range(6):
+        np.testing.assert_array_equal(got[0][f"arr_{i}"], got[1][f"arr_{i}"])
+    for i, want in enumerate(fs + bs):
+        np.testing.assert_allclose(got[0][f"arr_{i}"], want, rtol=5e-3, atol=5e-4 * np.abs(want).max())
+    np.testing.assert_allclose(got[0]["rmse"], [r["test_rmse"] for r in rows], rtol=5e-3)
