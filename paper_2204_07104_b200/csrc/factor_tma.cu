@@ -1023,7 +1023,10 @@ static int launch_tma(const int* rec, int rw, const int* visit, long long n_visi
   }
   const long long tiles = (n_visit + 127) / 128;
   // persistent grid minus the CTA slots left to the side-stream samplers
-  int slots = (N == 3 && J >= 16) ? 16 : 148;
+  // (order 3, J = 16: 32 slots, measured on the final code over 16 / 24 / 32 /
+  // 40 / 48 / 64 / 148: NF epoch 9.30 / 9.16 / 9.06 / 9.11 / 9.13 / 9.15 /
+  // 9.56 ms -- the samplers beside the pass gain more than the pass loses)
+  int slots = (N == 3 && J >= 16) ? 32 : 148;
   if (const char* e = getenv("SPTK_SAMPLER_SLOTS")) slots = atoi(e);
   long long blocks = 148LL * per_sm - (per_sm >= 2 ? slots : 0);
   if (const char* e = getenv("SPTK_TC_GRID")) blocks = atoll(e);

@@ -58,7 +58,7 @@ def fused_supported(model, config, nnz: int | None = None) -> bool:
             and (model.order, J) in ((3, 16), (4, 16), (3, 8), (6, 8)))
 
 
-FULL_GRID = 576  # the TMA kernel's single-GPU grid at J = 16 (4 CTAs x 148 SMs - 16 sampler slots)
+FULL_GRID = 560  # the TMA kernel's single-GPU grid at J = 16 (4 CTAs x 148 SMs - 32 sampler slots)
 
 
 def hot_row_concurrency(dims, m: int, div: int, nnz: int, n_rank: int) -> np.ndarray:
