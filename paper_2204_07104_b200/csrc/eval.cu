@@ -118,96 +118,87 @@ __device__ __forceinline__ void eval_block_sums(double sq, double ab, double* su
   }
 }
 
-// Uniform ranks (J_n = R for every mode, fp32): a thread scores two entries
-// (e and e + stride) at a time, their factor rows read as float4 loads, B(n)
-// from shared memory as float4 broadcasts that each feed eight FMAs.  The
+// Uniform ranks (J_n = R for every mode, fp32): a thread scores E entries
+// (e, e + stride, ...) at a time, their factor rows read as float4 loads, B(n)
+// from shared memory as float4 broadcasts that each feed 4E FMAs.  The
 // one-entry version (four FMAs per broadcast) was bound by those broadcasts:
-// NF train + test RMSE 7.45 -> 5.45 ms per epoch (ncu); staging the rows
-// through shared memory instead made it slower (8.28 ms).
-template <int N, int J, int RW>
-__global__ void __launch_bounds__(256, 2) eval_pair_kernel(const int* __restrict__ rec, long long m,
-                                                        const float* __restrict__ fac,
-                                                        const float* __restrict__ cor, ModelDesc md,
-                                                        float* __restrict__ pred_out, double* __restrict__ sums) {
+// NF train + test RMSE 7.45 -> 5.45 ms per epoch at E = 2, 5.06 at E = 4
+// (ncu); staging the rows through shared memory instead made it slower.
+template <int N, int J, int RW, int E, int MINB>
+__global__ void __launch_bounds__(256, MINB) eval_pair_kernel(const int* __restrict__ rec, long long m,
+                                                           const float* __restrict__ fac,
+                                                           const float* __restrict__ cor, ModelDesc md,
+                                                           float* __restrict__ pred_out, double* __restrict__ sums) {
   __shared__ __align__(16) float Bs[N * J * J];
   for (int i = threadIdx.x; i < N * J * J; i += blockDim.x) Bs[i] = cor[i];
   __syncthreads();
   double sq = 0.0, ab = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m; e += 2 * stride) {
-    const long long e2 = e + stride;
-    const bool ok2 = e2 < m;
-    int wa[8], wb[8];
-    {
-      const int4 a0 = __ldg(reinterpret_cast<const int4*>(rec + e * RW));
-      const int4 b0 = ok2 ? __ldg(reinterpret_cast<const int4*>(rec + e2 * RW)) : a0;
-      wa[0] = a0.x, wa[1] = a0.y, wa[2] = a0.z, wa[3] = a0.w;
-      wb[0] = b0.x, wb[1] = b0.y, wb[2] = b0.z, wb[3] = b0.w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m; e += E * stride) {
+    int w[E][8];
+    bool ok[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const long long ek = e + k * stride;
+      ok[k] = ek < m;
+      const long long ee = ok[k] ? ek : e;
+      const int4 a0 = __ldg(reinterpret_cast<const int4*>(rec + ee * RW));
+      w[k][0] = a0.x, w[k][1] = a0.y, w[k][2] = a0.z, w[k][3] = a0.w;
       if (RW >= 8) {
-        const int4 a1 = __ldg(reinterpret_cast<const int4*>(rec + e * RW) + 1);
-        const int4 b1 = ok2 ? __ldg(reinterpret_cast<const int4*>(rec + e2 * RW) + 1) : a1;
-        wa[4] = a1.x, wa[5] = a1.y, wa[6] = a1.z, wa[7] = a1.w;
-        wb[4] = b1.x, wb[5] = b1.y, wb[6] = b1.z, wb[7] = b1.w;
+        const int4 a1 = __ldg(reinterpret_cast<const int4*>(rec + ee * RW) + 1);
+        w[k][4] = a1.x, w[k][5] = a1.y, w[k][6] = a1.z, w[k][7] = a1.w;
       }
     }
-    float pa[J], pb[J];
+    float p[E][J];
 #pragma unroll
     for (int n = 0; n < N; ++n) {
-      const float4* sa = reinterpret_cast<const float4*>(fac + md.foff[n] + (long long)wa[n] * J);
-      const float4* sb = reinterpret_cast<const float4*>(fac + md.foff[n] + (long long)wb[n] * J);
-      float4 ra[J / 4], rb[J / 4];
+      float4 rr[E][J / 4];
 #pragma unroll
-      for (int q = 0; q < J / 4; ++q) {
-        ra[q] = __ldg(sa + q);
-        rb[q] = __ldg(sb + q);
+      for (int k = 0; k < E; ++k) {
+        const float4* src = reinterpret_cast<const float4*>(fac + md.foff[n] + (long long)w[k][n] * J);
+#pragma unroll
+        for (int q = 0; q < J / 4; ++q) rr[k][q] = __ldg(src + q);
       }
-      float ca[J], cb[J];
+      float c[E][J];
 #pragma unroll
-      for (int r = 0; r < J; ++r) ca[r] = cb[r] = 0.f;
+      for (int k = 0; k < E; ++k)
+#pragma unroll
+        for (int r = 0; r < J; ++r) c[k][r] = 0.f;
 #pragma unroll
       for (int q = 0; q < J / 4; ++q) {
-        const float av[4] = {ra[q].x, ra[q].y, ra[q].z, ra[q].w};
-        const float bv[4] = {rb[q].x, rb[q].y, rb[q].z, rb[q].w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = 4 * q + u;
 #pragma unroll
           for (int r4 = 0; r4 < J / 4; ++r4) {
             const float4 b = *reinterpret_cast<const float4*>(Bs + (n * J + j) * J + 4 * r4);
-            ca[4 * r4] = fmaf(av[u], b.x, ca[4 * r4]);
-            ca[4 * r4 + 1] = fmaf(av[u], b.y, ca[4 * r4 + 1]);
-            ca[4 * r4 + 2] = fmaf(av[u], b.z, ca[4 * r4 + 2]);
-            ca[4 * r4 + 3] = fmaf(av[u], b.w, ca[4 * r4 + 3]);
-            cb[4 * r4] = fmaf(bv[u], b.x, cb[4 * r4]);
-            cb[4 * r4 + 1] = fmaf(bv[u], b.y, cb[4 * r4 + 1]);
-            cb[4 * r4 + 2] = fmaf(bv[u], b.z, cb[4 * r4 + 2]);
-            cb[4 * r4 + 3] = fmaf(bv[u], b.w, cb[4 * r4 + 3]);
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+              const float av = u == 0 ? rr[k][q].x : u == 1 ? rr[k][q].y : u == 2 ? rr[k][q].z : rr[k][q].w;
+              c[k][4 * r4] = fmaf(av, b.x, c[k][4 * r4]);
+              c[k][4 * r4 + 1] = fmaf(av, b.y, c[k][4 * r4 + 1]);
+              c[k][4 * r4 + 2] = fmaf(av, b.z, c[k][4 * r4 + 2]);
+              c[k][4 * r4 + 3] = fmaf(av, b.w, c[k][4 * r4 + 3]);
+            }
           }
         }
       }
 #pragma unroll
-      for (int r = 0; r < J; ++r) {
-        pa[r] = n == 0 ? ca[r] : pa[r] * ca[r];
-        pb[r] = n == 0 ? cb[r] : pb[r] * cb[r];
-      }
-    }
-    float xa = 0.f, xb = 0.f;
+      for (int k = 0; k < E; ++k)
 #pragma unroll
-    for (int r = 0; r < J; ++r) {
-      xa += pa[r];
-      xb += pb[r];
+        for (int r = 0; r < J; ++r) p[k][r] = n == 0 ? c[k][r] : p[k][r] * c[k][r];
     }
-    if (pred_out) {
-      pred_out[e] = xa;
-      if (ok2) pred_out[e2] = xb;
-    }
-    const double da = (double)__int_as_float(wa[N]) - (double)xa;
-    sq += da * da;
-    ab += fabs(da);
-    if (ok2) {
-      const double db = (double)__int_as_float(wb[N]) - (double)xb;
-      sq += db * db;
-      ab += fabs(db);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      float xh = 0.f;
+#pragma unroll
+      for (int r = 0; r < J; ++r) xh += p[k][r];
+      if (ok[k]) {
+        if (pred_out) pred_out[e + k * stride] = xh;
+        const double d = (double)__int_as_float(w[k][N]) - (double)xh;
+        sq += d * d;
+        ab += fabs(d);
+      }
     }
   }
   if (sums) eval_block_sums(sq, ab, sums);
@@ -219,7 +210,13 @@ static int launch_eval_uniform(const int* rec, long long m, const float* fac, co
   constexpr int RW = N <= 3 ? 4 : 8;
   long long blocks = (m + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  eval_pair_kernel<N, J, RW><<<(unsigned)blocks, 256, 0, s>>>(rec, m, fac, cor, md, pred_out, sums);
+  // entries per thread (measured at NF, order 3 / J = 16, train + test per
+  // epoch: 1 / 2 / 3 / 4 -> 7.45 / 5.45 / 5.6 / 5.06 ms; four need 255
+  // registers, one CTA per SM)
+  if constexpr (N == 3 && J == 16)
+    eval_pair_kernel<N, J, RW, 4, 1><<<(unsigned)blocks, 256, 0, s>>>(rec, m, fac, cor, md, pred_out, sums);
+  else
+    eval_pair_kernel<N, J, RW, 2, 2><<<(unsigned)blocks, 256, 0, s>>>(rec, m, fac, cor, md, pred_out, sums);
   SPTK_CHECK_LAUNCH();
   return 0;
 }
