@@ -10,13 +10,15 @@ multiplications), from the formulas below.  Same interface: a global
 
 from __future__ import annotations
 
+from dataclasses import dataclass
 
+
+@dataclass
 class MultiplyCounter:
-    """Accumulates scalar-multiplication counts while enabled."""
+    """Global tally of scalar multiplications; ``add`` is a no-op unless enabled."""
 
-    def __init__(self):
-        self.enabled = False
-        self.total = 0
+    enabled: bool = False
+    total: int = 0
 
     def add(self, n: int) -> None:
         if self.enabled:
@@ -30,22 +32,25 @@ counter = MultiplyCounter()
 
 
 class count_multiplies:
-    """Context manager that enables counting and exposes the tally."""
+    """``with count_multiplies() as c:`` enables the counter for the block
+    (blocks nest); ``c.so_far`` inside, ``c.total`` after it."""
 
-    def __enter__(self):
-        self._was_enabled = counter.enabled
-        self._start = counter.total
-        counter.enabled = True
-        return self
-
-    def __exit__(self, *exc):
-        counter.enabled = self._was_enabled
-        self.total = counter.total - self._start
-        return False
+    def __init__(self):
+        self._start, self._prev, self.total = 0, False, 0
 
     @property
     def so_far(self) -> int:
         return counter.total - self._start
+
+    def __enter__(self):
+        self._prev, counter.enabled = counter.enabled, True
+        self._start = counter.total
+        return self
+
+    def __exit__(self, *exc):
+        counter.enabled = self._prev
+        self.total = self.so_far
+        return False
 
 
 def factor_sample_multiplies(j_ranks, r_core: int) -> int:
