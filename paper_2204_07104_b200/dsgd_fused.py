@@ -172,6 +172,14 @@ class FusedState:
 
         div = int(os.environ.get("SPTK_DSGD_GRID_DIV", 1))
         self.grid = -div if div > 1 else 0
+        # 8-way and wider at order 3 / J = 16: one CTA slot per SM left to the
+        # rank's samplers (3 factor CTAs per SM; per-rank NF epoch at M = 8
+        # 1.715 -> 1.665 ms; at M = 2 / 4 the default 32 free slots are
+        # faster: 4.80 vs 5.12, 2.62 vs 2.65 ms).  rho keeps the full grid
+        # (the step rule errs on the damped side).
+        if (div == 1 and plan.m >= 8 and runner.order == 3 and int(runner.dm.jr[0]) == 16
+                and "SPTK_SAMPLER_SLOTS" not in os.environ):
+            self.grid = 148 * 3
         self.rho = hot_row_concurrency(plan.dims, plan.m, div, runner.part.nnz, self.total)
         if not runner.hot_step_env:
             runner.hot_step_scale = np.where(runner.hot, np.minimum(1.0, self.rho ** (-2.0 / 3.0)), 1.0)
